@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark: product-to-sum element fill, element matrices/s (FP64) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+
+One step = one pass of the fill (moment kernel + contraction kernel, every
+element matrix written to HBM) over one batch of the workload's elements with
+alpha already resident in HBM.  Workload: BASELINE.json configs[1] (C2: 4096
+elements, 3-component, order 6, N_s = 2, 14^3 points) unless --config says
+otherwise.  Under torchrun every rank fills its own element range (weak
+scaling, no collective on the data path); the time is the max over ranks.
+
+--impl reference times the CPU oracle port of the reference algorithm
+(oracle/, the reference itself only implements the 2-D Chebyshev case) on the
+host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n-elem", type=int, default=0, help="override elements per rank")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="elements of the CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=20170328)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 8:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU oracle baseline
+
+def cpu_baseline(cfg, sample: int, seed: int, threads: int):
+    from oracle import oracle as O
+    o = O.Oracle(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
+    alpha = o.alpha(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, seed, 0, sample)
+    import numpy as np
+    out = np.empty((sample, o.n_tot, o.n_tot))
+    t0 = time.perf_counter()
+    o.fill(alpha, threads=threads, out=out)
+    dt = time.perf_counter() - t0
+    return sample / dt, dt
+
+
+def run_reference(args, cfg):
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = args.cpu_sample or _default_cpu_sample(cfg)
+    for _ in range(max(0, args.warmup)):
+        cpu_baseline(cfg, max(1, sample // 4), args.seed, threads)
+    rates, times = [], []
+    for _ in range(args.steps):
+        r, dt = cpu_baseline(cfg, sample, args.seed, threads)
+        rates.append(r)
+        times.append(dt)
+    total = sum(times)
+    value = sample * len(times) / total
+    line = {
+        "impl": "reference", "metric": "element matrices/s (FP64)", "value": value,
+        "unit": "elem/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded alpha, BASELINE.json shapes)",
+        "config": {"workload": cfg.name, "n_comp": cfg.n_comp, "order": list(cfg.order),
+                   "n_terms": len(cfg.kinds), "nq": list(cfg.nq), "elements_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": "elem/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} {cfg.name} elements per step (moments + banded "
+                                   f"contraction, oracle/p2s_oracle.c, {threads} threads)"},
+        "e2e": {"value": value, "unit": "elem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _default_cpu_sample(cfg):
+    per = {"c1": 256, "c2": 64, "c3": 48, "c4": 48, "c5": 1}
+    return per.get(cfg.name, 16)
+
+
+# ---------------------------------------------------------------- B200 arm
+
+def run_b200(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1703_09619_b200 import capi
+    from paper_1703_09619_b200.configs import algorithmic_counts
+
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    distributed = world > 1
+    torch.cuda.set_device(local)
+    if distributed:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    E = args.n_elem or cfg.n_elem
+    ctx = capi.Context(**cfg.problem(), device=local)
+    st = torch.cuda.current_stream()
+    sp = st.cuda_stream
+    n_tot = ctx.n_tot
+    alpha = torch.empty((E, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")
+    ctx.alpha_generate(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, args.seed, rank * E, E, alpha, sp)
+    M = torch.empty((E, n_tot, n_tot), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        ctx.fill(alpha, M, n_tot, E, sp)
+    torch.cuda.synchronize()
+
+    ctx.set_profiling(True)
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(st)
+    for _ in range(args.steps):
+        ctx.fill(alpha, M, n_tot, E, sp)
+    ev1.record(st)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    stages = ctx.stage_times()
+    ctx.set_profiling(False)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if distributed:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * E * args.steps / (ms_max / 1e3)
+
+    # checksum outside the timed region (guards against skipped work)
+    chk = float(M[:, :8, :8].abs().sum().item())
+
+    # ---- e2e through the host-buffer entry point (pinned buffers)
+    e2e = None
+    if not args.no_e2e:
+        E2 = min(E, 1024)
+        h_alpha = torch.empty((E2, ctx.alpha_per_elem), dtype=torch.float64, pin_memory=True)
+        h_alpha.copy_(alpha[:E2])
+        h_M = torch.empty((E2, n_tot, n_tot), dtype=torch.float64, pin_memory=True)
+        ctx.fill_host(h_alpha, h_M, n_tot, E2)  # warm-up
+        reps = 3
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            ctx.fill_host(h_alpha, h_M, n_tot, E2)
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if distributed:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        e2e = {"value": world * E2 * reps / dt, "unit": "elem/s",
+               "h2d_bytes_per_step": E2 * ctx.alpha_per_elem * 8,
+               "d2h_bytes_per_step": E2 * n_tot * n_tot * 8,
+               "elements_per_step": E2, "timing": "wall clock around p2s_fill_host (pinned host buffers)"}
+        del h_alpha, h_M
+
+    if rank != 0:
+        if distributed:
+            dist.destroy_process_group()
+        return
+
+    counts = algorithmic_counts(cfg)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
+    # dominant kernel = contraction (HBM-write bound)
+    n_con = max(1, stages["n_contract"])
+    con_ms_avg = stages["ms_contract"] / n_con
+    elems_total = E * args.steps
+    bytes_per_launch = counts["bytes_con"] * elems_total / n_con
+    achieved = bytes_per_launch / (con_ms_avg / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(cfg.name)
+            if tr:
+                traffic = tr["dram_bytes_per_launch"] * (bytes_per_launch / tr["alg_bytes_per_launch"])
+    except Exception:
+        pass
+    mom_ms_avg = stages["ms_moments"] / max(1, stages["n_moments"])
+    line = {
+        "metric": "element matrices/s (FP64)",
+        "value": value,
+        "unit": "elem/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded alpha on device, BASELINE.json shapes)",
+        "config": {"workload": cfg.name, "n_comp": cfg.n_comp, "order": list(cfg.order),
+                   "kinds": ["PP/DD/DP/PD"[3 * k:3 * k + 2] if isinstance(k, int) else str(k)
+                             for k in cfg.kinds],
+                   "n_terms": len(cfg.kinds), "nq": list(cfg.nq), "elements_per_rank": E,
+                   "n_tot": n_tot, "parallelism": f"element-partitioned x{world}, no collective",
+                   "l2": f"outputs {E * n_tot * n_tot * 8 / 1e9:.1f} GB per step >> 126 MB L2"},
+        "clocks": clk,
+        "gpu_launches": stages["n_moments"] + stages["n_contract"],
+        "stage_ms_per_step": {"moments": stages["ms_moments"] / args.steps,
+                              "contract": stages["ms_contract"] / args.steps},
+        "roofline": {"kernel": "contract_kernel", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "alg_bytes_per_elem": counts["bytes_con"],
+                     "moment_kernel": {"bound": "fp64/hbm", "avg_launch_ms": mom_ms_avg,
+                                       "alg_bytes_per_elem": counts["bytes_mom"],
+                                       "alg_flop_per_elem": counts["flop_mom"],
+                                       "achieved_gbs": counts["bytes_mom"] * elems_total /
+                                       max(1e-9, stages["ms_moments"] / 1e3) / 1e9,
+                                       "achieved_tflops": counts["flop_mom"] * elems_total /
+                                       max(1e-9, stages["ms_moments"] / 1e3) / 1e12}},
+        "checksum": chk,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sample = args.cpu_sample or _default_cpu_sample(cfg)
+        rate, dt = cpu_baseline(cfg, sample, args.seed, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": "elem/s", "cores": threads, "kind": "port",
+                                "sample": f"{sample} {cfg.name} elements (moments + banded contraction,"
+                                          f" oracle/p2s_oracle.c), {dt:.1f} s"}
+    print(json.dumps(line), flush=True)
+    if distributed:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from paper_1703_09619_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,145 @@
+/*
+ * p2s_b200.h -- C-ABI of the B200-native product-to-sum element fill.
+ *
+ * Drop-in boundary for the reference's fill path (/root/reference/proj):
+ *
+ *   reference (C++, include/chebfem/assembly.hpp)        this ABI
+ *   ---------------------------------------------------  ------------------------
+ *   poly_table / FlatTable / product_to_sum tables,       p2s_create
+ *     rebuilt per element (assembly.cpp:41-49,110-117,
+ *     332-352; chebyshev.cpp:156-178)
+ *   compute_kernel_tables(mesh, e, orders, nq)            p2s_moments
+ *     (assembly.hpp:52; assembly.cpp:276-314)
+ *   assemble_p2s_element(kernels, orders)                 p2s_contract
+ *     (assembly.hpp:56; assembly.cpp:375-474)
+ *   fill_elements(mesh, orders, Backend::p2s, nq, thr)    p2s_fill (device buffers)
+ *     (assembly.hpp:82-83; assembly.cpp:654-700)          p2s_fill_host (host buffers)
+ *   C++ exceptions (std::invalid_argument,                p2s_status + p2s_last_error
+ *     GeometryError, std::logic_error)                      (include/p2s_b200.hpp maps
+ *                                                           them back to exceptions)
+ *
+ * Problem: the paper's general 3-D scheme (Eqs. (1)-(4)) with
+ * Legendre kernel polynomials.  n_comp field components share the orders
+ * N_u, N_v, N_w (basis P_0..P_{N-1} per direction); every ordered component
+ * pair (gi, gj) carries n_terms coupling factors alpha_s^{gi gj}; term s uses,
+ * per direction, the operator pair kind (P2S_PP: P_m1 P_m2, P2S_DD: P'_m1
+ * P'_m2, P2S_DP: P'_m1 P_m2, P2S_PD: P_m1 P'_m2).
+ *
+ * Layouts (FP64, all row-major, u fastest in alpha, p fastest in M):
+ *   alpha  [E][P][S][nq_w][nq_v][nq_u]          P = n_comp^2, pair = gi*n_comp+gj
+ *          values of alpha_s at the Gauss-Legendre nodes; the quadrature
+ *          weights are NOT included (they live in the kernel tables).
+ *   I      [E][P] blocks of sizes.moments_per_pair doubles; term s of a pair
+ *          starts at sizes.moment_offset[s] and holds [K_u][K_v][K_w].
+ *   M      E matrices of n_tot x n_tot with leading dimension ld_M (>= n_tot),
+ *          matrix e at M + e * n_tot * ld_M;
+ *          row = gi*Nu*Nv*Nw + (m1*Nv + n1)*Nw + p1 (test),
+ *          col = gj*Nu*Nv*Nw + (m2*Nv + n2)*Nw + p2 (trial).
+ *
+ * Ownership: the caller owns alpha / I / M buffers; the context owns the
+ * uploaded tables and its scratch and is immutable after p2s_create (the
+ * profiling switch aside).  One context per device; calls on distinct streams
+ * may run concurrently except p2s_fill / p2s_fill_host, which use context
+ * scratch and must not overlap on one context.
+ *
+ * There is no CPU fallback: every compute entry point runs sm_100a kernels
+ * and fails with P2S_CUDA_ERROR when no B200 is present.
+ */
+#ifndef P2S_B200_H
+#define P2S_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define P2S_MAX_TERMS 4
+
+typedef enum {
+  P2S_OK = 0,
+  P2S_INVALID_ARG = 1,        /* std::invalid_argument in the reference      */
+  P2S_CUDA_ERROR = 2,         /* device / driver failure                      */
+  P2S_UNSUPPORTED_SHAPE = 3,  /* no kernel instantiation for these orders    */
+  P2S_GEOMETRY_ERROR = 4      /* GeometryError (J <= 0) in the reference      */
+} p2s_status;
+
+enum { P2S_PP = 0, P2S_DD = 1, P2S_DP = 2, P2S_PD = 3 };
+
+/* synthetic coupling-factor families of BASELINE.json's configs */
+enum { P2S_ALPHA_SINE = 0, P2S_ALPHA_JACOBIAN = 1, P2S_ALPHA_EXPSIN = 2 };
+
+typedef struct {
+  int32_t n_comp;                        /* 1 or 3                              */
+  int32_t order[3];                      /* N_u, N_v, N_w (>= 1)                */
+  int32_t n_terms;                       /* N_s (1 .. P2S_MAX_TERMS)            */
+  int32_t kind[P2S_MAX_TERMS][3];        /* P2S_PP / DD / DP / PD               */
+  int32_t nq[3];                         /* Gauss-Legendre points per direction */
+} p2s_problem;
+
+typedef struct {
+  int64_t alpha_per_elem;                /* doubles                              */
+  int64_t moments_per_elem;              /* doubles (= n_pairs * per_pair)       */
+  int64_t moments_per_pair;              /* doubles, padded to a multiple of 4   */
+  int64_t moment_offset[P2S_MAX_TERMS];  /* doubles, within a pair block         */
+  int32_t n_tot;                         /* matrix dimension                     */
+  int32_t n_pairs;                       /* n_comp^2                             */
+  int32_t K[P2S_MAX_TERMS][3];           /* kernel polynomial counts             */
+} p2s_sizes;
+
+typedef struct p2s_ctx p2s_ctx;
+
+/* Builds and uploads the Gauss-Legendre rules, weighted Legendre kernel tables
+ * and product-to-sum coefficient tables once. */
+p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out);
+void p2s_destroy(p2s_ctx* ctx);
+
+p2s_status p2s_get_sizes(const p2s_ctx* ctx, p2s_sizes* out);
+
+/* Moment stage:  I_s[k1][k2][k3] = sum_q w_q alpha_s(q) P_k1(u) P_k2(v) P_k3(w). */
+p2s_status p2s_moments(p2s_ctx* ctx, const double* d_alpha, double* d_I, int64_t n_elem,
+                       void* stream);
+
+/* Contraction stage:  M = sum_s sum_k C_u C_v C_w I_s, every entry written once. */
+p2s_status p2s_contract(p2s_ctx* ctx, const double* d_I, double* d_M, int64_t ld_M,
+                        int64_t n_elem, void* stream);
+
+/* Both stages over a batch, moments staged in context scratch (chunked so the
+ * scratch stays L2-resident). */
+p2s_status p2s_fill(p2s_ctx* ctx, const double* d_alpha, double* d_M, int64_t ld_M,
+                    int64_t n_elem, void* stream);
+
+/* Host buffers in and out; H2D, fill and D2H pipelined over chunks on the
+ * context's streams.  Returns after the last matrix is in h_M. */
+p2s_status p2s_fill_host(p2s_ctx* ctx, const double* h_alpha, double* h_M, int64_t ld_M,
+                         int64_t n_elem);
+
+/* Seeded synthetic coupling factor (benchmark harness input, not part of the
+ * fill): elements e0 .. e0+n_elem-1 into d_alpha.  lo/hi: frequency range. */
+p2s_status p2s_alpha_generate(p2s_ctx* ctx, int alpha_kind, double lo, double hi,
+                              uint64_t seed, int64_t e0, int64_t n_elem, double* d_alpha,
+                              void* stream);
+
+/* Host copies of the uploaded tables: phi = w_q P_k(x_q) as [K][nq],
+ * coef = [N][N][K]; nodes/weights [nq].  Any pointer may be NULL. */
+p2s_status p2s_get_tables(const p2s_ctx* ctx, int term, int dir, double* phi, double* coef,
+                          double* nodes, double* weights);
+
+/* Stage timing on the launching stream (CUDA events around every launch);
+ * accumulated until the next p2s_set_profiling call. */
+p2s_status p2s_set_profiling(p2s_ctx* ctx, int enable);
+p2s_status p2s_get_stage_times(p2s_ctx* ctx, double* ms_moments, double* ms_contract,
+                               int64_t* n_moment_launches, int64_t* n_contract_launches);
+
+/* 1 if the orders / kinds have a compiled kernel instantiation. */
+int p2s_shape_supported(const p2s_problem* spec);
+
+/* Thread-local description of the last failure on this thread. */
+const char* p2s_last_error(void);
+
+const char* p2s_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,227 @@
+"""ctypes binding of the C-ABI in include/p2s_b200.h (libp2s_b200.so).
+
+The product path: every compute call below launches the sm_100a kernels of
+libp2s_b200.so.  There is no CPU fallback -- if the library is missing this
+module raises at import of the library, and on a machine without a B200 the
+context constructor raises P2SError(P2S_CUDA_ERROR).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libp2s_b200.so")
+
+MAX_TERMS = 4
+PP, DD, DP, PD = 0, 1, 2, 3
+ALPHA_SINE, ALPHA_JACOBIAN, ALPHA_EXPSIN = 0, 1, 2
+
+OK, INVALID_ARG, CUDA_ERROR, UNSUPPORTED_SHAPE, GEOMETRY_ERROR = 0, 1, 2, 3, 4
+_STATUS = {0: "P2S_OK", 1: "P2S_INVALID_ARG", 2: "P2S_CUDA_ERROR", 3: "P2S_UNSUPPORTED_SHAPE",
+           4: "P2S_GEOMETRY_ERROR"}
+
+# every symbol include/p2s_b200.h declares
+EXPORTS = ("p2s_create", "p2s_destroy", "p2s_get_sizes", "p2s_moments", "p2s_contract",
+           "p2s_fill", "p2s_fill_host", "p2s_alpha_generate", "p2s_get_tables",
+           "p2s_set_profiling", "p2s_get_stage_times", "p2s_shape_supported", "p2s_last_error",
+           "p2s_version")
+
+
+class P2SError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class InvalidArgument(P2SError, ValueError):
+    """std::invalid_argument in the reference (assembly.cpp:20, 376-378)."""
+
+
+class UnsupportedShape(P2SError):
+    pass
+
+
+class Problem(C.Structure):
+    _fields_ = [
+        ("n_comp", C.c_int32),
+        ("order", C.c_int32 * 3),
+        ("n_terms", C.c_int32),
+        ("kind", (C.c_int32 * 3) * MAX_TERMS),
+        ("nq", C.c_int32 * 3),
+    ]
+
+
+class Sizes(C.Structure):
+    _fields_ = [
+        ("alpha_per_elem", C.c_int64),
+        ("moments_per_elem", C.c_int64),
+        ("moments_per_pair", C.c_int64),
+        ("moment_offset", C.c_int64 * MAX_TERMS),
+        ("n_tot", C.c_int32),
+        ("n_pairs", C.c_int32),
+        ("K", (C.c_int32 * 3) * MAX_TERMS),
+    ]
+
+
+def build(force: bool = False) -> str:
+    """Compile libp2s_b200.so (nvcc, sm_100a) in-tree."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-C", os.path.join(_HERE, "csrc"), "-s"], check=True)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(the fill has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, dp = C.c_void_p, C.c_int64, C.POINTER(C.c_double)
+        L.p2s_create.argtypes = [C.POINTER(Problem), C.c_int, C.POINTER(vp)]
+        L.p2s_destroy.argtypes = [vp]
+        L.p2s_destroy.restype = None
+        L.p2s_get_sizes.argtypes = [vp, C.POINTER(Sizes)]
+        L.p2s_moments.argtypes = [vp, vp, vp, i64, vp]
+        L.p2s_contract.argtypes = [vp, vp, vp, i64, i64, vp]
+        L.p2s_fill.argtypes = [vp, vp, vp, i64, i64, vp]
+        L.p2s_fill_host.argtypes = [vp, vp, vp, i64, i64]
+        L.p2s_alpha_generate.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_uint64, i64, i64,
+                                         vp, vp]
+        L.p2s_get_tables.argtypes = [vp, C.c_int, C.c_int, dp, dp, dp, dp]
+        L.p2s_set_profiling.argtypes = [vp, C.c_int]
+        L.p2s_get_stage_times.argtypes = [vp, dp, dp, C.POINTER(i64), C.POINTER(i64)]
+        L.p2s_shape_supported.argtypes = [C.POINTER(Problem)]
+        L.p2s_shape_supported.restype = C.c_int
+        L.p2s_last_error.restype = C.c_char_p
+        L.p2s_version.restype = C.c_char_p
+        for f in EXPORTS:
+            if f not in ("p2s_destroy", "p2s_shape_supported", "p2s_last_error", "p2s_version"):
+                getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != OK:
+        msg = lib().p2s_last_error().decode()
+        if status == INVALID_ARG:
+            raise InvalidArgument(status, msg)
+        if status == UNSUPPORTED_SHAPE:
+            raise UnsupportedShape(status, msg)
+        raise P2SError(status, msg)
+
+
+def make_problem(n_comp, order, kinds, nq) -> Problem:
+    pb = Problem()
+    pb.n_comp = n_comp
+    for d in range(3):
+        pb.order[d] = order[d]
+        pb.nq[d] = nq[d]
+    pb.n_terms = len(kinds)
+    for s, k in enumerate(kinds):
+        kk = tuple(k) if isinstance(k, (tuple, list)) else (k, k, k)
+        for d in range(3):
+            pb.kind[s][d] = kk[d]
+    return pb
+
+
+def shape_supported(n_comp, order, kinds, nq) -> bool:
+    return bool(lib().p2s_shape_supported(C.byref(make_problem(n_comp, order, kinds, nq))))
+
+
+def _ptr(t) -> int:
+    """Raw pointer of a torch tensor / int."""
+    if t is None:
+        return 0
+    if isinstance(t, int):
+        return t
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    if hasattr(t, "ctypes"):
+        return t.ctypes.data
+    raise TypeError(type(t))
+
+
+class Context:
+    """One p2s_ctx (tables uploaded once) on one device."""
+
+    def __init__(self, n_comp, order, kinds, nq, device: int = 0):
+        self.problem = make_problem(n_comp, order, kinds, nq)
+        self.n_comp = n_comp
+        self.order = tuple(order)
+        self.kinds = [tuple(k) if isinstance(k, (tuple, list)) else (k, k, k) for k in kinds]
+        self.nq = tuple(nq)
+        self.device = device
+        h = C.c_void_p()
+        _check(lib().p2s_create(C.byref(self.problem), device, C.byref(h)))
+        self.h = h
+        sz = Sizes()
+        _check(lib().p2s_get_sizes(self.h, C.byref(sz)))
+        self.sizes = sz
+        self.alpha_per_elem = sz.alpha_per_elem
+        self.moments_per_elem = sz.moments_per_elem
+        self.moments_per_pair = sz.moments_per_pair
+        self.n_tot = sz.n_tot
+        self.n_pairs = sz.n_pairs
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().p2s_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def K(self, term, d):
+        return self.sizes.K[term][d]
+
+    def moment_offset(self, pair, term):
+        return pair * self.moments_per_pair + self.sizes.moment_offset[term]
+
+    # ---- stages (device pointers; stream = raw cudaStream_t or 0)
+    def moments(self, d_alpha, d_I, n_elem, stream=0):
+        _check(lib().p2s_moments(self.h, _ptr(d_alpha), _ptr(d_I), n_elem, _ptr(stream)))
+
+    def contract(self, d_I, d_M, ld_M, n_elem, stream=0):
+        _check(lib().p2s_contract(self.h, _ptr(d_I), _ptr(d_M), ld_M, n_elem, _ptr(stream)))
+
+    def fill(self, d_alpha, d_M, ld_M, n_elem, stream=0):
+        _check(lib().p2s_fill(self.h, _ptr(d_alpha), _ptr(d_M), ld_M, n_elem, _ptr(stream)))
+
+    def fill_host(self, h_alpha, h_M, ld_M, n_elem):
+        _check(lib().p2s_fill_host(self.h, _ptr(h_alpha), _ptr(h_M), ld_M, n_elem))
+
+    def alpha_generate(self, kind, lo, hi, seed, e0, n_elem, d_alpha, stream=0):
+        _check(lib().p2s_alpha_generate(self.h, kind, lo, hi, seed, e0, n_elem, _ptr(d_alpha),
+                                        _ptr(stream)))
+
+    def tables(self, term, d):
+        import numpy as np
+        K, nq, N = self.K(term, d), self.nq[d], self.order[d]
+        phi = np.zeros((K, nq))
+        coef = np.zeros((N, N, K))
+        x = np.zeros(nq)
+        w = np.zeros(nq)
+        dp = C.POINTER(C.c_double)
+        _check(lib().p2s_get_tables(self.h, term, d, phi.ctypes.data_as(dp), coef.ctypes.data_as(dp),
+                                    x.ctypes.data_as(dp), w.ctypes.data_as(dp)))
+        return phi, coef, x, w
+
+    def set_profiling(self, enable: bool):
+        _check(lib().p2s_set_profiling(self.h, int(enable)))
+
+    def stage_times(self):
+        a, b = C.c_double(), C.c_double()
+        na, nb = C.c_int64(), C.c_int64()
+        _check(lib().p2s_get_stage_times(self.h, C.byref(a), C.byref(b), C.byref(na), C.byref(nb)))
+        return {"ms_moments": a.value, "ms_contract": b.value, "n_moments": na.value,
+                "n_contract": nb.value}

@@ -1,0 +1,690 @@
+// p2s_capi.cu -- C-ABI (include/p2s_b200.h): context, kernel registry and the
+// element-batch scheduler.  The scheduler replaces fill_elements
+// (assembly.cpp:654-700): elements are processed in chunks whose moment
+// scratch stays L2-resident; p2s_fill_host pipelines H2D / fill / D2H over a
+// two-slot device ring on three streams.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/p2s_b200.h"
+#include "p2s_kernels.cuh"
+#include "p2s_tables.hpp"
+
+namespace p2s {
+cudaError_t launch_alpha(double* alpha, const double* const x[3], const int nq[3], int nc, int S,
+                         int kind, double lo, double hi, uint64_t seed, int64_t e0, int64_t n,
+                         int64_t per_elem, cudaStream_t stream);
+}
+
+namespace {
+
+thread_local std::string g_last_error;
+
+p2s_status fail(p2s_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+p2s_status cuda_fail(cudaError_t err, const char* where) {
+  return fail(P2S_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(err));
+}
+
+#define P2S_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t err__ = (call);                          \
+    if (err__ != cudaSuccess) return cuda_fail(err__, #call); \
+  } while (0)
+
+using namespace p2s;
+
+// ------------------------------------------------------------ contraction registry
+
+struct ContractArgs {
+  const double* I;
+  double* M;
+  int64_t ldM, n_tot, n_elem;
+  int nc, P, Nv, Nw, Nt;
+  int S;
+  int Kv[kMaxTerms], Kw[kMaxTerms], kind_v[kMaxTerms], kind_w[kMaxTerms];
+  int64_t mom_per_elem, mom_per_pair, mom_off[kMaxTerms];
+  const double* Cv[kMaxTerms];
+  const double* Cw[kMaxTerms];
+  const double* cu_packed;  // host, Cfg-packed
+};
+
+struct Plan {  // per-context launch geometry of the contraction
+  int G, NG, threads;
+  size_t smem;
+};
+
+using contract_fn = cudaError_t (*)(const ContractArgs&, const Plan&, cudaStream_t);
+
+template <class Cfg>
+cudaError_t launch_contract(const ContractArgs& a, const Plan& pl, cudaStream_t st) {
+  ContractParams<Cfg> p;
+  std::memset(&p, 0, sizeof(p));
+  p.I = a.I;
+  p.M = a.M;
+  p.ldM = a.ldM;
+  p.mat_stride = a.n_tot * a.ldM;
+  p.nc = a.nc;
+  p.P = a.P;
+  p.Nv = a.Nv;
+  p.Nw = a.Nw;
+  p.Nt = a.Nt;
+  p.G = pl.G;
+  p.NG = pl.NG;
+  p.mom_per_elem = a.mom_per_elem;
+  p.mom_per_pair = a.mom_per_pair;
+  p.i_doubles = static_cast<int>(a.mom_per_pair);
+  int ao = 0, co = 0;
+  for (int s = 0; s < Cfg::S; ++s) {
+    p.Kv[s] = a.Kv[s];
+    p.Kw[s] = a.Kw[s];
+    p.kind_v[s] = a.kind_v[s];
+    p.kind_w[s] = a.kind_w[s];
+    p.mom_off[s] = static_cast<int>(a.mom_off[s]);
+    p.a_off[s] = ao;
+    ao += pl.G * Cfg::K(s) * a.Nv * a.Kw[s];
+    p.cv_off[s] = co;
+    co += a.Nv * a.Nv * a.Kv[s];
+    p.cw_off[s] = co;
+    co += a.Nw * a.Nw * a.Kw[s];
+    p.Cv[s] = a.Cv[s];
+    p.Cw[s] = a.Cw[s];
+  }
+  p.a_doubles = (ao + 1) & ~1;
+  p.c_doubles = (co + 1) & ~1;
+  std::memcpy(p.cu, a.cu_packed, sizeof(double) * Cfg::CTOT);
+  const int64_t n_cta = a.n_elem * a.P * pl.NG;
+  p.n_cta = n_cta;
+  if (n_cta == 0) return cudaSuccess;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(contract_kernel<Cfg>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  contract_kernel<Cfg><<<static_cast<unsigned>(n_cta), pl.threads, pl.smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <class Cfg>
+std::vector<double> pack_cu(const std::vector<const std::vector<double>*>& dense) {
+  // dense[s] = [NU][NU][K_s]
+  std::vector<double> out(static_cast<size_t>(Cfg::CTOT), 0.0);
+  for (int s = 0; s < Cfg::S; ++s) {
+    const int K = Cfg::K(s), kd = Cfg::kind(s);
+    for (int a = 0; a < Cfg::NU; ++a)
+      for (int b = 0; b < Cfg::NU; ++b) {
+        const int lo = band_lo(kd, a, b), cnt = band_count(kd, a, b);
+        for (int j = 0; j < cnt; ++j)
+          out[static_cast<size_t>(Cfg::coff(s, a, b) + j)] =
+              (*dense[static_cast<size_t>(s)])[(static_cast<size_t>(a) * Cfg::NU + b) * K + lo + 2 * j];
+      }
+  }
+  return out;
+}
+
+struct RegEntry {
+  int NU, S;
+  int kinds[kMaxTerms];
+  contract_fn launch;
+  std::vector<double> (*pack)(const std::vector<const std::vector<double>*>&);
+  int ktot;
+};
+
+template <int NU, int... KINDS>
+RegEntry make_entry() {
+  using Cfg = UCfg<NU, KINDS...>;
+  RegEntry r{};
+  r.NU = NU;
+  r.S = Cfg::S;
+  const int ks[] = {KINDS...};
+  for (int s = 0; s < Cfg::S; ++s) r.kinds[s] = ks[s];
+  r.launch = &launch_contract<Cfg>;
+  r.pack = &pack_cu<Cfg>;
+  r.ktot = Cfg::KTOT;
+  return r;
+}
+
+// Compiled shapes: (N_u, u-kind of each term).  The v / w orders, kinds,
+// component count and quadrature sizes are runtime parameters.
+const std::vector<RegEntry>& registry() {
+  static const std::vector<RegEntry> reg = {
+      make_entry<1, PP>(),          make_entry<2, PP>(),      make_entry<3, PP>(),
+      make_entry<4, PP>(),          make_entry<5, PP>(),      make_entry<6, PP>(),
+      make_entry<8, PP>(),          make_entry<10, PP>(),
+      make_entry<2, PP, DD>(),      make_entry<3, PP, DD>(),  make_entry<4, PP, DD>(),
+      make_entry<5, PP, DD>(),      make_entry<6, PP, DD>(),  make_entry<8, PP, DD>(),
+      make_entry<10, PP, DD>(),
+      make_entry<3, DD>(),          make_entry<3, DP>(),      make_entry<3, PD>(),
+      make_entry<4, DP, PD>(),      make_entry<3, PP, DP>(),  make_entry<4, PP, DD, DP, PD>(),
+  };
+  return reg;
+}
+
+const RegEntry* find_entry(const p2s_problem& pb) {
+  for (const RegEntry& r : registry()) {
+    if (r.NU != pb.order[0] || r.S != pb.n_terms) continue;
+    bool ok = true;
+    for (int s = 0; s < r.S; ++s) ok = ok && (r.kinds[s] == pb.kind[s][0]);
+    if (ok) return &r;
+  }
+  return nullptr;
+}
+
+// ------------------------------------------------------------ moment launch
+
+template <int KMAX>
+cudaError_t launch_moments_k(const MomentParams& p, size_t smem, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(moments_kernel<KMAX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  moments_kernel<KMAX><<<static_cast<unsigned>(p.n_units), 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moments(int kmax, const MomentParams& p, size_t smem, cudaStream_t st) {
+  if (p.n_units == 0) return cudaSuccess;
+  switch (kmax) {
+    case 8: return launch_moments_k<8>(p, smem, st);
+    case 12: return launch_moments_k<12>(p, smem, st);
+    case 16: return launch_moments_k<16>(p, smem, st);
+    case 20: return launch_moments_k<20>(p, smem, st);
+    case 24: return launch_moments_k<24>(p, smem, st);
+    default: return launch_moments_k<32>(p, smem, st);
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ context
+
+struct p2s_ctx {
+  p2s_problem pb{};
+  int device = 0;
+  p2s_sizes sz{};
+  std::vector<double> x[3], w[3];
+  std::vector<double> phi[kMaxTerms][3];   // [K][nq]
+  std::vector<double> coef[kMaxTerms][3];  // [N][N][K]
+  int Kpad[kMaxTerms][3]{};
+  double* d_phiT[kMaxTerms][3]{};          // [nq][Kpad]
+  double* d_coef[kMaxTerms][3]{};          // [N][N][K]
+  double* d_x[3]{};
+  const RegEntry* entry = nullptr;
+  std::vector<double> cu_packed;
+  Plan plan{};
+  int kmax = 8;
+  size_t mom_smem = 0;
+  int S2 = 1, S3 = 1;
+  // scheduler
+  int64_t chunk = 1;
+  double* d_scratch = nullptr;             // chunk * moments_per_elem
+  // host pipeline
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  int64_t host_chunk = 0;
+  double* d_ring_alpha[2]{};
+  double* d_ring_M[2]{};
+  cudaEvent_t ev_h2d[2]{}, ev_comp[2]{}, ev_d2h[2]{};
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_mom, ev_con;
+  double ms_mom = 0.0, ms_con = 0.0;
+  int64_t n_mom = 0, n_con = 0;
+};
+
+namespace {
+
+cudaEvent_t take_event(p2s_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void harvest(p2s_ctx* c) {
+  for (auto& pr : c->ev_mom) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pr.first, pr.second);
+    c->ms_mom += ms;
+    c->ev_pool.push_back(pr.first);
+    c->ev_pool.push_back(pr.second);
+  }
+  for (auto& pr : c->ev_con) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pr.first, pr.second);
+    c->ms_con += ms;
+    c->ev_pool.push_back(pr.first);
+    c->ev_pool.push_back(pr.second);
+  }
+  c->ev_mom.clear();
+  c->ev_con.clear();
+}
+
+p2s_status validate(const p2s_problem* pb) {
+  if (!pb) return fail(P2S_INVALID_ARG, "p2s_create: null problem");
+  if (pb->n_comp < 1 || pb->n_comp > 3) return fail(P2S_INVALID_ARG, "n_comp must be 1..3");
+  if (pb->n_terms < 1 || pb->n_terms > P2S_MAX_TERMS)
+    return fail(P2S_INVALID_ARG, "n_terms must be 1..4");
+  for (int d = 0; d < 3; ++d) {
+    if (pb->order[d] < 1 || pb->order[d] > 32) return fail(P2S_INVALID_ARG, "order must be 1..32");
+    if (pb->nq[d] < 1 || pb->nq[d] > 64) return fail(P2S_INVALID_ARG, "nq must be 1..64");
+  }
+  for (int s = 0; s < pb->n_terms; ++s)
+    for (int d = 0; d < 3; ++d)
+      if (pb->kind[s][d] < 0 || pb->kind[s][d] > 3) return fail(P2S_INVALID_ARG, "bad kind");
+  return P2S_OK;
+}
+
+p2s_status run_moments(p2s_ctx* c, const double* alpha, double* I, int64_t n, cudaStream_t st) {
+  MomentParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.alpha = alpha;
+  p.I = I;
+  p.P = c->sz.n_pairs;
+  p.S = c->pb.n_terms;
+  p.n_units = n * p.P * p.S;
+  for (int d = 0; d < 3; ++d) p.nq[d] = c->pb.nq[d];
+  for (int s = 0; s < p.S; ++s)
+    for (int d = 0; d < 3; ++d) {
+      p.K[s][d] = c->sz.K[s][d];
+      p.Kpad[s][d] = c->Kpad[s][d];
+      p.phiT[s][d] = c->d_phiT[s][d];
+    }
+  p.mom_per_elem = c->sz.moments_per_elem;
+  p.mom_per_pair = c->sz.moments_per_pair;
+  for (int s = 0; s < p.S; ++s) p.mom_off[s] = c->sz.moment_offset[s];
+  p.S2 = c->S2;
+  p.S3 = c->S3;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->prof) {
+    e0 = take_event(c);
+    e1 = take_event(c);
+    cudaEventRecord(e0, st);
+  }
+  cudaError_t err = launch_moments(c->kmax, p, c->mom_smem, st);
+  if (err != cudaSuccess) return cuda_fail(err, "moments_kernel launch");
+  if (c->prof) {
+    cudaEventRecord(e1, st);
+    c->ev_mom.emplace_back(e0, e1);
+    ++c->n_mom;
+  }
+  return P2S_OK;
+}
+
+p2s_status run_contract(p2s_ctx* c, const double* I, double* M, int64_t ldM, int64_t n,
+                        cudaStream_t st) {
+  ContractArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.I = I;
+  a.M = M;
+  a.ldM = ldM;
+  a.n_tot = c->sz.n_tot;
+  a.n_elem = n;
+  a.nc = c->pb.n_comp;
+  a.P = c->sz.n_pairs;
+  a.Nv = c->pb.order[1];
+  a.Nw = c->pb.order[2];
+  a.Nt = c->pb.order[0] * c->pb.order[1] * c->pb.order[2];
+  a.S = c->pb.n_terms;
+  for (int s = 0; s < a.S; ++s) {
+    a.Kv[s] = c->sz.K[s][1];
+    a.Kw[s] = c->sz.K[s][2];
+    a.kind_v[s] = c->pb.kind[s][1];
+    a.kind_w[s] = c->pb.kind[s][2];
+    a.mom_off[s] = c->sz.moment_offset[s];
+    a.Cv[s] = c->d_coef[s][1];
+    a.Cw[s] = c->d_coef[s][2];
+  }
+  a.mom_per_elem = c->sz.moments_per_elem;
+  a.mom_per_pair = c->sz.moments_per_pair;
+  a.cu_packed = c->cu_packed.data();
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->prof) {
+    e0 = take_event(c);
+    e1 = take_event(c);
+    cudaEventRecord(e0, st);
+  }
+  cudaError_t err = c->entry->launch(a, c->plan, st);
+  if (err != cudaSuccess) return cuda_fail(err, "contract_kernel launch");
+  if (c->prof) {
+    cudaEventRecord(e1, st);
+    c->ev_con.emplace_back(e0, e1);
+    ++c->n_con;
+  }
+  return P2S_OK;
+}
+
+p2s_status run_fill(p2s_ctx* c, const double* alpha, double* M, int64_t ldM, int64_t n,
+                    cudaStream_t st) {
+  const int64_t ape = c->sz.alpha_per_elem;
+  const int64_t mstride = static_cast<int64_t>(c->sz.n_tot) * ldM;
+  for (int64_t e0 = 0; e0 < n; e0 += c->chunk) {
+    const int64_t cnt = std::min(c->chunk, n - e0);
+    p2s_status s1 = run_moments(c, alpha + e0 * ape, c->d_scratch, cnt, st);
+    if (s1 != P2S_OK) return s1;
+    p2s_status s2 = run_contract(c, c->d_scratch, M + e0 * mstride, ldM, cnt, st);
+    if (s2 != P2S_OK) return s2;
+  }
+  return P2S_OK;
+}
+
+p2s_status check_ctx(const p2s_ctx* c) {
+  if (!c) return fail(P2S_INVALID_ARG, "null context");
+  return P2S_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* p2s_last_error(void) { return g_last_error.c_str(); }
+
+const char* p2s_version(void) { return "p2s_b200 0.1 (sm_100a)"; }
+
+int p2s_shape_supported(const p2s_problem* spec) {
+  if (!spec || validate(spec) != P2S_OK) return 0;
+  return find_entry(*spec) != nullptr;
+}
+
+p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
+  if (!out) return fail(P2S_INVALID_ARG, "p2s_create: null out");
+  *out = nullptr;
+  p2s_status st = validate(spec);
+  if (st != P2S_OK) return st;
+  const RegEntry* entry = find_entry(*spec);
+  if (!entry)
+    return fail(P2S_UNSUPPORTED_SHAPE, "p2s_create: no compiled contraction kernel for N_u=" +
+                                           std::to_string(spec->order[0]) + " with these u-kinds");
+  int ndev = 0;
+  cudaError_t err = cudaGetDeviceCount(&ndev);
+  if (err != cudaSuccess || ndev == 0)
+    return fail(P2S_CUDA_ERROR, "p2s_create: no CUDA device (the fill has no CPU fallback)");
+  if (device < 0 || device >= ndev) return fail(P2S_INVALID_ARG, "p2s_create: bad device");
+  P2S_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop{};
+  P2S_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(P2S_CUDA_ERROR, std::string("p2s_create: built for sm_100a, device is ") + prop.name);
+
+  auto c = std::make_unique<p2s_ctx>();
+  c->pb = *spec;
+  c->device = device;
+  c->entry = entry;
+  const int S = spec->n_terms, nc = spec->n_comp;
+  c->sz.n_pairs = nc * nc;
+  c->sz.n_tot = nc * spec->order[0] * spec->order[1] * spec->order[2];
+  c->sz.alpha_per_elem =
+      static_cast<int64_t>(c->sz.n_pairs) * S * spec->nq[0] * spec->nq[1] * spec->nq[2];
+  int64_t off = 0;
+  int kmax = 1;
+  for (int s = 0; s < S; ++s) {
+    c->sz.moment_offset[s] = off;
+    int64_t kk = 1;
+    for (int d = 0; d < 3; ++d) {
+      const int K = kernel_count(spec->kind[s][d], spec->order[d]);
+      c->sz.K[s][d] = K;
+      kk *= K;
+      kmax = std::max(kmax, K);
+    }
+    off += kk;
+  }
+  c->sz.moments_per_pair = (off + 3) & ~int64_t(3);
+  c->sz.moments_per_elem = c->sz.moments_per_pair * c->sz.n_pairs;
+  c->kmax = kmax <= 8 ? 8 : kmax <= 12 ? 12 : kmax <= 16 ? 16 : kmax <= 20 ? 20 : kmax <= 24 ? 24 : 32;
+  if (kmax > 32) return fail(P2S_UNSUPPORTED_SHAPE, "kernel count above 32");
+
+  // tables
+  for (int d = 0; d < 3; ++d) {
+    gauss_legendre_ld(spec->nq[d], c->x[d], c->w[d]);
+    P2S_CUDA(cudaMalloc(&c->d_x[d], sizeof(double) * spec->nq[d]));
+    P2S_CUDA(cudaMemcpy(c->d_x[d], c->x[d].data(), sizeof(double) * spec->nq[d],
+                        cudaMemcpyHostToDevice));
+  }
+  for (int s = 0; s < S; ++s)
+    for (int d = 0; d < 3; ++d) {
+      const int K = c->sz.K[s][d], nq = spec->nq[d];
+      c->phi[s][d] = weighted_kernel_table(K, c->x[d], c->w[d]);
+      c->coef[s][d] = product_to_sum_table(spec->kind[s][d], spec->order[d]);
+      const int Kp = (K + 1) & ~1;
+      c->Kpad[s][d] = Kp;
+      std::vector<double> T(static_cast<size_t>(nq) * Kp, 0.0);
+      for (int k = 0; k < K; ++k)
+        for (int q = 0; q < nq; ++q) T[static_cast<size_t>(q) * Kp + k] = c->phi[s][d][static_cast<size_t>(k) * nq + q];
+      P2S_CUDA(cudaMalloc(&c->d_phiT[s][d], sizeof(double) * T.size()));
+      P2S_CUDA(cudaMemcpy(c->d_phiT[s][d], T.data(), sizeof(double) * T.size(), cudaMemcpyHostToDevice));
+      P2S_CUDA(cudaMalloc(&c->d_coef[s][d], sizeof(double) * c->coef[s][d].size()));
+      P2S_CUDA(cudaMemcpy(c->d_coef[s][d], c->coef[s][d].data(), sizeof(double) * c->coef[s][d].size(),
+                          cudaMemcpyHostToDevice));
+    }
+  std::vector<const std::vector<double>*> dense;
+  for (int s = 0; s < S; ++s) dense.push_back(&c->coef[s][0]);
+  c->cu_packed = entry->pack(dense);
+
+  // moment-kernel shared memory
+  c->S2 = spec->nq[1] | 1;
+  c->S3 = spec->nq[2] | 1;
+  size_t msm = 0;
+  for (int s = 0; s < S; ++s) {
+    size_t t = 0;
+    for (int d = 0; d < 3; ++d) t += static_cast<size_t>(spec->nq[d]) * c->Kpad[s][d];
+    t += static_cast<size_t>(c->sz.K[s][0]) * spec->nq[2] * c->S2;
+    t += static_cast<size_t>(c->sz.K[s][0]) * c->sz.K[s][1] * c->S3;
+    msm = std::max(msm, t);
+  }
+  c->mom_smem = msm * sizeof(double);
+  if (c->mom_smem > 227 * 1024)
+    return fail(P2S_UNSUPPORTED_SHAPE, "moment stage needs more than 227 KB of shared memory");
+
+  // contraction plan: G n1-values per CTA, ~256 fibers per CTA
+  const int Nv = spec->order[1], Nw = spec->order[2];
+  const int per_n1 = Nw * Nv * Nw;
+  int G = std::max(1, std::min(Nv, 256 / std::max(1, per_n1)));
+  auto contract_smem = [&](int g) {
+    size_t dbl = static_cast<size_t>(c->sz.moments_per_pair);
+    for (int s = 0; s < S; ++s) {
+      dbl += static_cast<size_t>(g) * c->sz.K[s][0] * Nv * c->sz.K[s][2] + 1;
+      dbl += static_cast<size_t>(Nv) * Nv * c->sz.K[s][1] + static_cast<size_t>(Nw) * Nw * c->sz.K[s][2] + 1;
+    }
+    return dbl * sizeof(double) + 64;
+  };
+  while (G > 1 && contract_smem(G) > 227 * 1024) --G;
+  c->plan.G = G;
+  c->plan.NG = (Nv + G - 1) / G;
+  c->plan.threads = std::min(256, ((G * per_n1 + 31) / 32) * 32);
+  c->plan.smem = contract_smem(G);
+  if (c->plan.smem > 227 * 1024)
+    return fail(P2S_UNSUPPORTED_SHAPE, "contraction stage needs more than 227 KB of shared memory");
+  if (c->sz.moments_per_pair * 8 >= (1 << 20))
+    return fail(P2S_UNSUPPORTED_SHAPE, "moment block above the bulk-copy transaction limit");
+
+  // scheduler chunk: moment scratch of ~32 MB stays in L2 between the stages
+  const int64_t per = c->sz.moments_per_elem * 8;
+  c->chunk = std::max<int64_t>(1, (int64_t(32) << 20) / per);
+  P2S_CUDA(cudaMalloc(&c->d_scratch, sizeof(double) * c->sz.moments_per_elem * c->chunk));
+  *out = c.release();
+  return P2S_OK;
+}
+
+void p2s_destroy(p2s_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int s = 0; s < kMaxTerms; ++s)
+    for (int d = 0; d < 3; ++d) {
+      if (c->d_phiT[s][d]) cudaFree(c->d_phiT[s][d]);
+      if (c->d_coef[s][d]) cudaFree(c->d_coef[s][d]);
+    }
+  for (int d = 0; d < 3; ++d)
+    if (c->d_x[d]) cudaFree(c->d_x[d]);
+  if (c->d_scratch) cudaFree(c->d_scratch);
+  for (int i = 0; i < 2; ++i) {
+    if (c->d_ring_alpha[i]) cudaFree(c->d_ring_alpha[i]);
+    if (c->d_ring_M[i]) cudaFree(c->d_ring_M[i]);
+    if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
+    if (c->ev_comp[i]) cudaEventDestroy(c->ev_comp[i]);
+    if (c->ev_d2h[i]) cudaEventDestroy(c->ev_d2h[i]);
+  }
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_comp) cudaStreamDestroy(c->s_comp);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+  harvest(c);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+}
+
+p2s_status p2s_get_sizes(const p2s_ctx* c, p2s_sizes* out) {
+  if (check_ctx(c) != P2S_OK || !out) return fail(P2S_INVALID_ARG, "p2s_get_sizes: null argument");
+  *out = c->sz;
+  return P2S_OK;
+}
+
+p2s_status p2s_moments(p2s_ctx* c, const double* d_alpha, double* d_I, int64_t n, void* stream) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (n < 0 || (n > 0 && (!d_alpha || !d_I))) return fail(P2S_INVALID_ARG, "p2s_moments: bad buffers");
+  if (reinterpret_cast<uintptr_t>(d_alpha) % 16) return fail(P2S_INVALID_ARG, "alpha must be 16-byte aligned");
+  P2S_CUDA(cudaSetDevice(c->device));
+  return run_moments(c, d_alpha, d_I, n, static_cast<cudaStream_t>(stream));
+}
+
+p2s_status p2s_contract(p2s_ctx* c, const double* d_I, double* d_M, int64_t ldM, int64_t n,
+                        void* stream) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (n < 0 || (n > 0 && (!d_I || !d_M))) return fail(P2S_INVALID_ARG, "p2s_contract: bad buffers");
+  if (ldM < c->sz.n_tot) return fail(P2S_INVALID_ARG, "p2s_contract: ld_M < n_tot");
+  if (reinterpret_cast<uintptr_t>(d_I) % 16) return fail(P2S_INVALID_ARG, "I must be 16-byte aligned");
+  P2S_CUDA(cudaSetDevice(c->device));
+  return run_contract(c, d_I, d_M, ldM, n, static_cast<cudaStream_t>(stream));
+}
+
+p2s_status p2s_fill(p2s_ctx* c, const double* d_alpha, double* d_M, int64_t ldM, int64_t n,
+                    void* stream) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (n < 0 || (n > 0 && (!d_alpha || !d_M))) return fail(P2S_INVALID_ARG, "p2s_fill: bad buffers");
+  if (ldM < c->sz.n_tot) return fail(P2S_INVALID_ARG, "p2s_fill: ld_M < n_tot");
+  if (reinterpret_cast<uintptr_t>(d_alpha) % 16) return fail(P2S_INVALID_ARG, "alpha must be 16-byte aligned");
+  P2S_CUDA(cudaSetDevice(c->device));
+  return run_fill(c, d_alpha, d_M, ldM, n, static_cast<cudaStream_t>(stream));
+}
+
+p2s_status p2s_fill_host(p2s_ctx* c, const double* h_alpha, double* h_M, int64_t ldM, int64_t n) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (n < 0 || (n > 0 && (!h_alpha || !h_M))) return fail(P2S_INVALID_ARG, "p2s_fill_host: bad buffers");
+  if (ldM < c->sz.n_tot) return fail(P2S_INVALID_ARG, "p2s_fill_host: ld_M < n_tot");
+  P2S_CUDA(cudaSetDevice(c->device));
+  const int64_t nt = c->sz.n_tot;
+  const int64_t ape = c->sz.alpha_per_elem;
+  const int64_t mel = nt * nt;  // device ring keeps ld = n_tot
+  if (!c->s_h2d) {
+    P2S_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    P2S_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    P2S_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      P2S_CUDA(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
+      P2S_CUDA(cudaEventCreateWithFlags(&c->ev_comp[i], cudaEventDisableTiming));
+      P2S_CUDA(cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming));
+    }
+    // ~256 MB of matrices per slot
+    c->host_chunk = std::max<int64_t>(1, (int64_t(256) << 20) / (mel * 8));
+    for (int i = 0; i < 2; ++i) {
+      P2S_CUDA(cudaMalloc(&c->d_ring_alpha[i], sizeof(double) * ape * c->host_chunk));
+      P2S_CUDA(cudaMalloc(&c->d_ring_M[i], sizeof(double) * mel * c->host_chunk));
+    }
+  }
+  int64_t slot_iter[2] = {0, 0};
+  int it = 0;
+  for (int64_t e0 = 0; e0 < n; e0 += c->host_chunk, ++it) {
+    const int sl = it & 1;
+    const int64_t cnt = std::min(c->host_chunk, n - e0);
+    if (slot_iter[sl] > 0) P2S_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_d2h[sl], 0));
+    P2S_CUDA(cudaMemcpyAsync(c->d_ring_alpha[sl], h_alpha + e0 * ape, sizeof(double) * ape * cnt,
+                             cudaMemcpyHostToDevice, c->s_h2d));
+    P2S_CUDA(cudaEventRecord(c->ev_h2d[sl], c->s_h2d));
+    P2S_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_h2d[sl], 0));
+    p2s_status st = run_fill(c, c->d_ring_alpha[sl], c->d_ring_M[sl], nt, cnt, c->s_comp);
+    if (st != P2S_OK) return st;
+    P2S_CUDA(cudaEventRecord(c->ev_comp[sl], c->s_comp));
+    P2S_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_comp[sl], 0));
+    if (ldM == nt) {
+      P2S_CUDA(cudaMemcpyAsync(h_M + e0 * mel, c->d_ring_M[sl], sizeof(double) * mel * cnt,
+                               cudaMemcpyDeviceToHost, c->s_d2h));
+    } else {
+      P2S_CUDA(cudaMemcpy2DAsync(h_M + e0 * nt * ldM, sizeof(double) * ldM, c->d_ring_M[sl],
+                                 sizeof(double) * nt, sizeof(double) * nt, nt * cnt,
+                                 cudaMemcpyDeviceToHost, c->s_d2h));
+    }
+    P2S_CUDA(cudaEventRecord(c->ev_d2h[sl], c->s_d2h));
+    ++slot_iter[sl];
+  }
+  P2S_CUDA(cudaStreamSynchronize(c->s_d2h));
+  P2S_CUDA(cudaStreamSynchronize(c->s_comp));
+  return P2S_OK;
+}
+
+p2s_status p2s_alpha_generate(p2s_ctx* c, int kind, double lo, double hi, uint64_t seed,
+                              int64_t e0, int64_t n, double* d_alpha, void* stream) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (kind < 0 || kind > 2) return fail(P2S_INVALID_ARG, "p2s_alpha_generate: bad kind");
+  if (n < 0 || (n > 0 && !d_alpha)) return fail(P2S_INVALID_ARG, "p2s_alpha_generate: bad buffer");
+  P2S_CUDA(cudaSetDevice(c->device));
+  const double* xs[3] = {c->d_x[0], c->d_x[1], c->d_x[2]};
+  cudaError_t err = launch_alpha(d_alpha, xs, c->pb.nq, c->pb.n_comp, c->pb.n_terms, kind, lo, hi,
+                                 seed, e0, n, c->sz.alpha_per_elem, static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "alpha_kernel launch");
+  return P2S_OK;
+}
+
+p2s_status p2s_get_tables(const p2s_ctx* c, int term, int dir, double* phi, double* coef,
+                          double* nodes, double* weights) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (term < 0 || term >= c->pb.n_terms || dir < 0 || dir > 2)
+    return fail(P2S_INVALID_ARG, "p2s_get_tables: bad term/dir");
+  if (phi) std::memcpy(phi, c->phi[term][dir].data(), sizeof(double) * c->phi[term][dir].size());
+  if (coef) std::memcpy(coef, c->coef[term][dir].data(), sizeof(double) * c->coef[term][dir].size());
+  if (nodes) std::memcpy(nodes, c->x[dir].data(), sizeof(double) * c->x[dir].size());
+  if (weights) std::memcpy(weights, c->w[dir].data(), sizeof(double) * c->w[dir].size());
+  return P2S_OK;
+}
+
+p2s_status p2s_set_profiling(p2s_ctx* c, int enable) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  P2S_CUDA(cudaSetDevice(c->device));
+  P2S_CUDA(cudaDeviceSynchronize());
+  harvest(c);
+  c->prof = enable != 0;
+  c->ms_mom = c->ms_con = 0.0;
+  c->n_mom = c->n_con = 0;
+  return P2S_OK;
+}
+
+p2s_status p2s_get_stage_times(p2s_ctx* c, double* ms_mom, double* ms_con, int64_t* n_mom,
+                               int64_t* n_con) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  P2S_CUDA(cudaSetDevice(c->device));
+  P2S_CUDA(cudaDeviceSynchronize());
+  harvest(c);
+  if (ms_mom) *ms_mom = c->ms_mom;
+  if (ms_con) *ms_con = c->ms_con;
+  if (n_mom) *n_mom = c->n_mom;
+  if (n_con) *n_con = c->n_con;
+  return P2S_OK;
+}
+
+}  // extern "C"

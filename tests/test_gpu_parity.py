@@ -1,0 +1,200 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle.
+
+Bar (north_star): <= 1e-12 relative error with the reference comparator
+(verify.cpp:81-99: |a-b| <= 1e-12 max(|a|,|b|) or <= 1e-12 max|block|),
+applied per (gi, gj) pair block, on byte-identical alpha.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_1703_09619_b200 import capi
+from paper_1703_09619_b200.capi import DD, DP, PD, PP
+from paper_1703_09619_b200.configs import CONFIGS
+
+from helpers import RTOL, blocks_close, oracle_for
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_fill(ctx, alpha_np, ld=None):
+    n = alpha_np.shape[0]
+    ld = ld or ctx.n_tot
+    a = torch.from_numpy(np.ascontiguousarray(alpha_np)).cuda()
+    M = torch.full((n, ctx.n_tot, ld), float("nan"), dtype=torch.float64, device="cuda")
+    ctx.fill(a, M, ld, n, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return M.cpu().numpy()
+
+
+def _gpu_moments(ctx, alpha_np):
+    n = alpha_np.shape[0]
+    a = torch.from_numpy(np.ascontiguousarray(alpha_np)).cuda()
+    I = torch.zeros((n, ctx.moments_per_elem), dtype=torch.float64, device="cuda")
+    ctx.moments(a, I, n, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return I.cpu().numpy()
+
+
+def _check_case(n_comp, order, kinds, nq, alpha_kind, lo, hi, n_elem, seed=11, threads=8):
+    o = oracle_for(n_comp, order, kinds, nq)
+    ctx = capi.Context(n_comp, order, kinds, nq)
+    alpha = o.alpha(alpha_kind, lo, hi, seed, 0, n_elem)
+    Mg = _gpu_fill(ctx, alpha)
+    Mo = o.fill(alpha, threads=threads)
+    assert np.isfinite(Mg).all()
+    Nt = order[0] * order[1] * order[2]
+    worst = 0.0
+    for e in range(n_elem):
+        ok, msg, w = blocks_close(Mg[e], Mo[e], n_comp, Nt)
+        worst = max(worst, w)
+        assert ok, f"element {e}: {msg}"
+    return worst
+
+
+SMALL_CASES = [
+    # n_comp, order, kinds, nq, alpha_kind
+    (1, (4, 4, 4), [PP], (8, 8, 8), O.ALPHA_SINE),                      # C1 shape
+    (1, (2, 3, 4), [PP], (5, 6, 7), O.ALPHA_SINE),                      # anisotropic
+    (3, (3, 3, 3), [PP, DD], (6, 6, 6), O.ALPHA_JACOBIAN),              # small C2 analogue
+    (1, (3, 5, 2), [DD], (7, 8, 6), O.ALPHA_SINE),
+    (1, (3, 4, 3), [DP], (7, 7, 7), O.ALPHA_SINE),
+    (1, (3, 2, 4), [PD], (7, 7, 7), O.ALPHA_SINE),
+    (1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7), O.ALPHA_SINE),
+    (3, (4, 2, 3), [PP, (DD, PP, DP), (DP, PD, PD), (PD, DD, PP)], (6, 5, 4), O.ALPHA_SINE),
+    (1, (5, 5, 5), [PP, DD], (9, 9, 9), O.ALPHA_EXPSIN),
+    (1, (1, 1, 1), [PP], (3, 3, 3), O.ALPHA_SINE),
+    (1, (3, 3, 3), [PP, (DP, DD, PD)], (5, 5, 5), O.ALPHA_SINE),
+    (1, (2, 6, 5), [PP, DD], (4, 9, 8), O.ALPHA_SINE),
+]
+
+
+@pytest.mark.parametrize("case", SMALL_CASES, ids=lambda c: f"{c[0]}c-{c[1]}-{len(c[2])}t")
+def test_small_shapes_match_oracle(case):
+    n_comp, order, kinds, nq, ak = case
+    _check_case(n_comp, order, kinds, nq, ak, 0.5, 3.0, n_elem=5)
+
+
+@pytest.mark.parametrize("name,n_elem", [("c1", 1), ("c2", 6), ("c3", 4), ("c4", 4)])
+def test_baseline_configs_match_oracle(name, n_elem):
+    cfg = CONFIGS[name]
+    worst = _check_case(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq, cfg.alpha_kind,
+                        cfg.alpha_lo, cfg.alpha_hi, n_elem=n_elem, seed=2024)
+    assert worst < 1e-12
+
+
+def test_moments_match_oracle():
+    cfg = CONFIGS["c2"]
+    o = oracle_for(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
+    ctx = capi.Context(**cfg.problem())
+    alpha = o.alpha(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 5, 0, 3)
+    Ig = _gpu_moments(ctx, alpha)
+    Io = o.moments(alpha, threads=4)
+    for e in range(3):
+        for pr in range(ctx.n_pairs):
+            for s in range(len(cfg.kinds)):
+                K = [ctx.K(s, d) for d in range(3)]
+                n = K[0] * K[1] * K[2]
+                g = Ig[e, ctx.moment_offset(pr, s):ctx.moment_offset(pr, s) + n].reshape(K[0], -1)
+                r = Io[e, o.moment_offset(pr, s):o.moment_offset(pr, s) + n].reshape(K[0], -1)
+                ok, (i, j) = O.block_close(g, r, RTOL)
+                assert ok, (e, pr, s, i, j, g[i, j], r[i, j])
+
+
+def test_tables_match_oracle():
+    for kinds, order, nq in [([PP, DD], (6, 8, 10), (14, 9, 20)), ([DP, PD], (5, 4, 3), (7, 8, 9))]:
+        o = oracle_for(1, order, kinds, nq)
+        ctx = capi.Context(1, order, kinds, nq)
+        for s in range(len(kinds)):
+            for d in range(3):
+                phi, coef, x, w = ctx.tables(s, d)
+                np.testing.assert_allclose(x, o.nodes(d), rtol=0, atol=4e-16)
+                np.testing.assert_allclose(w, o.weights(d), rtol=4e-15, atol=0)
+                np.testing.assert_allclose(phi, o.phi(s, d), rtol=1e-14, atol=1e-15)
+                c = o.coef(s, d)
+                np.testing.assert_allclose(coef, c, rtol=4e-16, atol=0)
+                assert np.array_equal(coef == 0, c == 0)
+
+
+def test_device_alpha_matches_host_generator():
+    for name in ("c1", "c2", "c3", "c4"):
+        cfg = CONFIGS[name]
+        o = oracle_for(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
+        ctx = capi.Context(**cfg.problem())
+        n = 3
+        d = torch.empty((n, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")
+        ctx.alpha_generate(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 77, 1000, n, d)
+        torch.cuda.synchronize()
+        h = o.alpha(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 77, 1000, n)
+        np.testing.assert_allclose(d.cpu().numpy(), h, rtol=1e-13, atol=1e-14)
+
+
+def test_fill_equals_two_stage_and_is_deterministic():
+    cfg = CONFIGS["c2"]
+    ctx = capi.Context(**cfg.problem())
+    n = 300  # > one scheduler chunk
+    st = torch.cuda.current_stream().cuda_stream
+    a = torch.empty((n, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")
+    ctx.alpha_generate(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 3, 0, n, a, st)
+    M1 = torch.empty((n, ctx.n_tot, ctx.n_tot), dtype=torch.float64, device="cuda")
+    M2 = torch.empty_like(M1)
+    I = torch.empty((n, ctx.moments_per_elem), dtype=torch.float64, device="cuda")
+    ctx.fill(a, M1, ctx.n_tot, n, st)
+    ctx.moments(a, I, n, st)
+    ctx.contract(I, M2, ctx.n_tot, n, st)
+    torch.cuda.synchronize()
+    assert torch.equal(M1, M2)
+    ctx.fill(a, M2, ctx.n_tot, n, st)
+    torch.cuda.synchronize()
+    assert torch.equal(M1, M2)
+    # element matrices are symmetric for symmetric alpha and PP / P'P' terms
+    assert torch.equal(M1, M1.transpose(1, 2))
+
+
+def test_linearity_doubling_is_exact():
+    cfg = CONFIGS["c3"]
+    ctx = capi.Context(**cfg.problem())
+    n = 64
+    a = torch.empty((n, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")
+    ctx.alpha_generate(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 9, 0, n, a)
+    M1 = torch.empty((n, ctx.n_tot, ctx.n_tot), dtype=torch.float64, device="cuda")
+    M2 = torch.empty_like(M1)
+    ctx.fill(a, M1, ctx.n_tot, n, 0)
+    a2 = a * 2.0
+    ctx.fill(a2, M2, ctx.n_tot, n, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(M2, 2.0 * M1)
+
+
+def test_leading_dimension_and_host_path():
+    cfg = CONFIGS["c2"]
+    o = oracle_for(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
+    ctx = capi.Context(**cfg.problem())
+    n = 3
+    alpha = o.alpha(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 21, 0, n)
+    ld = ctx.n_tot + 5
+    Mg = _gpu_fill(ctx, alpha, ld=ld)
+    assert np.isnan(Mg[:, :, ctx.n_tot:]).all()  # padding untouched
+    Mh = np.full((n, ctx.n_tot, ld), np.nan)
+    ctx.fill_host(np.ascontiguousarray(alpha), Mh, ld, n)
+    assert np.array_equal(Mh[:, :, :ctx.n_tot], Mg[:, :, :ctx.n_tot])
+    Mo = o.fill(alpha, threads=4)
+    for e in range(n):
+        ok, msg, _ = blocks_close(Mh[e, :, :ctx.n_tot], Mo[e], cfg.n_comp, 216)
+        assert ok, msg
+
+
+def test_error_paths():
+    cfg = CONFIGS["c1"]
+    ctx = capi.Context(**cfg.problem())
+    a = torch.zeros((1, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")
+    M = torch.zeros((1, ctx.n_tot, ctx.n_tot), dtype=torch.float64, device="cuda")
+    with pytest.raises(capi.InvalidArgument):
+        ctx.fill(a, M, ctx.n_tot - 1, 1)
+    with pytest.raises(capi.InvalidArgument):
+        ctx.fill(0, M, ctx.n_tot, 1)
+    with pytest.raises(capi.UnsupportedShape):
+        capi.Context(1, (7, 3, 3), [DP], (5, 5, 5))
+    with pytest.raises(capi.InvalidArgument):
+        capi.Context(1, (0, 3, 3), [PP], (5, 5, 5))
