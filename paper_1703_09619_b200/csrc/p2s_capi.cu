@@ -7,12 +7,14 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/p2s_b200.h"
+#include "p2s_contract_v2.cuh"
 #include "p2s_kernels.cuh"
 #include "p2s_tables.hpp"
 
@@ -181,6 +183,122 @@ const RegEntry* find_entry(const p2s_problem& pb) {
   return nullptr;
 }
 
+// ------------------------------------------------------------ shape-specialised registry
+
+struct V2Args {
+  const double* I;
+  double* M;
+  int64_t ldM, n_tot, n_elem, mom_per_elem;
+  int nc, P, Nt;
+  const std::vector<double>* dense[kMaxTerms][3];  // [N][N][K] per term, direction
+};
+
+using v2_fn = cudaError_t (*)(const V2Args&, const std::vector<double>&, cudaStream_t, int);
+using v2_pack_fn = std::vector<double> (*)(const V2Args&);
+
+template <class Sh>
+std::vector<double> pack_v2(const V2Args& a) {
+  std::vector<double> out(static_cast<size_t>(Sh::ctot(0) + Sh::ctot(1) + Sh::ctot(2)), 0.0);
+  const int base[3] = {0, Sh::ctot(0), Sh::ctot(0) + Sh::ctot(1)};
+  for (int d = 0; d < 3; ++d)
+    for (int s = 0; s < Sh::S; ++s) {
+      const int K = Sh::K(s, d), kd = Sh::kind(s, d), N = Sh::N(d);
+      const std::vector<double>& C = *a.dense[s][d];
+      for (int x = 0; x < N; ++x)
+        for (int y = 0; y < N; ++y) {
+          const int lo = band_lo(kd, x, y), cnt = band_count(kd, x, y);
+          const int co = Sh::coff(d, s, x, y);
+          for (int j = 0; j < cnt; ++j)
+            out[static_cast<size_t>(base[d] + co + j)] =
+                C[(static_cast<size_t>(x) * N + y) * K + lo + 2 * j];
+        }
+    }
+  return out;
+}
+
+template <class Sh>
+cudaError_t launch_v2(const V2Args& a, const std::vector<double>& packed, cudaStream_t st,
+                      int num_sms) {
+  V2Params<Sh> p;
+  p.I = a.I;
+  p.M = a.M;
+  p.ldM = a.ldM;
+  p.mat_stride = a.n_tot * a.ldM;
+  p.n_units = a.n_elem * a.P;
+  p.nc = a.nc;
+  p.P = a.P;
+  p.Nt = a.Nt;
+  p.mom_per_elem = a.mom_per_elem;
+  std::memcpy(p.cu, packed.data(), sizeof(double) * Sh::ctot(0));
+  std::memcpy(p.cv, packed.data() + Sh::ctot(0), sizeof(double) * Sh::ctot(1));
+  std::memcpy(p.cw, packed.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));
+  if (p.n_units == 0) return cudaSuccess;
+  static int blocks_per_sm = -1;  // per instantiation (kernel attributes are process-wide)
+  if (blocks_per_sm < 0) {
+    cudaError_t e = cudaFuncSetAttribute(contract_v2_kernel<Sh>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
+    if (e != cudaSuccess) return e;
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, contract_v2_kernel<Sh>, Sh::THREADS,
+                                                      Sh::SMEM);
+    if (e != cudaSuccess) return e;
+    if (b < 1) return cudaErrorInvalidConfiguration;
+    blocks_per_sm = b;
+  }
+  const int64_t grid = std::min<int64_t>(p.n_units, static_cast<int64_t>(blocks_per_sm) * num_sms);
+  contract_v2_kernel<Sh><<<static_cast<unsigned>(grid), Sh::THREADS, Sh::SMEM, st>>>(p);
+  return cudaGetLastError();
+}
+
+struct V2Entry {
+  int order[3];
+  int S;
+  int kinds[kMaxTerms][3];
+  v2_fn launch;
+  v2_pack_fn pack;
+  size_t smem;
+};
+
+template <class Sh>
+V2Entry make_v2() {
+  V2Entry r{};
+  for (int d = 0; d < 3; ++d) r.order[d] = Sh::N(d);
+  r.S = Sh::S;
+  for (int s = 0; s < Sh::S; ++s)
+    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Sh::kind(s, d);
+  r.launch = &launch_v2<Sh>;
+  r.pack = &pack_v2<Sh>;
+  r.smem = Sh::SMEM;
+  return r;
+}
+
+constexpr int kPPP = enc_kind(PP, PP, PP);
+constexpr int kDDD = enc_kind(DD, DD, DD);
+
+// <N_u, N_v, N_w, n1 tile, threads, min CTAs/SM, term kinds...>
+const std::vector<V2Entry>& v2_registry() {
+  static const std::vector<V2Entry> reg = {
+      make_v2<Shape<4, 4, 4, 4, 256, 2, kPPP>>(),          // C1
+      make_v2<Shape<6, 6, 6, 1, 224, 2, kPPP, kDDD>>(),    // C2
+      make_v2<Shape<8, 8, 8, 1, 512, 1, kPPP, kDDD>>(),    // C3
+      make_v2<Shape<10, 6, 4, 2, 192, 2, kPPP, kDDD>>(),   // C4
+      make_v2<Shape<3, 3, 3, 3, 96, 4, kPPP, kDDD>>(),     // small vector test shape
+      make_v2<Shape<4, 3, 3, 3, 96, 4, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+  };
+  return reg;
+}
+
+const V2Entry* find_v2(const p2s_problem& pb) {
+  for (const V2Entry& r : v2_registry()) {
+    bool ok = r.S == pb.n_terms;
+    for (int d = 0; d < 3; ++d) ok = ok && r.order[d] == pb.order[d];
+    for (int s = 0; ok && s < r.S; ++s)
+      for (int d = 0; d < 3; ++d) ok = ok && r.kinds[s][d] == pb.kind[s][d];
+    if (ok) return &r;
+  }
+  return nullptr;
+}
+
 // ------------------------------------------------------------ moment launch
 
 template <int KMAX>
@@ -224,6 +342,10 @@ struct p2s_ctx {
   double* d_coef[kMaxTerms][3]{};          // [N][N][K]
   double* d_x[3]{};
   const RegEntry* entry = nullptr;
+  const V2Entry* v2 = nullptr;
+  std::vector<double> v2_packed;
+  int num_sms = 148;
+  bool force_generic = false;
   std::vector<double> cu_packed;
   Plan plan{};
   int kmax = 8;
@@ -362,7 +484,22 @@ p2s_status run_contract(p2s_ctx* c, const double* I, double* M, int64_t ldM, int
     e1 = take_event(c);
     cudaEventRecord(e0, st);
   }
-  cudaError_t err = c->entry->launch(a, c->plan, st);
+  cudaError_t err;
+  if (c->v2 && !c->force_generic) {
+    V2Args v;
+    v.I = I;
+    v.M = M;
+    v.ldM = ldM;
+    v.n_tot = c->sz.n_tot;
+    v.n_elem = n;
+    v.mom_per_elem = c->sz.moments_per_elem;
+    v.nc = c->pb.n_comp;
+    v.P = c->sz.n_pairs;
+    v.Nt = a.Nt;
+    err = c->v2->launch(v, c->v2_packed, st, c->num_sms);
+  } else {
+    err = c->entry->launch(a, c->plan, st);
+  }
   if (err != cudaSuccess) return cuda_fail(err, "contract_kernel launch");
   if (c->prof) {
     cudaEventRecord(e1, st);
@@ -401,7 +538,7 @@ const char* p2s_version(void) { return "p2s_b200 0.1 (sm_100a)"; }
 
 int p2s_shape_supported(const p2s_problem* spec) {
   if (!spec || validate(spec) != P2S_OK) return 0;
-  return find_entry(*spec) != nullptr;
+  return find_entry(*spec) != nullptr || find_v2(*spec) != nullptr;
 }
 
 p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
@@ -410,7 +547,8 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
   p2s_status st = validate(spec);
   if (st != P2S_OK) return st;
   const RegEntry* entry = find_entry(*spec);
-  if (!entry)
+  const V2Entry* v2e = find_v2(*spec);
+  if (!entry && !v2e)
     return fail(P2S_UNSUPPORTED_SHAPE, "p2s_create: no compiled contraction kernel for N_u=" +
                                            std::to_string(spec->order[0]) + " with these u-kinds");
   int ndev = 0;
@@ -428,6 +566,9 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
   c->pb = *spec;
   c->device = device;
   c->entry = entry;
+  c->v2 = v2e;
+  c->num_sms = prop.multiProcessorCount;
+  if (const char* g = std::getenv("P2S_FORCE_GENERIC")) c->force_generic = entry && g[0] == '1';
   const int S = spec->n_terms, nc = spec->n_comp;
   c->sz.n_pairs = nc * nc;
   c->sz.n_tot = nc * spec->order[0] * spec->order[1] * spec->order[2];
@@ -476,7 +617,13 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
     }
   std::vector<const std::vector<double>*> dense;
   for (int s = 0; s < S; ++s) dense.push_back(&c->coef[s][0]);
-  c->cu_packed = entry->pack(dense);
+  if (entry) c->cu_packed = entry->pack(dense);
+  if (v2e) {
+    V2Args v{};
+    for (int s = 0; s < S; ++s)
+      for (int d = 0; d < 3; ++d) v.dense[s][d] = &c->coef[s][d];
+    c->v2_packed = v2e->pack(v);
+  }
 
   // moment-kernel shared memory
   c->S2 = spec->nq[1] | 1;
@@ -510,7 +657,7 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
   c->plan.NG = (Nv + G - 1) / G;
   c->plan.threads = std::min(256, ((G * per_n1 + 31) / 32) * 32);
   c->plan.smem = contract_smem(G);
-  if (c->plan.smem > 227 * 1024)
+  if (!v2e && c->plan.smem > 227 * 1024)
     return fail(P2S_UNSUPPORTED_SHAPE, "contraction stage needs more than 227 KB of shared memory");
   if (c->sz.moments_per_pair * 8 >= (1 << 20))
     return fail(P2S_UNSUPPORTED_SHAPE, "moment block above the bulk-copy transaction limit");
