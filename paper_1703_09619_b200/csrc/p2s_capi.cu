@@ -15,6 +15,7 @@
 
 #include "../../include/p2s_b200.h"
 #include "p2s_contract_v2.cuh"
+#include "p2s_moments_v2.cuh"
 #include "p2s_kernels.cuh"
 #include "p2s_tables.hpp"
 
@@ -299,6 +300,95 @@ const V2Entry* find_v2(const p2s_problem& pb) {
   return nullptr;
 }
 
+// ------------------------------------------------------------ shape-specialised moments
+
+using mv2_fn = cudaError_t (*)(const double*, double*, int64_t, int, int64_t,
+                               const std::vector<double>&, cudaStream_t);
+using mv2_pack_fn = std::vector<double> (*)(const std::vector<double> (*)[3]);
+
+template <class Ms>
+std::vector<double> pack_mv2(const std::vector<double> (*phi)[3]) {
+  // phi[s][d] = [K][nq] full weighted table -> half tables [K][H]
+  std::vector<double> out(static_cast<size_t>(Ms::TTOT), 0.0);
+  for (int s = 0; s < Ms::S; ++s)
+    for (int d = 0; d < 3; ++d) {
+      const int K = Ms::K(s, d), Q = Ms::Q(d), H = Ms::H(d);
+      for (int k = 0; k < K; ++k)
+        for (int h = 0; h < H; ++h)
+          out[static_cast<size_t>(Ms::toff(s, d) + k * H + h)] = phi[s][d][static_cast<size_t>(k) * Q + h];
+    }
+  return out;
+}
+
+template <class Ms>
+cudaError_t launch_mv2(const double* alpha, double* I, int64_t n_elem, int P, int64_t mom_per_elem,
+                       const std::vector<double>& packed, cudaStream_t st) {
+  MV2Params<Ms> p;
+  p.alpha = alpha;
+  p.I = I;
+  p.P = P;
+  p.n_units = n_elem * P * Ms::S;
+  p.mom_per_elem = mom_per_elem;
+  std::memcpy(p.tab, packed.data(), sizeof(double) * Ms::TTOT);
+  if (p.n_units == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(moments_v2_kernel<Ms>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ms::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  moments_v2_kernel<Ms><<<static_cast<unsigned>(p.n_units), Ms::THREADS, Ms::SMEM, st>>>(p);
+  return cudaGetLastError();
+}
+
+struct MV2Entry {
+  int order[3], nq[3], S;
+  int kinds[kMaxTerms][3];
+  mv2_fn launch;
+  mv2_pack_fn pack;
+};
+
+template <class Ms>
+MV2Entry make_mv2() {
+  MV2Entry r{};
+  for (int d = 0; d < 3; ++d) {
+    r.order[d] = Ms::N(d);
+    r.nq[d] = Ms::Q(d);
+  }
+  r.S = Ms::S;
+  for (int s = 0; s < Ms::S; ++s)
+    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Ms::kind(s, d);
+  r.launch = &launch_mv2<Ms>;
+  r.pack = &pack_mv2<Ms>;
+  return r;
+}
+
+// <N_u, N_v, N_w, nq_u, nq_v, nq_w, threads, term kinds...>
+const std::vector<MV2Entry>& mv2_registry() {
+  static const std::vector<MV2Entry> reg = {
+      make_mv2<MShape<4, 4, 4, 8, 8, 8, 128, kPPP>>(),                    // C1
+      make_mv2<MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),           // C2
+      make_mv2<MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),           // C3
+      make_mv2<MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>>(),          // C4
+      make_mv2<MShape<3, 3, 3, 6, 6, 6, 128, kPPP, kDDD>>(),              // test shapes
+      make_mv2<MShape<4, 3, 3, 9, 5, 7, 128, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+      make_mv2<MShape<5, 5, 5, 9, 9, 9, 128, kPPP, kDDD>>(),
+  };
+  return reg;
+}
+
+const MV2Entry* find_mv2(const p2s_problem& pb) {
+  for (const MV2Entry& r : mv2_registry()) {
+    bool ok = r.S == pb.n_terms;
+    for (int d = 0; d < 3; ++d) ok = ok && r.order[d] == pb.order[d] && r.nq[d] == pb.nq[d];
+    for (int s = 0; ok && s < r.S; ++s)
+      for (int d = 0; d < 3; ++d) ok = ok && r.kinds[s][d] == pb.kind[s][d];
+    if (ok) return &r;
+  }
+  return nullptr;
+}
+
 // ------------------------------------------------------------ moment launch
 
 template <int KMAX>
@@ -343,6 +433,8 @@ struct p2s_ctx {
   double* d_x[3]{};
   const RegEntry* entry = nullptr;
   const V2Entry* v2 = nullptr;
+  const MV2Entry* mv2 = nullptr;
+  std::vector<double> mv2_packed;
   std::vector<double> v2_packed;
   int num_sms = 148;
   bool force_generic = false;
@@ -441,7 +533,11 @@ p2s_status run_moments(p2s_ctx* c, const double* alpha, double* I, int64_t n, cu
     e1 = take_event(c);
     cudaEventRecord(e0, st);
   }
-  cudaError_t err = launch_moments(c->kmax, p, c->mom_smem, st);
+  cudaError_t err;
+  if (c->mv2 && !c->force_generic)
+    err = c->mv2->launch(alpha, I, n, p.P, p.mom_per_elem, c->mv2_packed, st);
+  else
+    err = launch_moments(c->kmax, p, c->mom_smem, st);
   if (err != cudaSuccess) return cuda_fail(err, "moments_kernel launch");
   if (c->prof) {
     cudaEventRecord(e1, st);
@@ -618,6 +714,8 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
   std::vector<const std::vector<double>*> dense;
   for (int s = 0; s < S; ++s) dense.push_back(&c->coef[s][0]);
   if (entry) c->cu_packed = entry->pack(dense);
+  c->mv2 = find_mv2(*spec);
+  if (c->mv2) c->mv2_packed = c->mv2->pack(c->phi);
   if (v2e) {
     V2Args v{};
     for (int s = 0; s < S; ++s)

@@ -1,0 +1,169 @@
+// p2s_moments_v2.cuh -- shape-specialised moment kernel.
+//
+// I_s[k1][k2][k3] = sum_q alpha_s(q) phi_k1(u_q1) phi_k2(v_q2) phi_k3(w_q3),
+// phi_k(x_q) = w_q P_k(x_q), by three 1-D passes.  The Gauss-Legendre rule is
+// symmetric (x_{n-1-h} = -x_h, w_{n-1-h} = w_h) and P_k(-x) = (-1)^k P_k(x),
+// so every pass first folds a fiber into its even part a_h + a_{n-1-h} and odd
+// part a_h - a_{n-1-h}; even k then contract the even part and odd k the odd
+// part over half the nodes: half the FMAs of the plain sum factorisation.
+// Sizes are compile-time, tables are constant-bank operands, fibers live in
+// registers:
+//   pass u: thread = alpha row (q_w, q_v), 16-B global loads    -> T1[k1][q_w][q_v]
+//   pass v: thread = fiber (k1, q_w) of T1                      -> T2[k1 k2][q_w]
+//   pass w: thread = fiber (k1, k2) of T2                       -> I (global or smem)
+#pragma once
+
+#include "p2s_kernels.cuh"
+
+namespace p2s {
+
+template <int NU_, int NV_, int NW_, int QU_, int QV_, int QW_, int THREADS_, int... TK>
+struct MShape {
+  static constexpr int NU = NU_, NV = NV_, NW = NW_, THREADS = THREADS_;
+  static constexpr int S = sizeof...(TK);
+  static constexpr int N(int d) { return d == 0 ? NU : d == 1 ? NV : NW; }
+  static constexpr int Q(int d) { return d == 0 ? QU_ : d == 1 ? QV_ : QW_; }
+  static constexpr int H(int d) { return (Q(d) + 1) / 2; }  // half rule incl. centre
+  static constexpr int kind(int s, int d) {
+    const int k[] = {TK...};
+    return (k[s] >> (2 * d)) & 3;
+  }
+  static constexpr int K(int s, int d) { return kernel_count(kind(s, d), N(d)); }
+  static constexpr int toff(int s, int d) {  // half-table offsets in the param block
+    int o = 0;
+    for (int t = 0; t <= s; ++t)
+      for (int e = 0; e < 3; ++e) {
+        if (t == s && e == d) return o;
+        o += K(t, e) * H(e);
+      }
+    return o;
+  }
+  static constexpr int TTOT = toff(S - 1, 2) + K(S - 1, 2) * H(2);
+  static constexpr int moff(int s) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) o += K(i, 0) * K(i, 1) * K(i, 2);
+    return o;
+  }
+  static constexpr int MPP = (moff(S) + 3) & ~3;
+  static constexpr int S2 = Q(1) | 1, S3 = Q(2) | 1;
+  static constexpr int t1_dbl(int s) { return K(s, 0) * Q(2) * S2; }
+  static constexpr int t2_dbl(int s) { return K(s, 0) * K(s, 1) * S3; }
+  static constexpr int scratch_dbl() {
+    int m = 0;
+    for (int s = 0; s < S; ++s) {
+      const int v = t1_dbl(s) + t2_dbl(s);
+      m = v > m ? v : m;
+    }
+    return (m + 1) & ~1;
+  }
+  static constexpr size_t SMEM = sizeof(double) * (size_t)scratch_dbl();
+};
+
+template <class Ms>
+struct MV2Params {
+  const double* alpha;
+  double* I;
+  int64_t n_units;     // E * P * S
+  int P;
+  int64_t mom_per_elem;
+  double tab[Ms::TTOT];  // per (s, d): [K][H] = w_h P_k(x_h), h < H (x_h <= 0)
+};
+
+// Even/odd folded contraction of one register fiber a[Q] against the half
+// table tb[K][H]; out(k, value) receives each result.
+template <int Q, int K, class Out>
+__device__ __forceinline__ void fold_contract(const double (&a)[Q], const double* tb, Out&& out) {
+  constexpr int Hf = Q / 2;
+  constexpr int H = (Q + 1) / 2;
+  double ev[Hf > 0 ? Hf : 1], od[Hf > 0 ? Hf : 1];
+#pragma unroll
+  for (int h = 0; h < Hf; ++h) {
+    ev[h] = a[h] + a[Q - 1 - h];
+    od[h] = a[h] - a[Q - 1 - h];
+  }
+  static_for<0, K>([&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    double v = 0.0;
+    if constexpr ((k & 1) == 0) {
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) v = fma(tb[k * H + h], ev[h], v);
+      if constexpr (Q & 1) v = fma(tb[k * H + Hf], a[Hf], v);
+    } else {
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) v = fma(tb[k * H + h], od[h], v);
+    }
+    out(k, v);
+  });
+}
+
+// Moments of one (alpha slab, term) into Iout (global or shared), using the
+// smem scratch T1/T2.  All threads of the CTA participate; ends with a
+// __syncthreads().
+template <class Ms, int s>
+__device__ __forceinline__ void moments_unit(const double* __restrict__ a, const double* tab,
+                                             double* scratch, double* Iout) {
+  constexpr int QU = Ms::Q(0), QV = Ms::Q(1), QW = Ms::Q(2);
+  constexpr int KU = Ms::K(s, 0), KV = Ms::K(s, 1), KW = Ms::K(s, 2);
+  constexpr int S2 = Ms::S2, S3 = Ms::S3;
+  double* T1 = scratch;                    // [KU][QW][S2]
+  double* T2 = scratch + Ms::t1_dbl(s);    // [KU*KV][S3]
+  const int tid = threadIdx.x;
+  const double* tu = tab + Ms::toff(s, 0);
+  const double* tv = tab + Ms::toff(s, 1);
+  const double* tw = tab + Ms::toff(s, 2);
+
+  for (int r = tid; r < QW * QV; r += Ms::THREADS) {
+    const int q3 = r / QV, q2 = r - (r / QV) * QV;
+    double x[QU];
+    if constexpr ((QU & 1) == 0) {
+      const double2* row = reinterpret_cast<const double2*>(a + static_cast<int64_t>(r) * QU);
+#pragma unroll
+      for (int q = 0; q < QU / 2; ++q) {
+        const double2 v = __ldg(row + q);
+        x[2 * q] = v.x;
+        x[2 * q + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < QU; ++q) x[q] = __ldg(a + static_cast<int64_t>(r) * QU + q);
+    }
+    fold_contract<QU, KU>(x, tu, [&](int k, double v) { T1[(k * QW + q3) * S2 + q2] = v; });
+  }
+  __syncthreads();
+  for (int r = tid; r < KU * QW; r += Ms::THREADS) {
+    const int k1 = r / QW, q3 = r - (r / QW) * QW;
+    const double* src = T1 + (k1 * QW + q3) * S2;
+    double x[QV];
+#pragma unroll
+    for (int q = 0; q < QV; ++q) x[q] = src[q];
+    fold_contract<QV, KV>(x, tv, [&](int k, double v) { T2[(k1 * KV + k) * S3 + q3] = v; });
+  }
+  __syncthreads();
+  for (int r = tid; r < KU * KV; r += Ms::THREADS) {
+    const double* src = T2 + r * S3;
+    double x[QW];
+#pragma unroll
+    for (int q = 0; q < QW; ++q) x[q] = src[q];
+    fold_contract<QW, KW>(x, tw, [&](int k, double v) { Iout[r * KW + k] = v; });
+  }
+  __syncthreads();
+}
+
+// one CTA per (element, pair, term)
+template <class Ms>
+__global__ void __launch_bounds__(Ms::THREADS) moments_v2_kernel(const __grid_constant__ MV2Params<Ms> p) {
+  extern __shared__ __align__(16) double sm[];
+  const int64_t unit = blockIdx.x;
+  const int ps = static_cast<int>(unit % (p.P * Ms::S));
+  const int64_t e = unit / (p.P * Ms::S);
+  const int pair = ps / Ms::S, s = ps - pair * Ms::S;
+  constexpr int slab = Ms::Q(0) * Ms::Q(1) * Ms::Q(2);
+  const double* a = p.alpha + unit * slab;
+  double* base = p.I + e * p.mom_per_elem + static_cast<int64_t>(pair) * Ms::MPP;
+  static_for<0, Ms::S>([&](auto sc) {
+    constexpr int ss = decltype(sc)::value;
+    if (s == ss) moments_unit<Ms, ss>(a, p.tab, sm, base + Ms::moff(ss));
+  });
+}
+
+}  // namespace p2s
