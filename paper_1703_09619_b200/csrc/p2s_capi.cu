@@ -276,28 +276,46 @@ V2Entry make_v2() {
 constexpr int kPPP = enc_kind(PP, PP, PP);
 constexpr int kDDD = enc_kind(DD, DD, DD);
 
-// <N_u, N_v, N_w, n1 tile, threads, min CTAs/SM, term kinds...>
+// <N_u, N_v, N_w, n1 tile, p1 tile, threads, min CTAs/SM, A once per unit, fibers per
+//  thread, term kinds...>.  Several variants per shape: the first is the default,
+//  P2S_V2_VARIANT=k selects the k-th match (tuning).
 const std::vector<V2Entry>& v2_registry() {
   static const std::vector<V2Entry> reg = {
-      make_v2<Shape<4, 4, 4, 4, 256, 2, kPPP>>(),          // C1
-      make_v2<Shape<6, 6, 6, 1, 224, 2, kPPP, kDDD>>(),    // C2
-      make_v2<Shape<8, 8, 8, 1, 512, 1, kPPP, kDDD>>(),    // C3
-      make_v2<Shape<10, 6, 4, 2, 192, 2, kPPP, kDDD>>(),   // C4
-      make_v2<Shape<3, 3, 3, 3, 96, 4, kPPP, kDDD>>(),     // small vector test shape
-      make_v2<Shape<4, 3, 3, 3, 96, 4, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+      make_v2<Shape<4, 4, 4, 4, 4, 256, 2, 1, 1, kPPP>>(),                 // C1
+      make_v2<Shape<6, 6, 6, 1, 6, 224, 2, 1, 1, kPPP, kDDD>>(),           // C2
+      make_v2<Shape<6, 6, 6, 1, 6, 224, 2, 0, 1, kPPP, kDDD>>(),
+      make_v2<Shape<6, 6, 6, 2, 6, 224, 2, 0, 2, kPPP, kDDD>>(),
+      make_v2<Shape<6, 6, 6, 2, 6, 224, 1, 1, 2, kPPP, kDDD>>(),
+      make_v2<Shape<6, 6, 6, 1, 6, 128, 3, 0, 2, kPPP, kDDD>>(),
+      make_v2<Shape<6, 6, 6, 1, 3, 128, 3, 0, 1, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 8, 512, 1, 0, 1, kPPP, kDDD>>(),           // C3
+      make_v2<Shape<8, 8, 8, 1, 2, 128, 2, 0, 1, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 4, 256, 1, 0, 1, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 8, 256, 1, 0, 2, kPPP, kDDD>>(),
+      make_v2<Shape<10, 6, 4, 2, 4, 192, 2, 0, 1, kPPP, kDDD>>(),          // C4
+      make_v2<Shape<10, 6, 4, 2, 4, 192, 2, 1, 1, kPPP, kDDD>>(),
+      make_v2<Shape<10, 6, 4, 3, 4, 160, 2, 1, 2, kPPP, kDDD>>(),
+      make_v2<Shape<3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>>(),            // test shapes
+      make_v2<Shape<3, 3, 3, 1, 1, 64, 4, 1, 2, kPPP, kDDD>>(),
+      make_v2<Shape<4, 3, 3, 3, 3, 96, 4, 0, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
   };
   return reg;
 }
 
 const V2Entry* find_v2(const p2s_problem& pb) {
+  int want = 0, seen = 0;
+  if (const char* v = std::getenv("P2S_V2_VARIANT")) want = std::atoi(v);
+  const V2Entry* first = nullptr;
   for (const V2Entry& r : v2_registry()) {
     bool ok = r.S == pb.n_terms;
     for (int d = 0; d < 3; ++d) ok = ok && r.order[d] == pb.order[d];
     for (int s = 0; ok && s < r.S; ++s)
       for (int d = 0; d < 3; ++d) ok = ok && r.kinds[s][d] == pb.kind[s][d];
-    if (ok) return &r;
+    if (!ok) continue;
+    if (!first) first = &r;
+    if (seen++ == want) return &r;
   }
-  return nullptr;
+  return first;
 }
 
 // ------------------------------------------------------------ shape-specialised moments

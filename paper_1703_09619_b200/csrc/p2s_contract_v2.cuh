@@ -7,16 +7,18 @@
 //   I  -> smem            one bulk copy (TMA engine, cp.async.bulk) on an
 //                         mbarrier; the next unit's copy is issued as soon as
 //                         the last stage A of this unit has read I
-// and per tile of T n1-values:
 //   stage A (v):  thread = fiber (k1, k3) of I_s, Kv values in registers;
-//                 A_s[i][k1][n2][k3] = sum_k2 Cv[n1][n2][k2] I_s[k1][k2][k3]
-//   stage B (w):  thread = fiber (i, k1, n2) of A_s, Kw values in registers;
-//                 B_s[i][k1][p1][n2][p2] = sum_k3 Cw[p1][p2][k3] A_s[i][k1][n2][k3]
-//   stage C (u):  thread = fiber (i, p1, n2, p2) of B_s over all terms;
+//                 A_s[n1][k1][n2][k3] = sum_k2 Cv[n1][n2][k2] I_s[k1][k2][k3]
+//                 (all n1 at once when AALL, else per n1 tile)
+// and per tile of T n1-values:
+//   stage B (w):  thread = (fiber (i, k1, n2) of A_s, p1), Kw values in registers;
+//                 B_s[i][k1][p1][n2][p2] = sum_k3 Cw[p1][p2][k3] A_s[n1][k1][n2][k3]
+//   stage C (u):  thread = FPT fibers (i, p1, n2, p2) of B over all terms;
 //                 M[m1 n1 p1][m2 n2 p2] = sum_s sum_k1 Cu[m1][m2][k1] B_s[..k1..]
 // Every output loop is unrolled with compile-time bands, every coefficient is
-// a constant-bank operand, every fiber is register resident: one DFMA per
-// product-to-sum term and one store per element-matrix entry.
+// a constant-bank operand shared by the thread's FPT fibers, every fiber is
+// register resident: one DFMA per product-to-sum term and one store per
+// element-matrix entry.
 #pragma once
 
 #include "p2s_kernels.cuh"
@@ -25,12 +27,18 @@ namespace p2s {
 
 constexpr int enc_kind(int ku, int kv, int kw) { return ku | (kv << 2) | (kw << 4); }
 
-template <int NU_, int NV_, int NW_, int T_, int THREADS_, int MINB_, int... TK>
+// AALL: stage A for all n1 once per unit; FPT: stage-C fibers per thread.
+template <int NU_, int NV_, int NW_, int T_, int P1T_, int THREADS_, int MINB_, int AALL_, int FPT_,
+          int... TK>
 struct Shape {
   static constexpr int NU = NU_, NV = NV_, NW = NW_, T = T_, THREADS = THREADS_, MINB = MINB_;
+  static constexpr int AALL = AALL_, FPT = FPT_, P1T = P1T_;
+  static constexpr int NP1 = NW_ / P1T_;
+  static_assert(NW_ % P1T_ == 0, "p1 tile must divide N_w");
   static constexpr int S = sizeof...(TK);
   static constexpr int NT = NV / T;
   static_assert(NV % T == 0, "n1 tile must divide N_v");
+  static constexpr int AT = AALL ? NV : T;  // n1 slots held in the A buffer
   static constexpr int N(int d) { return d == 0 ? NU : d == 1 ? NV : NW; }
   static constexpr int kind(int s, int d) {
     const int k[] = {TK...};
@@ -68,11 +76,24 @@ struct Shape {
     return o;
   }
   static constexpr int MPP = (moff(S) + 3) & ~3;
+  // fiber counts / prefix sums over terms
+  static constexpr int fa(int s) { return K(s, 0) * K(s, 2); }                // stage A fibers
+  static constexpr int fb(int s) { return T * K(s, 0) * NV * P1T; }          // stage B items
+  static constexpr int fa_off(int s) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) o += fa(i);
+    return o;
+  }
+  static constexpr int fb_off(int s) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) o += fb(i);
+    return o;
+  }
   // smem (doubles)
-  static constexpr int BSTR = (NW * NV * NW) | 1;  // odd k1 stride of B
+  static constexpr int BSTR = (P1T * NV * NW) | 1;  // odd k1 stride of B
   static constexpr int aoff(int s) {
     int o = 0;
-    for (int i = 0; i < s; ++i) o += T * K(i, 0) * NV * K(i, 2);
+    for (int i = 0; i < s; ++i) o += AT * K(i, 0) * NV * K(i, 2);
     return o;
   }
   static constexpr int boff(int s) {
@@ -98,34 +119,104 @@ struct V2Params {
   double cw[Sh::ctot(2)];
 };
 
-template <class Sh, int N1>
-__device__ __forceinline__ void v2_stage_a_n1(const V2Params<Sh>& p, const double* Ibuf,
-                                              double* Abuf, int i) {
-  // one n1 value (compile-time) of the tile, slot i
+// Stage A for the n1 values N1 .. N1+CNT-1 (compile-time), stored at slots
+// SLOT0 .. of the A buffer.  Fibers of all terms in one loop.
+template <class Sh, int N1, int CNT, int SLOT0>
+__device__ __forceinline__ void v2_stage_a(const V2Params<Sh>& p, const double* Ibuf, double* Abuf) {
   constexpr int NV = Sh::NV;
+  constexpr int FTOT = Sh::fa_off(Sh::S);
+  for (int f = threadIdx.x; f < FTOT; f += Sh::THREADS) {
+    static_for<0, Sh::S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      if (f >= Sh::fa_off(s) && f < Sh::fa_off(s) + Sh::fa(s)) {
+        constexpr int Ku = Sh::K(s, 0), Kv = Sh::K(s, 1), Kw = Sh::K(s, 2);
+        constexpr int kv = Sh::kind(s, 1);
+        const int g = f - Sh::fa_off(s);
+        const int k1 = g / Kw, k3 = g - (g / Kw) * Kw;
+        const double* Is = Ibuf + Sh::moff(s);
+        double x[Kv];
+#pragma unroll
+        for (int k2 = 0; k2 < Kv; ++k2) x[k2] = Is[(k1 * Kv + k2) * Kw + k3];
+        static_for<0, CNT>([&](auto ic) {
+          constexpr int i = decltype(ic)::value;
+          constexpr int n1 = N1 + i;
+          double* As = Abuf + Sh::aoff(s) + (SLOT0 + i) * (Ku * NV * Kw);
+          static_for<0, NV>([&](auto n2c) {
+            constexpr int n2 = decltype(n2c)::value;
+            constexpr int lo = band_lo(kv, n1, n2), cnt = band_count(kv, n1, n2);
+            constexpr int co = Sh::coff(1, s, n1, n2);
+            double v = 0.0;
+            static_for<0, cnt>([&](auto jc) {
+              constexpr int j = decltype(jc)::value;
+              v = fma(p.cv[co + j], x[lo + 2 * j], v);
+            });
+            As[(k1 * NV + n2) * Kw + k3] = v;
+          });
+        });
+      }
+    });
+  }
+}
+
+// Stage B for the current tile: item = (s, (i*Ku + k1)*NV + n2, p1) with p1
+// slowest inside a term, so p1 (and its compile-time band) is warp-uniform
+// except at boundaries.
+template <class Sh>
+__device__ __forceinline__ void v2_stage_b(const V2Params<Sh>& p, const double* Abuf, double* Bbuf,
+                                           int aslot0, int p1base) {
+  constexpr int NV = Sh::NV, NW = Sh::NW, T = Sh::T;
+  constexpr int FTOT = Sh::fb_off(Sh::S);
+  for (int f = threadIdx.x; f < FTOT; f += Sh::THREADS) {
+    static_for<0, Sh::S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      if (f >= Sh::fb_off(s) && f < Sh::fb_off(s) + Sh::fb(s)) {
+        constexpr int Ku = Sh::K(s, 0), Kw = Sh::K(s, 2);
+        constexpr int kw = Sh::kind(s, 2);
+        constexpr int NFIB = T * Ku * NV;
+        const int g = f - Sh::fb_off(s);
+        const int p1l = g / NFIB;
+        const int p1 = p1base + p1l;
+        const int fib = g - p1l * NFIB;         // (i*Ku + k1)*NV + n2
+        const int n2 = fib % NV;
+        const int ik = fib / NV;                // i*Ku + k1
+        const int i = ik / Ku, k1 = ik - i * Ku;
+        const double* src =
+            Abuf + Sh::aoff(s) + (((aslot0 + i) * Ku + k1) * NV + n2) * Kw;
+        double y[Kw];
+#pragma unroll
+        for (int k3 = 0; k3 < Kw; ++k3) y[k3] = src[k3];
+        double* dst = Bbuf + Sh::boff(s) + ik * Sh::BSTR + n2 * NW;
+        static_for<0, NW>([&](auto p1c) {
+          constexpr int pp1 = decltype(p1c)::value;
+          if (p1 == pp1) {
+            static_for<0, NW>([&](auto p2c) {
+              constexpr int p2 = decltype(p2c)::value;
+              constexpr int lo = band_lo(kw, pp1, p2), cnt = band_count(kw, pp1, p2);
+              constexpr int co = Sh::coff(2, s, pp1, p2);
+              double v = 0.0;
+              static_for<0, cnt>([&](auto jc) {
+                constexpr int j = decltype(jc)::value;
+                v = fma(p.cw[co + j], y[lo + 2 * j], v);
+              });
+              dst[p1l * NV * NW + p2] = v;
+            });
+          }
+        });
+      }
+    });
+  }
+}
+
+template <class Sh>
+__device__ __forceinline__ void v2_load_fiber(const double* Bbuf, int i, int p1, int r,
+                                              double (&b)[Sh::KTOT_U()]) {
+  constexpr int NV = Sh::NV, NW = Sh::NW;
   static_for<0, Sh::S>([&](auto sc) {
     constexpr int s = decltype(sc)::value;
-    constexpr int Ku = Sh::K(s, 0), Kv = Sh::K(s, 1), Kw = Sh::K(s, 2);
-    constexpr int kv = Sh::kind(s, 1);
-    const double* Is = Ibuf + Sh::moff(s);
-    double* As = Abuf + Sh::aoff(s) + i * (Ku * NV * Kw);
-    for (int f = threadIdx.x; f < Ku * Kw; f += Sh::THREADS) {
-      const int k1 = f / Kw, k3 = f - (f / Kw) * Kw;
-      double x[Kv];
+    constexpr int Ku = Sh::K(s, 0);
+    const double* src = Bbuf + Sh::boff(s) + (i * Ku) * Sh::BSTR + p1 * NV * NW + r;  // p1 local
 #pragma unroll
-      for (int k2 = 0; k2 < Kv; ++k2) x[k2] = Is[(k1 * Kv + k2) * Kw + k3];
-      static_for<0, NV>([&](auto n2c) {
-        constexpr int n2 = decltype(n2c)::value;
-        constexpr int lo = band_lo(kv, N1, n2), cnt = band_count(kv, N1, n2);
-        constexpr int co = Sh::coff(1, s, N1, n2);
-        double v = 0.0;
-        static_for<0, cnt>([&](auto jc) {
-          constexpr int j = decltype(jc)::value;
-          v = fma(p.cv[co + j], x[lo + 2 * j], v);
-        });
-        As[(k1 * NV + n2) * Kw + k3] = v;
-      });
-    }
+    for (int k1 = 0; k1 < Ku; ++k1) b[Sh::kuoff(s) + k1] = src[k1 * Sh::BSTR];
   });
 }
 
@@ -133,7 +224,7 @@ template <class Sh>
 __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     contract_v2_kernel(const __grid_constant__ V2Params<Sh> p) {
   extern __shared__ __align__(16) double sm[];
-  constexpr int S = Sh::S, NU = Sh::NU, NV = Sh::NV, NW = Sh::NW, T = Sh::T;
+  constexpr int S = Sh::S, NU = Sh::NU, NV = Sh::NV, NW = Sh::NW, T = Sh::T, FPT = Sh::FPT;
   double* Ibuf = sm;
   double* Abuf = Ibuf + Sh::MPP;
   double* Bbuf = Abuf + Sh::A_DBL;
@@ -154,6 +245,18 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
   }
   __syncthreads();
   uint32_t phase = 0;
+  auto issue_next = [&]() {
+    if (tid == 0) {
+      const int64_t nxt = unit + gridDim.x;
+      if (nxt < p.n_units) {
+        const int64_t e2 = nxt / p.P;
+        const int pair2 = static_cast<int>(nxt - e2 * p.P);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(bar, kIBytes);
+        bulk_g2s(Ibuf, p.I + e2 * p.mom_per_elem + pair2 * Sh::MPP, kIBytes, bar);
+      }
+    }
+  };
   for (; unit < p.n_units; unit += gridDim.x) {
     const int64_t e = unit / p.P;
     const int pair = static_cast<int>(unit - e * p.P);
@@ -161,84 +264,51 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     mbar_wait_parity(bar, phase);
     phase ^= 1u;
     double* Mbase = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt) * p.ldM + gcj * p.Nt;
+    if constexpr (Sh::AALL) {
+      v2_stage_a<Sh, 0, NV, 0>(p, Ibuf, Abuf);
+      __syncthreads();
+      issue_next();
+    }
 
     for (int t = 0; t < Sh::NT; ++t) {
-      // ---- stage A
-      static_for<0, Sh::NT>([&](auto tc) {
-        constexpr int tt = decltype(tc)::value;
-        if (t == tt) {
-          static_for<0, T>([&](auto ic) {
-            constexpr int i = decltype(ic)::value;
-            v2_stage_a_n1<Sh, tt * T + i>(p, Ibuf, Abuf, i);
-          });
-        }
-      });
-      __syncthreads();
-      if (t == Sh::NT - 1 && tid == 0) {
-        const int64_t nxt = unit + gridDim.x;
-        if (nxt < p.n_units) {
-          const int64_t e2 = nxt / p.P;
-          const int pair2 = static_cast<int>(nxt - e2 * p.P);
-          fence_proxy_async_smem();
-          mbar_arrive_expect_tx(bar, kIBytes);
-          bulk_g2s(Ibuf, p.I + e2 * p.mom_per_elem + pair2 * Sh::MPP, kIBytes, bar);
-        }
+      if constexpr (!Sh::AALL) {
+        static_for<0, Sh::NT>([&](auto tc) {
+          constexpr int tt = decltype(tc)::value;
+          if (t == tt) v2_stage_a<Sh, tt * T, T, 0>(p, Ibuf, Abuf);
+        });
+        __syncthreads();
+        if (t == Sh::NT - 1) issue_next();
       }
-      // ---- stage B
-      static_for<0, S>([&](auto sc) {
-        constexpr int s = decltype(sc)::value;
-        constexpr int Ku = Sh::K(s, 0), Kw = Sh::K(s, 2);
-        constexpr int kw = Sh::kind(s, 2);
-        const double* As = Abuf + Sh::aoff(s);
-        double* Bs = Bbuf + Sh::boff(s);
-        for (int f = tid; f < T * Ku * NV; f += Sh::THREADS) {
-          // f = (i*Ku + k1)*NV + n2
-          const int n2 = f % NV;
-          const int ik = f / NV;
-          double y[Kw];
-#pragma unroll
-          for (int k3 = 0; k3 < Kw; ++k3) y[k3] = As[f * Kw + k3];
-          double* dst = Bs + ik * Sh::BSTR + n2 * NW;
-          static_for<0, NW>([&](auto p1c) {
-            constexpr int p1 = decltype(p1c)::value;
-            static_for<0, NW>([&](auto p2c) {
-              constexpr int p2 = decltype(p2c)::value;
-              constexpr int lo = band_lo(kw, p1, p2), cnt = band_count(kw, p1, p2);
-              constexpr int co = Sh::coff(2, s, p1, p2);
-              double v = 0.0;
-              static_for<0, cnt>([&](auto jc) {
-                constexpr int j = decltype(jc)::value;
-                v = fma(p.cw[co + j], y[lo + 2 * j], v);
-              });
-              dst[p1 * NV * NW + p2] = v;
-            });
-          });
-        }
-      });
+      for (int pt = 0; pt < Sh::NP1; ++pt) {
+      v2_stage_b<Sh>(p, Abuf, Bbuf, Sh::AALL ? t * T : 0, pt * Sh::P1T);
       __syncthreads();
       // ---- stage C
-      constexpr int NF = T * NW * NV * NW;
-      for (int f = tid; f < NF; f += Sh::THREADS) {
-        // f = ((i*NW + p1)*NV + n2)*NW + p2
-        const int r = f % (NV * NW);  // n2*NW + p2
-        const int ip = f / (NV * NW);
-        const int p1 = ip % NW, i = ip / NW;
-        const int n1 = t * T + i;
-        double b[Sh::KTOT_U()];
-        static_for<0, S>([&](auto sc) {
-          constexpr int s = decltype(sc)::value;
-          constexpr int Ku = Sh::K(s, 0);
-          const double* src = Bbuf + Sh::boff(s) + (i * Ku) * Sh::BSTR + p1 * NV * NW + r;
+      constexpr int NF = T * Sh::P1T * NV * NW;   // fibers of the sub-tile
+      constexpr int NFT = (NF + FPT - 1) / FPT;
+      const int64_t rowstep = static_cast<int64_t>(NV * NW) * p.ldM;
+      for (int f0 = tid; f0 < NFT; f0 += Sh::THREADS) {
+        double b[FPT][Sh::KTOT_U()];
+        double* out[FPT];
+        bool live[FPT];
 #pragma unroll
-          for (int k1 = 0; k1 < Ku; ++k1) b[Sh::kuoff(s) + k1] = src[k1 * Sh::BSTR];
-        });
-        double* out = Mbase + static_cast<int64_t>(n1 * NW + p1) * p.ldM + r;
-        const int64_t rowstep = static_cast<int64_t>(NV * NW) * p.ldM;
+        for (int q = 0; q < FPT; ++q) {
+          const int f = f0 + q * NFT;  // f = ((i*P1T + p1l)*NV + n2)*NW + p2
+          live[q] = f < NF;
+          const int fs = live[q] ? f : 0;
+          const int r = fs % (NV * NW);
+          const int ip = fs / (NV * NW);
+          const int p1l = ip % Sh::P1T, i = ip / Sh::P1T;
+          const int n1 = t * T + i, p1 = pt * Sh::P1T + p1l;
+          v2_load_fiber<Sh>(Bbuf, i, p1l, r, b[q]);
+          out[q] = Mbase + static_cast<int64_t>(n1 * NW + p1) * p.ldM + r;
+        }
         static_for<0, NU>([&](auto m1c) {
           constexpr int m1 = decltype(m1c)::value;
           static_for<0, NU>([&](auto m2c) {
             constexpr int m2 = decltype(m2c)::value;
-            double v = 0.0;
+            double v[FPT];
+#pragma unroll
+            for (int q = 0; q < FPT; ++q) v[q] = 0.0;
             static_for<0, S>([&](auto sc) {
               constexpr int s = decltype(sc)::value;
               constexpr int ku = Sh::kind(s, 0);
@@ -247,14 +317,19 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
               constexpr int ko = Sh::kuoff(s);
               static_for<0, cnt>([&](auto jc) {
                 constexpr int j = decltype(jc)::value;
-                v = fma(p.cu[co + j], b[ko + lo + 2 * j], v);
+                const double c = p.cu[co + j];
+#pragma unroll
+                for (int q = 0; q < FPT; ++q) v[q] = fma(c, b[q][ko + lo + 2 * j], v[q]);
               });
             });
-            st_cs(out + m1 * rowstep + m2 * (NV * NW), v);
+#pragma unroll
+            for (int q = 0; q < FPT; ++q)
+              if (live[q]) st_cs(out[q] + m1 * rowstep + m2 * (NV * NW), v[q]);
           });
         });
       }
       __syncthreads();
+      }  // p1 sub-tiles
     }
   }
 }

@@ -1,0 +1,76 @@
+// tools/peaks.cu -- roofline denominators not in MEASURED_PEAKS.json:
+//   write-only HBM bandwidth (8-B and 16-B streaming stores, like the fill's),
+//   read+write copy bandwidth, and FP64 FMA throughput (DFMA).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/peaks tools/peaks.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void write8(double* p, size_t n, double v) {
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+  for (; i < n; i += st) __stcs(p + i, v + i);
+}
+__global__ void write16(double2* p, size_t n, double v) {
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+  for (; i < n; i += st) __stcs(p + i, make_double2(v, v + i));
+}
+__global__ void copy16(const double2* a, double2* b, size_t n) {
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+  for (; i < n; i += st) b[i] = __ldcs(a + i);
+}
+__global__ void dfma_loop(double* out, int iters, double a, double b) {
+  double x[8];
+  for (int j = 0; j < 8; ++j) x[j] = threadIdx.x * 1e-3 + j;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = fma(x[j], a, b);
+  double s = 0;
+  for (int j = 0; j < 8; ++j) s += x[j];
+  if (s == 12345.678) out[0] = s;
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const size_t bytes = size_t(8) << 30;
+  double *a, *b;
+  cudaMalloc(&a, bytes);
+  cudaMalloc(&b, bytes);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float ms, best;
+  const size_t n8 = bytes / 8, n16 = bytes / 16;
+  auto bw = [&](const char* name, auto launch, double moved) {
+    best = 1e30f;
+    for (int r = 0; r < 8; ++r) {
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r >= 2 && ms < best) best = ms;
+    }
+    printf("{\"test\": \"%s\", \"GB_s\": %.1f}\n", name, moved / (best * 1e-3) / 1e9);
+  };
+  bw("write_8B_stcs", [&] { write8<<<sms * 8, 256>>>(a, n8, 1.0); }, (double)bytes);
+  bw("write_16B_stcs", [&] { write16<<<sms * 8, 256>>>((double2*)a, n16, 1.0); }, (double)bytes);
+  bw("memset", [&] { cudaMemsetAsync(a, 0, bytes); }, (double)bytes);
+  bw("copy_16B", [&] { copy16<<<sms * 8, 256>>>((double2*)a, (double2*)b, n16); }, 2.0 * bytes);
+  // FP64 FMA throughput
+  const int iters = 1 << 14;
+  best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    dfma_loop<<<sms * 4, 512>>>(b, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 1 && ms < best) best = ms;
+  }
+  const double flops = 2.0 * 8 * iters * (double)sms * 4 * 512;
+  printf("{\"test\": \"dfma\", \"TFLOP_s\": %.2f}\n", flops / (best * 1e-3) / 1e12);
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  printf("{\"sms\": %d, \"max_clock_mhz\": %d}\n", sms, clk / 1000);
+  return 0;
+}
