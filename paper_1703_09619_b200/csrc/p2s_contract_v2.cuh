@@ -28,11 +28,13 @@ namespace p2s {
 constexpr int enc_kind(int ku, int kv, int kw) { return ku | (kv << 2) | (kw << 4); }
 
 // AALL: stage A for all n1 once per unit; FPT: stage-C fibers per thread.
-template <int NU_, int NV_, int NW_, int T_, int P1T_, int THREADS_, int MINB_, int AALL_, int FPT_,
-          int... TK>
+template <int NU_, int NV_, int NW_, int T_, int P1T_, int PG_, int THREADS_, int MINB_, int AALL_,
+          int FPT_, int... TK>
 struct Shape {
   static constexpr int NU = NU_, NV = NV_, NW = NW_, T = T_, THREADS = THREADS_, MINB = MINB_;
-  static constexpr int AALL = AALL_, FPT = FPT_, P1T = P1T_;
+  static constexpr int AALL = AALL_, FPT = FPT_, P1T = P1T_, PG = PG_;
+  static constexpr int NPG = P1T_ / PG_;
+  static_assert(P1T_ % PG_ == 0, "p1 group must divide the p1 tile");
   static constexpr int NP1 = NW_ / P1T_;
   static_assert(NW_ % P1T_ == 0, "p1 tile must divide N_w");
   static constexpr int S = sizeof...(TK);
@@ -78,7 +80,7 @@ struct Shape {
   static constexpr int MPP = (moff(S) + 3) & ~3;
   // fiber counts / prefix sums over terms
   static constexpr int fa(int s) { return K(s, 0) * K(s, 2); }                // stage A fibers
-  static constexpr int fb(int s) { return T * K(s, 0) * NV * P1T; }          // stage B items
+  static constexpr int fb(int s) { return T * K(s, 0) * NV * NPG; }          // stage B items
   static constexpr int fa_off(int s) {
     int o = 0;
     for (int i = 0; i < s; ++i) o += fa(i);
@@ -174,9 +176,8 @@ __device__ __forceinline__ void v2_stage_b(const V2Params<Sh>& p, const double* 
         constexpr int kw = Sh::kind(s, 2);
         constexpr int NFIB = T * Ku * NV;
         const int g = f - Sh::fb_off(s);
-        const int p1l = g / NFIB;
-        const int p1 = p1base + p1l;
-        const int fib = g - p1l * NFIB;         // (i*Ku + k1)*NV + n2
+        const int pg = g / NFIB;
+        const int fib = g - pg * NFIB;          // (i*Ku + k1)*NV + n2
         const int n2 = fib % NV;
         const int ik = fib / NV;                // i*Ku + k1
         const int i = ik / Ku, k1 = ik - i * Ku;
@@ -186,22 +187,27 @@ __device__ __forceinline__ void v2_stage_b(const V2Params<Sh>& p, const double* 
 #pragma unroll
         for (int k3 = 0; k3 < Kw; ++k3) y[k3] = src[k3];
         double* dst = Bbuf + Sh::boff(s) + ik * Sh::BSTR + n2 * NW;
-        static_for<0, NW>([&](auto p1c) {
-          constexpr int pp1 = decltype(p1c)::value;
-          if (p1 == pp1) {
-            static_for<0, NW>([&](auto p2c) {
-              constexpr int p2 = decltype(p2c)::value;
-              constexpr int lo = band_lo(kw, pp1, p2), cnt = band_count(kw, pp1, p2);
-              constexpr int co = Sh::coff(2, s, pp1, p2);
-              double v = 0.0;
-              static_for<0, cnt>([&](auto jc) {
-                constexpr int j = decltype(jc)::value;
-                v = fma(p.cw[co + j], y[lo + 2 * j], v);
+#pragma unroll
+        for (int jg = 0; jg < Sh::PG; ++jg) {
+          const int p1l = pg * Sh::PG + jg;
+          const int p1 = p1base + p1l;
+          static_for<0, NW>([&](auto p1c) {
+            constexpr int pp1 = decltype(p1c)::value;
+            if (p1 == pp1) {
+              static_for<0, NW>([&](auto p2c) {
+                constexpr int p2 = decltype(p2c)::value;
+                constexpr int lo = band_lo(kw, pp1, p2), cnt = band_count(kw, pp1, p2);
+                constexpr int co = Sh::coff(2, s, pp1, p2);
+                double v = 0.0;
+                static_for<0, cnt>([&](auto jc) {
+                  constexpr int j = decltype(jc)::value;
+                  v = fma(p.cw[co + j], y[lo + 2 * j], v);
+                });
+                dst[p1l * NV * NW + p2] = v;
               });
-              dst[p1l * NV * NW + p2] = v;
-            });
-          }
-        });
+            }
+          });
+        }
       }
     });
   }
