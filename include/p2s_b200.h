@@ -139,6 +139,10 @@ const char* p2s_last_error(void);
 
 const char* p2s_version(void);
 
+/* Which kernels p2s_fill runs for this context (shape-specialised fused
+ * kernel, two-stage specialised, or the runtime-shaped generic kernels). */
+const char* p2s_kernel_path(const p2s_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,7 @@ _STATUS = {0: "P2S_OK", 1: "P2S_INVALID_ARG", 2: "P2S_CUDA_ERROR", 3: "P2S_UNSUP
 EXPORTS = ("p2s_create", "p2s_destroy", "p2s_get_sizes", "p2s_moments", "p2s_contract",
            "p2s_fill", "p2s_fill_host", "p2s_alpha_generate", "p2s_get_tables",
            "p2s_set_profiling", "p2s_get_stage_times", "p2s_shape_supported", "p2s_last_error",
-           "p2s_version")
+           "p2s_version", "p2s_kernel_path")
 
 
 class P2SError(RuntimeError):
@@ -100,8 +100,11 @@ def lib():
         L.p2s_shape_supported.restype = C.c_int
         L.p2s_last_error.restype = C.c_char_p
         L.p2s_version.restype = C.c_char_p
+        L.p2s_kernel_path.argtypes = [vp]
+        L.p2s_kernel_path.restype = C.c_char_p
         for f in EXPORTS:
-            if f not in ("p2s_destroy", "p2s_shape_supported", "p2s_last_error", "p2s_version"):
+            if f not in ("p2s_destroy", "p2s_shape_supported", "p2s_last_error", "p2s_version",
+                         "p2s_kernel_path"):
                 getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -215,6 +218,10 @@ class Context:
         _check(lib().p2s_get_tables(self.h, term, d, phi.ctypes.data_as(dp), coef.ctypes.data_as(dp),
                                     x.ctypes.data_as(dp), w.ctypes.data_as(dp)))
         return phi, coef, x, w
+
+    @property
+    def kernel_path(self) -> str:
+        return lib().p2s_kernel_path(self.h).decode()
 
     def set_profiling(self, enable: bool):
         _check(lib().p2s_set_profiling(self.h, int(enable)))

@@ -15,6 +15,7 @@
 
 #include "../../include/p2s_b200.h"
 #include "p2s_contract_v2.cuh"
+#include "p2s_fused.cuh"
 #include "p2s_moments_v2.cuh"
 #include "p2s_kernels.cuh"
 #include "p2s_tables.hpp"
@@ -408,6 +409,104 @@ const MV2Entry* find_mv2(const p2s_problem& pb) {
   return nullptr;
 }
 
+// ------------------------------------------------------------ fused fill registry
+
+using fused_fn = cudaError_t (*)(const double*, double*, int64_t, int64_t, int64_t, int, int, int,
+                                 const std::vector<double>&, const std::vector<double>&,
+                                 cudaStream_t, int);
+
+template <class Sh, class Ms>
+cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_tot, int64_t n_elem,
+                         int nc, int P, int Nt, const std::vector<double>& cpack,
+                         const std::vector<double>& mpack, cudaStream_t st, int num_sms) {
+  FusedParams<Sh, Ms> p;
+  p.c.I = nullptr;
+  p.c.M = M;
+  p.c.ldM = ldM;
+  p.c.mat_stride = n_tot * ldM;
+  p.c.n_units = n_elem * P;
+  p.c.nc = nc;
+  p.c.P = P;
+  p.c.Nt = Nt;
+  p.c.mom_per_elem = 0;
+  std::memcpy(p.c.cu, cpack.data(), sizeof(double) * Sh::ctot(0));
+  std::memcpy(p.c.cv, cpack.data() + Sh::ctot(0), sizeof(double) * Sh::ctot(1));
+  std::memcpy(p.c.cw, cpack.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));
+  p.alpha = alpha;
+  std::memcpy(p.tab, mpack.data(), sizeof(double) * Ms::TTOT);
+  if (p.c.n_units == 0) return cudaSuccess;
+  constexpr size_t smem = FusedLayout<Sh, Ms>::SMEM;
+  static int blocks_per_sm = -1;
+  if (blocks_per_sm < 0) {
+    cudaError_t e = cudaFuncSetAttribute(fill_fused_kernel<Sh, Ms>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fill_fused_kernel<Sh, Ms>, Sh::THREADS, smem);
+    if (e != cudaSuccess) return e;
+    if (b < 1) return cudaErrorInvalidConfiguration;
+    blocks_per_sm = b;
+  }
+  const int64_t grid = std::min<int64_t>(p.c.n_units, static_cast<int64_t>(blocks_per_sm) * num_sms);
+  fill_fused_kernel<Sh, Ms><<<static_cast<unsigned>(grid), Sh::THREADS, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+struct FusedEntry {
+  int order[3], nq[3], S;
+  int kinds[kMaxTerms][3];
+  fused_fn launch;
+  v2_pack_fn cpack;
+  mv2_pack_fn mpack;
+};
+
+template <class Sh, class Ms>
+FusedEntry make_fused() {
+  FusedEntry r{};
+  for (int d = 0; d < 3; ++d) {
+    r.order[d] = Sh::N(d);
+    r.nq[d] = Ms::Q(d);
+  }
+  r.S = Sh::S;
+  for (int s = 0; s < Sh::S; ++s)
+    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Sh::kind(s, d);
+  r.launch = &launch_fused<Sh, Ms>;
+  r.cpack = &pack_v2<Sh>;
+  r.mpack = &pack_mv2<Ms>;
+  return r;
+}
+
+const std::vector<FusedEntry>& fused_registry() {
+  static const std::vector<FusedEntry> reg = {
+      make_fused<Shape<4, 4, 4, 4, 4, 4, 256, 2, 1, 1, kPPP>,
+                 MShape<4, 4, 4, 8, 8, 8, 256, kPPP>>(),                              // C1
+      make_fused<Shape<6, 6, 6, 2, 6, 1, 224, 2, 0, 2, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 224, kPPP, kDDD>>(),                     // C2
+      make_fused<Shape<8, 8, 8, 1, 8, 4, 256, 1, 0, 2, kPPP, kDDD>,
+                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),                     // C3
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 0, 1, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),                    // C4
+      make_fused<Shape<3, 3, 3, 3, 3, 1, 96, 4, 0, 1, kPPP, kDDD>,
+                 MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),                         // tests
+      make_fused<Shape<4, 3, 3, 3, 3, 3, 96, 4, 0, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>,
+                 MShape<4, 3, 3, 9, 5, 7, 96, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+  };
+  return reg;
+}
+
+const FusedEntry* find_fused(const p2s_problem& pb) {
+  if (const char* v = std::getenv("P2S_NO_FUSED"))
+    if (v[0] == '1') return nullptr;
+  for (const FusedEntry& r : fused_registry()) {
+    bool ok = r.S == pb.n_terms;
+    for (int d = 0; d < 3; ++d) ok = ok && r.order[d] == pb.order[d] && r.nq[d] == pb.nq[d];
+    for (int s = 0; ok && s < r.S; ++s)
+      for (int d = 0; d < 3; ++d) ok = ok && r.kinds[s][d] == pb.kind[s][d];
+    if (ok) return &r;
+  }
+  return nullptr;
+}
+
 // ------------------------------------------------------------ moment launch
 
 template <int KMAX>
@@ -453,6 +552,8 @@ struct p2s_ctx {
   const RegEntry* entry = nullptr;
   const V2Entry* v2 = nullptr;
   const MV2Entry* mv2 = nullptr;
+  const FusedEntry* fused = nullptr;
+  std::vector<double> fused_cpack, fused_mpack;
   std::vector<double> mv2_packed;
   std::vector<double> v2_packed;
   int num_sms = 148;
@@ -476,7 +577,7 @@ struct p2s_ctx {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_mom, ev_con;
   double ms_mom = 0.0, ms_con = 0.0;
-  int64_t n_mom = 0, n_con = 0;
+  int64_t n_mom = 0, n_con = 0, n_fused = 0;
 };
 
 namespace {
@@ -626,6 +727,25 @@ p2s_status run_contract(p2s_ctx* c, const double* I, double* M, int64_t ldM, int
 
 p2s_status run_fill(p2s_ctx* c, const double* alpha, double* M, int64_t ldM, int64_t n,
                     cudaStream_t st) {
+  if (c->fused) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->prof) {
+      e0 = take_event(c);
+      e1 = take_event(c);
+      cudaEventRecord(e0, st);
+    }
+    cudaError_t err = c->fused->launch(alpha, M, ldM, c->sz.n_tot, n, c->pb.n_comp, c->sz.n_pairs,
+                                       c->pb.order[0] * c->pb.order[1] * c->pb.order[2],
+                                       c->fused_cpack, c->fused_mpack, st, c->num_sms);
+    if (err != cudaSuccess) return cuda_fail(err, "fill_fused_kernel launch");
+    if (c->prof) {
+      cudaEventRecord(e1, st);
+      c->ev_con.emplace_back(e0, e1);
+      ++c->n_con;
+      ++c->n_fused;
+    }
+    return P2S_OK;
+  }
   const int64_t ape = c->sz.alpha_per_elem;
   const int64_t mstride = static_cast<int64_t>(c->sz.n_tot) * ldM;
   for (int64_t e0 = 0; e0 < n; e0 += c->chunk) {
@@ -650,6 +770,16 @@ extern "C" {
 const char* p2s_last_error(void) { return g_last_error.c_str(); }
 
 const char* p2s_version(void) { return "p2s_b200 0.1 (sm_100a)"; }
+
+const char* p2s_kernel_path(const p2s_ctx* c) {
+  if (!c) return "";
+  if (c->fused) return "fused: fill_fused_kernel (moments + contraction, one persistent kernel)";
+  if (c->v2 && !c->force_generic)
+    return c->mv2 ? "two-stage: moments_v2_kernel + contract_v2_kernel"
+                  : "two-stage: moments_kernel + contract_v2_kernel";
+  return c->mv2 && !c->force_generic ? "two-stage: moments_v2_kernel + contract_kernel"
+                                     : "two-stage: moments_kernel + contract_kernel (generic)";
+}
 
 int p2s_shape_supported(const p2s_problem* spec) {
   if (!spec || validate(spec) != P2S_OK) return 0;
@@ -733,6 +863,14 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
   std::vector<const std::vector<double>*> dense;
   for (int s = 0; s < S; ++s) dense.push_back(&c->coef[s][0]);
   if (entry) c->cu_packed = entry->pack(dense);
+  c->fused = find_fused(*spec);
+  if (c->fused) {
+    V2Args v{};
+    for (int s = 0; s < S; ++s)
+      for (int d = 0; d < 3; ++d) v.dense[s][d] = &c->coef[s][d];
+    c->fused_cpack = c->fused->cpack(v);
+    c->fused_mpack = c->fused->mpack(c->phi);
+  }
   c->mv2 = find_mv2(*spec);
   if (c->mv2) c->mv2_packed = c->mv2->pack(c->phi);
   if (v2e) {
@@ -934,7 +1072,7 @@ p2s_status p2s_set_profiling(p2s_ctx* c, int enable) {
   harvest(c);
   c->prof = enable != 0;
   c->ms_mom = c->ms_con = 0.0;
-  c->n_mom = c->n_con = 0;
+  c->n_mom = c->n_con = c->n_fused = 0;
   return P2S_OK;
 }
 

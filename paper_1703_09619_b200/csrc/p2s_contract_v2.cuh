@@ -226,70 +226,33 @@ __device__ __forceinline__ void v2_load_fiber(const double* Bbuf, int i, int p1,
   });
 }
 
-template <class Sh>
-__global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
-    contract_v2_kernel(const __grid_constant__ V2Params<Sh> p) {
-  extern __shared__ __align__(16) double sm[];
+// Contraction of one (element, pair) unit whose moments are in Ibuf.
+// after_a() runs once the last stage A has read Ibuf (all threads, after a
+// barrier), e.g. to start the next unit's bulk copy into Ibuf.
+template <class Sh, class AfterA>
+__device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibuf, double* Abuf,
+                                        double* Bbuf, double* Mbase, AfterA&& after_a) {
   constexpr int S = Sh::S, NU = Sh::NU, NV = Sh::NV, NW = Sh::NW, T = Sh::T, FPT = Sh::FPT;
-  double* Ibuf = sm;
-  double* Abuf = Ibuf + Sh::MPP;
-  double* Bbuf = Abuf + Sh::A_DBL;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Bbuf + Sh::B_DBL);
   const int tid = threadIdx.x;
-  constexpr uint32_t kIBytes = Sh::MPP * 8u;
-
-  int64_t unit = blockIdx.x;
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-    if (unit < p.n_units) {
-      const int64_t e = unit / p.P;
-      const int pair = static_cast<int>(unit - e * p.P);
-      mbar_arrive_expect_tx(bar, kIBytes);
-      bulk_g2s(Ibuf, p.I + e * p.mom_per_elem + pair * Sh::MPP, kIBytes, bar);
-    }
+  if constexpr (Sh::AALL) {
+    v2_stage_a<Sh, 0, NV, 0>(p, Ibuf, Abuf);
+    __syncthreads();
+    after_a();
   }
-  __syncthreads();
-  uint32_t phase = 0;
-  auto issue_next = [&]() {
-    if (tid == 0) {
-      const int64_t nxt = unit + gridDim.x;
-      if (nxt < p.n_units) {
-        const int64_t e2 = nxt / p.P;
-        const int pair2 = static_cast<int>(nxt - e2 * p.P);
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(bar, kIBytes);
-        bulk_g2s(Ibuf, p.I + e2 * p.mom_per_elem + pair2 * Sh::MPP, kIBytes, bar);
-      }
-    }
-  };
-  for (; unit < p.n_units; unit += gridDim.x) {
-    const int64_t e = unit / p.P;
-    const int pair = static_cast<int>(unit - e * p.P);
-    const int gci = pair / p.nc, gcj = pair - gci * p.nc;
-    mbar_wait_parity(bar, phase);
-    phase ^= 1u;
-    double* Mbase = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt) * p.ldM + gcj * p.Nt;
-    if constexpr (Sh::AALL) {
-      v2_stage_a<Sh, 0, NV, 0>(p, Ibuf, Abuf);
+  for (int t = 0; t < Sh::NT; ++t) {
+    if constexpr (!Sh::AALL) {
+      static_for<0, Sh::NT>([&](auto tc) {
+        constexpr int tt = decltype(tc)::value;
+        if (t == tt) v2_stage_a<Sh, tt * T, T, 0>(p, Ibuf, Abuf);
+      });
       __syncthreads();
-      issue_next();
+      if (t == Sh::NT - 1) after_a();
     }
-
-    for (int t = 0; t < Sh::NT; ++t) {
-      if constexpr (!Sh::AALL) {
-        static_for<0, Sh::NT>([&](auto tc) {
-          constexpr int tt = decltype(tc)::value;
-          if (t == tt) v2_stage_a<Sh, tt * T, T, 0>(p, Ibuf, Abuf);
-        });
-        __syncthreads();
-        if (t == Sh::NT - 1) issue_next();
-      }
-      for (int pt = 0; pt < Sh::NP1; ++pt) {
+    for (int pt = 0; pt < Sh::NP1; ++pt) {
       v2_stage_b<Sh>(p, Abuf, Bbuf, Sh::AALL ? t * T : 0, pt * Sh::P1T);
       __syncthreads();
       // ---- stage C
-      constexpr int NF = T * Sh::P1T * NV * NW;   // fibers of the sub-tile
+      constexpr int NF = T * Sh::P1T * NV * NW;  // fibers of the sub-tile
       constexpr int NFT = (NF + FPT - 1) / FPT;
       const int64_t rowstep = static_cast<int64_t>(NV * NW) * p.ldM;
       for (int f0 = tid; f0 < NFT; f0 += Sh::THREADS) {
@@ -335,8 +298,53 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
         });
       }
       __syncthreads();
-      }  // p1 sub-tiles
+    }  // p1 sub-tiles
+  }
+}
+
+template <class Sh>
+__global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
+    contract_v2_kernel(const __grid_constant__ V2Params<Sh> p) {
+  extern __shared__ __align__(16) double sm[];
+  double* Ibuf = sm;
+  double* Abuf = Ibuf + Sh::MPP;
+  double* Bbuf = Abuf + Sh::A_DBL;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Bbuf + Sh::B_DBL);
+  const int tid = threadIdx.x;
+  constexpr uint32_t kIBytes = Sh::MPP * 8u;
+
+  int64_t unit = blockIdx.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    if (unit < p.n_units) {
+      const int64_t e = unit / p.P;
+      const int pair = static_cast<int>(unit - e * p.P);
+      mbar_arrive_expect_tx(bar, kIBytes);
+      bulk_g2s(Ibuf, p.I + e * p.mom_per_elem + pair * Sh::MPP, kIBytes, bar);
     }
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (; unit < p.n_units; unit += gridDim.x) {
+    const int64_t e = unit / p.P;
+    const int pair = static_cast<int>(unit - e * p.P);
+    const int gci = pair / p.nc, gcj = pair - gci * p.nc;
+    mbar_wait_parity(bar, phase);
+    phase ^= 1u;
+    double* Mbase = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt) * p.ldM + gcj * p.Nt;
+    v2_unit<Sh>(p, Ibuf, Abuf, Bbuf, Mbase, [&]() {
+      if (tid == 0) {
+        const int64_t nxt = unit + gridDim.x;
+        if (nxt < p.n_units) {
+          const int64_t e2 = nxt / p.P;
+          const int pair2 = static_cast<int>(nxt - e2 * p.P);
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(bar, kIBytes);
+          bulk_g2s(Ibuf, p.I + e2 * p.mom_per_elem + pair2 * Sh::MPP, kIBytes, bar);
+        }
+      }
+    });
   }
 }
 

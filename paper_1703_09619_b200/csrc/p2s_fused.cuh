@@ -1,0 +1,52 @@
+// p2s_fused.cuh -- the fill as ONE persistent kernel: per (element, pair)
+// unit the CTA computes the moments of every term from alpha straight into
+// shared memory (moments_unit, p2s_moments_v2.cuh), then contracts them and
+// streams the element matrix out (v2_unit, p2s_contract_v2.cuh).  HBM traffic
+// is alpha read + M write only; the FP64-heavy moment phase of one CTA
+// overlaps the store-heavy contraction phase of the other CTA(s) on the SM.
+#pragma once
+
+#include "p2s_contract_v2.cuh"
+#include "p2s_moments_v2.cuh"
+
+namespace p2s {
+
+template <class Sh, class Ms>
+struct FusedParams {
+  V2Params<Sh> c;      // contraction part (c.I unused)
+  const double* alpha;
+  double tab[Ms::TTOT];
+};
+
+template <class Sh, class Ms>
+struct FusedLayout {
+  static_assert(Sh::MPP == Ms::MPP, "moment block layouts differ");
+  static constexpr int AB = Sh::A_DBL + Sh::B_DBL;
+  static constexpr int WORK = AB > Ms::scratch_dbl() ? AB : Ms::scratch_dbl();
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(Sh::MPP + WORK);
+};
+
+template <class Sh, class Ms>
+__global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
+    fill_fused_kernel(const __grid_constant__ FusedParams<Sh, Ms> p) {
+  extern __shared__ __align__(16) double sm[];
+  double* Ibuf = sm;
+  double* Abuf = Ibuf + Sh::MPP;
+  double* Bbuf = Abuf + Sh::A_DBL;
+  constexpr int slab = Ms::Q(0) * Ms::Q(1) * Ms::Q(2);
+  for (int64_t unit = blockIdx.x; unit < p.c.n_units; unit += gridDim.x) {
+    const int64_t e = unit / p.c.P;
+    const int pair = static_cast<int>(unit - e * p.c.P);
+    const int gci = pair / p.c.nc, gcj = pair - gci * p.c.nc;
+    const double* a = p.alpha + unit * (static_cast<int64_t>(Ms::S) * slab);
+    static_for<0, Ms::S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      moments_unit<Ms, s, Sh::THREADS>(a + s * slab, p.tab, Abuf, Ibuf + Sh::moff(s));
+    });
+    double* Mbase =
+        p.c.M + e * p.c.mat_stride + static_cast<int64_t>(gci * p.c.Nt) * p.c.ldM + gcj * p.c.Nt;
+    v2_unit<Sh>(p.c, Ibuf, Abuf, Bbuf, Mbase, []() {});
+  }
+}
+
+}  // namespace p2s

@@ -99,7 +99,7 @@ __device__ __forceinline__ void fold_contract(const double (&a)[Q], const double
 // Moments of one (alpha slab, term) into Iout (global or shared), using the
 // smem scratch T1/T2.  All threads of the CTA participate; ends with a
 // __syncthreads().
-template <class Ms, int s>
+template <class Ms, int s, int NTHR = Ms::THREADS>
 __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const double* tab,
                                              double* scratch, double* Iout) {
   constexpr int QU = Ms::Q(0), QV = Ms::Q(1), QW = Ms::Q(2);
@@ -112,7 +112,7 @@ __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const
   const double* tv = tab + Ms::toff(s, 1);
   const double* tw = tab + Ms::toff(s, 2);
 
-  for (int r = tid; r < QW * QV; r += Ms::THREADS) {
+  for (int r = tid; r < QW * QV; r += NTHR) {
     const int q3 = r / QV, q2 = r - (r / QV) * QV;
     double x[QU];
     if constexpr ((QU & 1) == 0) {
@@ -130,7 +130,7 @@ __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const
     fold_contract<QU, KU>(x, tu, [&](int k, double v) { T1[(k * QW + q3) * S2 + q2] = v; });
   }
   __syncthreads();
-  for (int r = tid; r < KU * QW; r += Ms::THREADS) {
+  for (int r = tid; r < KU * QW; r += NTHR) {
     const int k1 = r / QW, q3 = r - (r / QW) * QW;
     const double* src = T1 + (k1 * QW + q3) * S2;
     double x[QV];
@@ -139,7 +139,7 @@ __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const
     fold_contract<QV, KV>(x, tv, [&](int k, double v) { T2[(k1 * KV + k) * S3 + q3] = v; });
   }
   __syncthreads();
-  for (int r = tid; r < KU * KV; r += Ms::THREADS) {
+  for (int r = tid; r < KU * KV; r += NTHR) {
     const double* src = T2 + r * S3;
     double x[QW];
 #pragma unroll
