@@ -273,140 +273,6 @@ def run_b200(args, cfg):
         pass
     fp64_peak = 34.1  # tools/peaks.cu DFMA loop on this pool's B200 (profiles/r1_peaks.json)
     line = {
-        "impl": "reference", "metric": "element matrices/s (FP64)", "value": value,
-        "unit": "elem/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded alpha, BASELINE.json shapes)",
-        "config": {"workload": cfg.name, "n_comp": cfg.n_comp, "order": list(cfg.order),
-                   "n_terms": len(cfg.kinds), "nq": list(cfg.nq), "elements_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": "elem/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} {cfg.name} elements per step (moments + banded "
-                                   f"contraction, oracle/p2s_oracle.c, {threads} threads)"},
-        "e2e": {"value": value, "unit": "elem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def _default_cpu_sample(cfg):
-    per = {"c1": 256, "c2": 64, "c3": 48, "c4": 48, "c5": 1}
-    return per.get(cfg.name, 16)
-
-
-# ---------------------------------------------------------------- B200 arm
-
-def run_b200(args, cfg):
-    import torch
-    import torch.distributed as dist
-
-    from paper_1703_09619_b200 import capi
-    from paper_1703_09619_b200.configs import algorithmic_counts
-
-    rank = _env_int("RANK", 0)
-    world = _env_int("WORLD_SIZE", 1)
-    local = _env_int("LOCAL_RANK", 0)
-    distributed = world > 1
-    torch.cuda.set_device(local)
-    if distributed:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    E = args.n_elem or cfg.n_elem
-    ctx = capi.Context(**cfg.problem(), device=local)
-    st = torch.cuda.current_stream()
-    sp = st.cuda_stream
-    n_tot = ctx.n_tot
-    alpha = torch.empty((E, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")
-    ctx.alpha_generate(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, args.seed, rank * E, E, alpha, sp)
-    M = torch.empty((E, n_tot, n_tot), dtype=torch.float64, device="cuda")
-    torch.cuda.synchronize()
-
-    def barrier():
-        if distributed:
-            dist.barrier()
-
-    for _ in range(max(3, args.warmup)):
-        ctx.fill(alpha, M, n_tot, E, sp)
-    torch.cuda.synchronize()
-
-    ctx.set_profiling(True)
-    clocks = ClockSampler(local)
-    barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(st)
-    for _ in range(args.steps):
-        ctx.fill(alpha, M, n_tot, E, sp)
-    ev1.record(st)
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    barrier()
-    ms = ev0.elapsed_time(ev1)
-    stages = ctx.stage_times()
-    ctx.set_profiling(False)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if distributed:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = world * E * args.steps / (ms_max / 1e3)
-
-    # checksum outside the timed region (guards against skipped work)
-    chk = float(M[:, :8, :8].abs().sum().item())
-
-    # ---- e2e through the host-buffer entry point (pinned buffers)
-    e2e = None
-    if not args.no_e2e:
-        E2 = min(E, 1024)
-        h_alpha = torch.empty((E2, ctx.alpha_per_elem), dtype=torch.float64, pin_memory=True)
-        h_alpha.copy_(alpha[:E2])
-        h_M = torch.empty((E2, n_tot, n_tot), dtype=torch.float64, pin_memory=True)
-        ctx.fill_host(h_alpha, h_M, n_tot, E2)  # warm-up
-        reps = 3
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            ctx.fill_host(h_alpha, h_M, n_tot, E2)
-        dt = time.perf_counter() - t0
-        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        if distributed:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dt = float(tt.item())
-        e2e = {"value": world * E2 * reps / dt, "unit": "elem/s",
-               "h2d_bytes_per_step": E2 * ctx.alpha_per_elem * 8,
-               "d2h_bytes_per_step": E2 * n_tot * n_tot * 8,
-               "elements_per_step": E2, "timing": "wall clock around p2s_fill_host (pinned host buffers)"}
-        del h_alpha, h_M
-
-    if rank != 0:
-        if distributed:
-            dist.destroy_process_group()
-        return
-
-    counts = algorithmic_counts(cfg)
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except Exception:
-        pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
-    # dominant kernel = contraction (HBM-write bound)
-    n_con = max(1, stages["n_contract"])
-    con_ms_avg = stages["ms_contract"] / n_con
-    elems_total = E * args.steps
-    bytes_per_launch = counts["bytes_con"] * elems_total / n_con
-    achieved = bytes_per_launch / (con_ms_avg / 1e3) / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(cfg.name)
-            if tr:
-                traffic = tr["dram_bytes_per_launch"] * (bytes_per_launch / tr["alg_bytes_per_launch"])
-    except Exception:
-        pass
-    mom_ms_avg = stages["ms_moments"] / max(1, stages["n_moments"])
-    line = {
         "metric": "element matrices/s (FP64)",
         "value": value,
         "unit": "elem/s",
