@@ -93,9 +93,10 @@ struct Shape {
   }
   // smem (doubles)
   static constexpr int BSTR = (P1T * NV * NW) | 1;  // odd k1 stride of B
+  static constexpr int aks(int s) { return (NV * K(s, 2)) | 1; }  // odd k1 stride of A
   static constexpr int aoff(int s) {
     int o = 0;
-    for (int i = 0; i < s; ++i) o += AT * K(i, 0) * NV * K(i, 2);
+    for (int i = 0; i < s; ++i) o += AT * K(i, 0) * aks(i);
     return o;
   }
   static constexpr int boff(int s) {
@@ -142,7 +143,7 @@ __device__ __forceinline__ void v2_stage_a(const V2Params<Sh>& p, const double* 
         static_for<0, CNT>([&](auto ic) {
           constexpr int i = decltype(ic)::value;
           constexpr int n1 = N1 + i;
-          double* As = Abuf + Sh::aoff(s) + (SLOT0 + i) * (Ku * NV * Kw);
+          double* As = Abuf + Sh::aoff(s) + (SLOT0 + i) * (Ku * Sh::aks(s));
           static_for<0, NV>([&](auto n2c) {
             constexpr int n2 = decltype(n2c)::value;
             constexpr int lo = band_lo(kv, n1, n2), cnt = band_count(kv, n1, n2);
@@ -152,7 +153,7 @@ __device__ __forceinline__ void v2_stage_a(const V2Params<Sh>& p, const double* 
               constexpr int j = decltype(jc)::value;
               v = fma(p.cv[co + j], x[lo + 2 * j], v);
             });
-            As[(k1 * NV + n2) * Kw + k3] = v;
+            As[k1 * Sh::aks(s) + n2 * Kw + k3] = v;
           });
         });
       }
@@ -177,12 +178,12 @@ __device__ __forceinline__ void v2_stage_b(const V2Params<Sh>& p, const double* 
         constexpr int NFIB = T * Ku * NV;
         const int g = f - Sh::fb_off(s);
         const int pg = g / NFIB;
-        const int fib = g - pg * NFIB;          // (i*Ku + k1)*NV + n2
-        const int n2 = fib % NV;
-        const int ik = fib / NV;                // i*Ku + k1
+        const int fib = g - pg * NFIB;          // n2*(T*Ku) + (i*Ku + k1): k1 fastest
+        const int n2 = fib / (T * Ku);
+        const int ik = fib - n2 * (T * Ku);     // i*Ku + k1
         const int i = ik / Ku, k1 = ik - i * Ku;
         const double* src =
-            Abuf + Sh::aoff(s) + (((aslot0 + i) * Ku + k1) * NV + n2) * Kw;
+            Abuf + Sh::aoff(s) + ((aslot0 + i) * Ku + k1) * Sh::aks(s) + n2 * Kw;
         double y[Kw];
 #pragma unroll
         for (int k3 = 0; k3 < Kw; ++k3) y[k3] = src[k3];

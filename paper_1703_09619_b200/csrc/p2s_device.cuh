@@ -65,6 +65,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Bulk prefetch of global memory into L2 (bytes multiple of 16).
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Streaming (evict-first) 8-byte store: element matrices are written once and
 // never re-read by the fill.
 __device__ __forceinline__ void st_cs(double* p, double v) { __stcs(p, v); }

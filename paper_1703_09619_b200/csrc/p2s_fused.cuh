@@ -39,6 +39,11 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     const int pair = static_cast<int>(unit - e * p.c.P);
     const int gci = pair / p.c.nc, gcj = pair - gci * p.c.nc;
     const double* a = p.alpha + unit * (static_cast<int64_t>(Ms::S) * slab);
+    // warm L2 with the next unit's alpha while this unit is processed
+    if constexpr ((Ms::S * slab) % 2 == 0)  // 16-B granularity of the bulk prefetch
+      if (threadIdx.x == 0 && unit + gridDim.x < p.c.n_units)
+        prefetch_l2(a + static_cast<int64_t>(gridDim.x) * Ms::S * slab,
+                    static_cast<uint32_t>(Ms::S * slab * 8));
     static_for<0, Ms::S>([&](auto sc) {
       constexpr int s = decltype(sc)::value;
       moments_unit<Ms, s, Sh::THREADS>(a + s * slab, p.tab, Abuf, Ibuf + Sh::moff(s));
