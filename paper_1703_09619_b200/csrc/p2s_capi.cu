@@ -282,24 +282,22 @@ constexpr int kDDD = enc_kind(DD, DD, DD);
 //  P2S_V2_VARIANT=k selects the k-th match (tuning).
 const std::vector<V2Entry>& v2_registry() {
   static const std::vector<V2Entry> reg = {
-      // <NU, NV, NW, T, P1T, PG, threads, minB, AALL, FPT, kinds...>
+      // <NU, NV, NW, T, P1T, PG, threads, minB, flags (1 AALL, 2 ROWLOOP), FPT, kinds...>
       make_v2<Shape<4, 4, 4, 4, 4, 4, 256, 2, 1, 1, kPPP>>(),                 // C1
       make_v2<Shape<6, 6, 6, 2, 6, 1, 224, 2, 0, 2, kPPP, kDDD>>(),           // C2
+      make_v2<Shape<6, 6, 6, 2, 6, 1, 224, 2, 2, 2, kPPP, kDDD>>(),
       make_v2<Shape<6, 6, 6, 2, 6, 2, 224, 2, 0, 2, kPPP, kDDD>>(),
-      make_v2<Shape<6, 6, 6, 2, 6, 1, 224, 1, 0, 2, kPPP, kDDD>>(),
-      make_v2<Shape<6, 6, 6, 2, 3, 1, 224, 2, 0, 1, kPPP, kDDD>>(),
-      make_v2<Shape<6, 6, 6, 3, 6, 2, 320, 1, 1, 2, kPPP, kDDD>>(),
-      make_v2<Shape<8, 8, 8, 1, 2, 1, 128, 2, 0, 1, kPPP, kDDD>>(),           // C3
-      make_v2<Shape<8, 8, 8, 1, 2, 2, 128, 2, 0, 1, kPPP, kDDD>>(),
-      make_v2<Shape<8, 8, 8, 1, 4, 2, 256, 1, 0, 1, kPPP, kDDD>>(),
-      make_v2<Shape<8, 8, 8, 1, 8, 4, 256, 1, 0, 2, kPPP, kDDD>>(),
-      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 0, 1, kPPP, kDDD>>(),          // C4
-      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 1, 0, 1, kPPP, kDDD>>(),
-      make_v2<Shape<10, 6, 4, 2, 4, 2, 192, 2, 1, 1, kPPP, kDDD>>(),
-      make_v2<Shape<10, 6, 4, 3, 4, 4, 288, 1, 1, 1, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 8, 4, 256, 1, 0, 2, kPPP, kDDD>>(),           // C3
+      make_v2<Shape<8, 8, 8, 1, 8, 4, 256, 1, 2, 2, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 2, 1, 128, 2, 2, 1, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 4, 2, 256, 1, 2, 2, kPPP, kDDD>>(),
+      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 1, kPPP, kDDD>>(),          // C4
+      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 0, 1, kPPP, kDDD>>(),
+      make_v2<Shape<10, 6, 4, 3, 4, 4, 288, 1, 2, 2, kPPP, kDDD>>(),
+      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 2, kPPP, kDDD>>(),
       make_v2<Shape<3, 3, 3, 3, 3, 1, 96, 4, 0, 1, kPPP, kDDD>>(),            // test shapes
-      make_v2<Shape<3, 3, 3, 1, 1, 1, 64, 4, 1, 2, kPPP, kDDD>>(),
-      make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 0, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+      make_v2<Shape<3, 3, 3, 1, 1, 1, 64, 4, 3, 2, kPPP, kDDD>>(),
+      make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 2, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
   };
   return reg;
 }
@@ -484,7 +482,7 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<6, 6, 6, 14, 14, 14, 224, kPPP, kDDD>>(),                     // C2
       make_fused<Shape<8, 8, 8, 1, 8, 4, 256, 1, 0, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),                     // C3
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 0, 1, kPPP, kDDD>,
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),                    // C4
       make_fused<Shape<3, 3, 3, 3, 3, 1, 96, 4, 0, 1, kPPP, kDDD>,
                  MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),                         // tests

@@ -27,12 +27,15 @@ namespace p2s {
 
 constexpr int enc_kind(int ku, int kv, int kw) { return ku | (kv << 2) | (kw << 4); }
 
-// AALL: stage A for all n1 once per unit; FPT: stage-C fibers per thread.
-template <int NU_, int NV_, int NW_, int T_, int P1T_, int PG_, int THREADS_, int MINB_, int AALL_,
+// FLAGS bit 0 (AALL): stage A for all n1 once per unit; bit 1 (ROWLOOP): stage C
+// walks the m1 rows in a runtime loop (bounds the scheduler's window and
+// register pressure for large N_u); FPT: stage-C fibers per thread.
+template <int NU_, int NV_, int NW_, int T_, int P1T_, int PG_, int THREADS_, int MINB_, int FLAGS_,
           int FPT_, int... TK>
 struct Shape {
   static constexpr int NU = NU_, NV = NV_, NW = NW_, T = T_, THREADS = THREADS_, MINB = MINB_;
-  static constexpr int AALL = AALL_, FPT = FPT_, P1T = P1T_, PG = PG_;
+  static constexpr int AALL = FLAGS_ & 1, ROWLOOP = (FLAGS_ >> 1) & 1;
+  static constexpr int FPT = FPT_, P1T = P1T_, PG = PG_;
   static constexpr int NPG = P1T_ / PG_;
   static_assert(P1T_ % PG_ == 0, "p1 group must divide the p1 tile");
   static constexpr int NP1 = NW_ / P1T_;
@@ -188,26 +191,32 @@ __device__ __forceinline__ void v2_stage_b(const V2Params<Sh>& p, const double* 
 #pragma unroll
         for (int k3 = 0; k3 < Kw; ++k3) y[k3] = src[k3];
         double* dst = Bbuf + Sh::boff(s) + ik * Sh::BSTR + n2 * NW;
-#pragma unroll
-        for (int jg = 0; jg < Sh::PG; ++jg) {
-          const int p1l = pg * Sh::PG + jg;
-          const int p1 = p1base + p1l;
-          static_for<0, NW>([&](auto p1c) {
-            constexpr int pp1 = decltype(p1c)::value;
-            if (p1 == pp1) {
-              static_for<0, NW>([&](auto p2c) {
-                constexpr int p2 = decltype(p2c)::value;
-                constexpr int lo = band_lo(kw, pp1, p2), cnt = band_count(kw, pp1, p2);
-                constexpr int co = Sh::coff(2, s, pp1, p2);
-                double v = 0.0;
-                static_for<0, cnt>([&](auto jc) {
-                  constexpr int j = decltype(jc)::value;
-                  v = fma(p.cw[co + j], y[lo + 2 * j], v);
-                });
-                dst[p1l * NV * NW + p2] = v;
-              });
-            }
+        auto emit = [&](auto p1c, int p1l) {
+          constexpr int pp1 = decltype(p1c)::value;
+          static_for<0, NW>([&](auto p2c) {
+            constexpr int p2 = decltype(p2c)::value;
+            constexpr int lo = band_lo(kw, pp1, p2), cnt = band_count(kw, pp1, p2);
+            constexpr int co = Sh::coff(2, s, pp1, p2);
+            double v = 0.0;
+            static_for<0, cnt>([&](auto jc) {
+              constexpr int j = decltype(jc)::value;
+              v = fma(p.cw[co + j], y[lo + 2 * j], v);
+            });
+            dst[p1l * NV * NW + p2] = v;
           });
+        };
+        if constexpr (Sh::PG == NW) {
+          // one item covers every p1: compile-time p1, no dispatch
+          static_for<0, NW>([&](auto p1c) { emit(p1c, decltype(p1c)::value); });
+        } else {
+#pragma unroll
+          for (int jg = 0; jg < Sh::PG; ++jg) {
+            const int p1l = pg * Sh::PG + jg;
+            const int p1 = p1base + p1l;
+            static_for<0, NW>([&](auto p1c) {
+              if (p1 == decltype(p1c)::value) emit(p1c, p1l);
+            });
+          }
         }
       }
     });
@@ -272,7 +281,7 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
           v2_load_fiber<Sh>(Bbuf, i, p1l, r, b[q]);
           out[q] = Mbase + static_cast<int64_t>(n1 * NW + p1) * p.ldM + r;
         }
-        static_for<0, NU>([&](auto m1c) {
+        auto row = [&](auto m1c) {
           constexpr int m1 = decltype(m1c)::value;
           static_for<0, NU>([&](auto m2c) {
             constexpr int m2 = decltype(m2c)::value;
@@ -296,7 +305,16 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
             for (int q = 0; q < FPT; ++q)
               if (live[q]) st_cs(out[q] + m1 * rowstep + m2 * (NV * NW), v[q]);
           });
-        });
+        };
+        if constexpr (Sh::ROWLOOP) {
+#pragma unroll 1
+          for (int m1 = 0; m1 < NU; ++m1)
+            static_for<0, NU>([&](auto m1c) {
+              if (m1 == decltype(m1c)::value) row(m1c);
+            });
+        } else {
+          static_for<0, NU>([&](auto m1c) { row(m1c); });
+        }
       }
       __syncthreads();
     }  // p1 sub-tiles
