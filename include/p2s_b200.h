@@ -114,6 +114,13 @@ p2s_status p2s_fill(p2s_ctx* ctx, const double* d_alpha, double* d_M, int64_t ld
 p2s_status p2s_fill_host(p2s_ctx* ctx, const double* h_alpha, double* h_M, int64_t ld_M,
                          int64_t n_elem);
 
+/* Host-buffer variants of the two stages (the reference's value-semantics
+ * compute_kernel_tables / assemble_p2s_element on host memory): device
+ * staging is internal; synchronous. */
+p2s_status p2s_moments_host(p2s_ctx* ctx, const double* h_alpha, double* h_I, int64_t n_elem);
+p2s_status p2s_contract_host(p2s_ctx* ctx, const double* h_I, double* h_M, int64_t ld_M,
+                             int64_t n_elem);
+
 /* Seeded synthetic coupling factor (benchmark harness input, not part of the
  * fill): elements e0 .. e0+n_elem-1 into d_alpha.  lo/hi: frequency range. */
 p2s_status p2s_alpha_generate(p2s_ctx* ctx, int alpha_kind, double lo, double hi,

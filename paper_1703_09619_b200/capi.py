@@ -26,7 +26,7 @@ _STATUS = {0: "P2S_OK", 1: "P2S_INVALID_ARG", 2: "P2S_CUDA_ERROR", 3: "P2S_UNSUP
 EXPORTS = ("p2s_create", "p2s_destroy", "p2s_get_sizes", "p2s_moments", "p2s_contract",
            "p2s_fill", "p2s_fill_host", "p2s_alpha_generate", "p2s_get_tables",
            "p2s_set_profiling", "p2s_get_stage_times", "p2s_shape_supported", "p2s_last_error",
-           "p2s_version", "p2s_kernel_path")
+           "p2s_version", "p2s_kernel_path", "p2s_moments_host", "p2s_contract_host")
 
 
 class P2SError(RuntimeError):
@@ -91,6 +91,8 @@ def lib():
         L.p2s_contract.argtypes = [vp, vp, vp, i64, i64, vp]
         L.p2s_fill.argtypes = [vp, vp, vp, i64, i64, vp]
         L.p2s_fill_host.argtypes = [vp, vp, vp, i64, i64]
+        L.p2s_moments_host.argtypes = [vp, vp, vp, i64]
+        L.p2s_contract_host.argtypes = [vp, vp, vp, i64, i64]
         L.p2s_alpha_generate.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_uint64, i64, i64,
                                          vp, vp]
         L.p2s_get_tables.argtypes = [vp, C.c_int, C.c_int, dp, dp, dp, dp]
@@ -202,6 +204,12 @@ class Context:
 
     def fill_host(self, h_alpha, h_M, ld_M, n_elem):
         _check(lib().p2s_fill_host(self.h, _ptr(h_alpha), _ptr(h_M), ld_M, n_elem))
+
+    def moments_host(self, h_alpha, h_I, n_elem):
+        _check(lib().p2s_moments_host(self.h, _ptr(h_alpha), _ptr(h_I), n_elem))
+
+    def contract_host(self, h_I, h_M, ld_M, n_elem):
+        _check(lib().p2s_contract_host(self.h, _ptr(h_I), _ptr(h_M), ld_M, n_elem))
 
     def alpha_generate(self, kind, lo, hi, seed, e0, n_elem, d_alpha, stream=0):
         _check(lib().p2s_alpha_generate(self.h, kind, lo, hi, seed, e0, n_elem, _ptr(d_alpha),

@@ -1038,6 +1038,48 @@ p2s_status p2s_fill_host(p2s_ctx* c, const double* h_alpha, double* h_M, int64_t
   return P2S_OK;
 }
 
+p2s_status p2s_moments_host(p2s_ctx* c, const double* h_alpha, double* h_I, int64_t n) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (n < 0 || (n > 0 && (!h_alpha || !h_I))) return fail(P2S_INVALID_ARG, "p2s_moments_host: bad buffers");
+  if (n == 0) return P2S_OK;
+  P2S_CUDA(cudaSetDevice(c->device));
+  double *da = nullptr, *dI = nullptr;
+  const size_t na = sizeof(double) * c->sz.alpha_per_elem * n, ni = sizeof(double) * c->sz.moments_per_elem * n;
+  P2S_CUDA(cudaMalloc(&da, na));
+  cudaError_t e = cudaMalloc(&dI, ni);
+  p2s_status st = P2S_OK;
+  if (e == cudaSuccess) e = cudaMemcpy(da, h_alpha, na, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) st = run_moments(c, da, dI, n, 0);
+  if (e == cudaSuccess && st == P2S_OK) e = cudaMemcpy(h_I, dI, ni, cudaMemcpyDeviceToHost);
+  cudaFree(da);
+  if (dI) cudaFree(dI);
+  if (e != cudaSuccess) return cuda_fail(e, "p2s_moments_host");
+  return st;
+}
+
+p2s_status p2s_contract_host(p2s_ctx* c, const double* h_I, double* h_M, int64_t ldM, int64_t n) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (n < 0 || (n > 0 && (!h_I || !h_M))) return fail(P2S_INVALID_ARG, "p2s_contract_host: bad buffers");
+  if (ldM < c->sz.n_tot) return fail(P2S_INVALID_ARG, "p2s_contract_host: ld_M < n_tot");
+  if (n == 0) return P2S_OK;
+  P2S_CUDA(cudaSetDevice(c->device));
+  double *dI = nullptr, *dM = nullptr;
+  const int64_t nt = c->sz.n_tot;
+  const size_t ni = sizeof(double) * c->sz.moments_per_elem * n, nm = sizeof(double) * nt * nt * n;
+  P2S_CUDA(cudaMalloc(&dI, ni));
+  cudaError_t e = cudaMalloc(&dM, nm);
+  p2s_status st = P2S_OK;
+  if (e == cudaSuccess) e = cudaMemcpy(dI, h_I, ni, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) st = run_contract(c, dI, dM, nt, n, 0);
+  if (e == cudaSuccess && st == P2S_OK)
+    e = cudaMemcpy2D(h_M, sizeof(double) * ldM, dM, sizeof(double) * nt, sizeof(double) * nt, nt * n,
+                     cudaMemcpyDeviceToHost);
+  cudaFree(dI);
+  if (dM) cudaFree(dM);
+  if (e != cudaSuccess) return cuda_fail(e, "p2s_contract_host");
+  return st;
+}
+
 p2s_status p2s_alpha_generate(p2s_ctx* c, int kind, double lo, double hi, uint64_t seed,
                               int64_t e0, int64_t n, double* d_alpha, void* stream) {
   if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
