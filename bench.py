@@ -39,12 +39,13 @@ def _env_int(k, d):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n-elem", type=int, default=0, help="override elements per rank")
-    ap.add_argument("--cpu-sample", type=int, default=0, help="elements of the CPU-baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="seconds of CPU work per CPU-baseline sample / reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=20170328)
@@ -106,16 +107,25 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- CPU oracle baseline
 
-def cpu_baseline(cfg, sample: int, seed: int, threads: int):
+def cpu_baseline(cfg, seconds: float, seed: int, threads: int, batch: int = 0, e0: int = 0):
+    """Oracle fill (moments + banded contraction, oracle/p2s_oracle.c) over
+    consecutive batches of the workload's elements until `seconds` of CPU work
+    are done; the output buffer is one batch, reused.  Returns (elem/s,
+    elements, seconds)."""
+    import numpy as np
+
     from oracle import oracle as O
     o = O.Oracle(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
-    alpha = o.alpha(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, seed, 0, sample)
-    import numpy as np
-    out = np.empty((sample, o.n_tot, o.n_tot))
-    t0 = time.perf_counter()
-    o.fill(alpha, threads=threads, out=out)
-    dt = time.perf_counter() - t0
-    return sample / dt, dt
+    batch = batch or max(threads, min(256, int(2e9 // (8 * o.n_tot * o.n_tot))))
+    out = np.empty((batch, o.n_tot, o.n_tot))
+    done, elapsed = 0, 0.0
+    while done == 0 or elapsed < seconds:
+        alpha = o.alpha(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, seed, e0 + done, batch)
+        t0 = time.perf_counter()
+        o.fill(alpha, threads=threads, out=out)
+        elapsed += time.perf_counter() - t0
+        done += batch
+    return done / elapsed, done, elapsed
 
 
 def run_reference(args, cfg):
@@ -124,34 +134,31 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample or _default_cpu_sample(cfg)
+    # bounded: the whole reference run stays within ~2 minutes of CPU work
+    secs = min(args.cpu_seconds, 120.0 / max(1, args.steps))
     for _ in range(max(0, args.warmup)):
-        cpu_baseline(cfg, max(1, sample // 4), args.seed, threads)
-    rates, times = [], []
-    for _ in range(args.steps):
-        r, dt = cpu_baseline(cfg, sample, args.seed, threads)
-        rates.append(r)
-        times.append(dt)
-    total = sum(times)
-    value = sample * len(times) / total
+        cpu_baseline(cfg, 0.0, args.seed, threads)
+    n_total, t_total = 0, 0.0
+    for i in range(args.steps):
+        _, n, dt = cpu_baseline(cfg, secs, args.seed, threads, e0=n_total)
+        n_total += n
+        t_total += dt
+    value = n_total / t_total
+    sample = n_total // max(1, args.steps)
     line = {
         "impl": "reference", "metric": "element matrices/s (FP64)", "value": value,
         "unit": "elem/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * t_total / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded alpha, BASELINE.json shapes)",
         "config": {"workload": cfg.name, "n_comp": cfg.n_comp, "order": list(cfg.order),
                    "n_terms": len(cfg.kinds), "nq": list(cfg.nq), "elements_per_step": sample},
         "cpu_baseline": {"value": value, "unit": "elem/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} {cfg.name} elements per step (moments + banded "
-                                   f"contraction, oracle/p2s_oracle.c, {threads} threads)"},
+                         "sample": f"~{sample} {cfg.name} elements per step (>= {secs:.0f} s of "
+                                   f"moments + banded contraction, oracle/p2s_oracle.c, "
+                                   f"{threads} threads)"},
         "e2e": {"value": value, "unit": "elem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-
-
-def _default_cpu_sample(cfg):
-    per = {"c1": 256, "c2": 64, "c3": 48, "c4": 48, "c5": 1}
-    return per.get(cfg.name, 16)
 
 
 # ---------------------------------------------------------------- B200 arm
@@ -194,6 +201,7 @@ def run_b200(args, cfg):
     barrier()
     torch.cuda.synchronize()
     clocks.start()
+    time.sleep(0.5)  # nvidia-smi needs a moment before its first sample
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(st)
@@ -310,11 +318,10 @@ def run_b200(args, cfg):
         line["e2e"] = e2e
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        sample = args.cpu_sample or _default_cpu_sample(cfg)
-        rate, dt = cpu_baseline(cfg, sample, args.seed, threads)
+        rate, n, dt = cpu_baseline(cfg, args.cpu_seconds, args.seed, threads)
         line["cpu_baseline"] = {"value": rate, "unit": "elem/s", "cores": threads, "kind": "port",
-                                "sample": f"{sample} {cfg.name} elements (moments + banded contraction,"
-                                          f" oracle/p2s_oracle.c), {dt:.1f} s"}
+                                "sample": f"{n} {cfg.name} elements, {dt:.1f} s (moments + banded "
+                                          f"contraction, oracle/p2s_oracle.c, {threads} threads)"}
     print(json.dumps(line), flush=True)
     if distributed:
         dist.destroy_process_group()
