@@ -34,7 +34,13 @@ template <int NU_, int NV_, int NW_, int T_, int P1T_, int PG_, int THREADS_, in
           int FPT_, int... TK>
 struct Shape {
   static constexpr int NU = NU_, NV = NV_, NW = NW_, T = T_, THREADS = THREADS_, MINB = MINB_;
-  static constexpr int AALL = FLAGS_ & 1, ROWLOOP = (FLAGS_ >> 1) & 1;
+  // SYM (bit 2): v- and w-kinds of every term are symmetric (PP / DD), so
+  // A is symmetric in (n1, n2) and B in (p1, p2): both are computed and stored
+  // for the upper triangle only, A once per unit.
+  static constexpr int SYM = (FLAGS_ >> 2) & 1;
+  static constexpr int AALL = (FLAGS_ & 1) | SYM, ROWLOOP = (FLAGS_ >> 1) & 1;
+  static constexpr int NQV = NV_ * (NV_ + 1) / 2, NQW = NW_ * (NW_ + 1) / 2;
+  static constexpr int tri(int a, int b, int n) { return a * n - a * (a - 1) / 2 + (b - a); }
   static constexpr int FPT = FPT_, P1T = P1T_, PG = PG_;
   static constexpr int NPG = P1T_ / PG_;
   static_assert(P1T_ % PG_ == 0, "p1 group must divide the p1 tile");
@@ -83,7 +89,7 @@ struct Shape {
   static constexpr int MPP = (moff(S) + 3) & ~3;
   // fiber counts / prefix sums over terms
   static constexpr int fa(int s) { return K(s, 0) * K(s, 2); }                // stage A fibers
-  static constexpr int fb(int s) { return T * K(s, 0) * NV * NPG; }          // stage B items
+  static constexpr int fb(int s) { return SYM ? T * K(s, 0) * NV : T * K(s, 0) * NV * NPG; }
   static constexpr int fa_off(int s) {
     int o = 0;
     for (int i = 0; i < s; ++i) o += fa(i);
@@ -95,13 +101,20 @@ struct Shape {
     return o;
   }
   // smem (doubles)
-  static constexpr int BSTR = (P1T * NV * NW) | 1;  // odd k1 stride of B
-  static constexpr int aks(int s) { return (NV * K(s, 2)) | 1; }  // odd k1 stride of A
+  static constexpr int BSTR = SYM ? (NV * NQW) | 1 : (P1T * NV * NW) | 1;  // odd k1 stride of B
+  static constexpr int aks(int s) { return SYM ? (NQV * K(s, 2)) | 1 : (NV * K(s, 2)) | 1; }
   static constexpr int aoff(int s) {
     int o = 0;
-    for (int i = 0; i < s; ++i) o += AT * K(i, 0) * aks(i);
+    for (int i = 0; i < s; ++i) o += (SYM ? 1 : AT) * K(i, 0) * aks(i);
     return o;
   }
+  static constexpr bool sym_ok() {
+    for (int s = 0; s < S; ++s)
+      for (int d = 1; d < 3; ++d)
+        if (kind(s, d) != PP && kind(s, d) != DD) return false;
+    return true;
+  }
+  static_assert(!SYM || (sym_ok() && P1T == NW_), "SYM needs symmetric v/w kinds and P1T == N_w");
   static constexpr int boff(int s) {
     int o = 0;
     for (int i = 0; i < s; ++i) o += T * K(i, 0) * BSTR;
@@ -223,14 +236,102 @@ __device__ __forceinline__ void v2_stage_b(const V2Params<Sh>& p, const double* 
   }
 }
 
+// SYM stage A: A_s[k1][tri(n1, n2)][k3] for n1 <= n2, all n1, once per unit.
 template <class Sh>
-__device__ __forceinline__ void v2_load_fiber(const double* Bbuf, int i, int p1, int r,
+__device__ __forceinline__ void v2_stage_a_sym(const V2Params<Sh>& p, const double* Ibuf, double* Abuf) {
+  constexpr int NV = Sh::NV;
+  constexpr int FTOT = Sh::fa_off(Sh::S);
+  for (int f = threadIdx.x; f < FTOT; f += Sh::THREADS) {
+    static_for<0, Sh::S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      if (f >= Sh::fa_off(s) && f < Sh::fa_off(s) + Sh::fa(s)) {
+        constexpr int Kv = Sh::K(s, 1), Kw = Sh::K(s, 2);
+        constexpr int kv = Sh::kind(s, 1);
+        const int g = f - Sh::fa_off(s);
+        const int k1 = g / Kw, k3 = g - (g / Kw) * Kw;
+        const double* Is = Ibuf + Sh::moff(s);
+        double x[Kv];
+#pragma unroll
+        for (int k2 = 0; k2 < Kv; ++k2) x[k2] = Is[(k1 * Kv + k2) * Kw + k3];
+        double* As = Abuf + Sh::aoff(s) + k1 * Sh::aks(s) + k3;
+        static_for<0, NV>([&](auto n1c) {
+          constexpr int n1 = decltype(n1c)::value;
+          static_for<n1, NV>([&](auto n2c) {
+            constexpr int n2 = decltype(n2c)::value;
+            constexpr int lo = band_lo(kv, n1, n2), cnt = band_count(kv, n1, n2);
+            constexpr int co = Sh::coff(1, s, n1, n2);
+            double v = 0.0;
+            static_for<0, cnt>([&](auto jc) {
+              constexpr int j = decltype(jc)::value;
+              v = fma(p.cv[co + j], x[lo + 2 * j], v);
+            });
+            As[Sh::tri(n1, n2, NV) * Kw] = v;
+          });
+        });
+      }
+    });
+  }
+}
+
+// SYM stage B: item (s, n2, i*Ku + k1) with k1 fastest (conflict-free odd
+// stride); B_s[i*Ku + k1][n2][tri(p1, p2)] for p1 <= p2.
+template <class Sh>
+__device__ __forceinline__ void v2_stage_b_sym(const V2Params<Sh>& p, const double* Abuf, double* Bbuf,
+                                               int n1base) {
+  constexpr int NV = Sh::NV, NW = Sh::NW, T = Sh::T, NQW = Sh::NQW;
+  constexpr int FTOT = Sh::fb_off(Sh::S);
+  for (int f = threadIdx.x; f < FTOT; f += Sh::THREADS) {
+    static_for<0, Sh::S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      if (f >= Sh::fb_off(s) && f < Sh::fb_off(s) + Sh::fb(s)) {
+        constexpr int Ku = Sh::K(s, 0), Kw = Sh::K(s, 2);
+        constexpr int kw = Sh::kind(s, 2);
+        const int g = f - Sh::fb_off(s);
+        const int n2 = g / (T * Ku);
+        const int ik = g - n2 * (T * Ku);
+        const int i = ik / Ku, k1 = ik - i * Ku;
+        const int n1 = n1base + i;
+        const int a = n1 < n2 ? n1 : n2, b = n1 < n2 ? n2 : n1;
+        const double* src = Abuf + Sh::aoff(s) + k1 * Sh::aks(s) + Sh::tri(a, b, NV) * Kw;
+        double y[Kw];
+#pragma unroll
+        for (int k3 = 0; k3 < Kw; ++k3) y[k3] = src[k3];
+        double* dst = Bbuf + Sh::boff(s) + ik * Sh::BSTR + n2 * NQW;
+        static_for<0, NW>([&](auto p1c) {
+          constexpr int p1 = decltype(p1c)::value;
+          static_for<p1, NW>([&](auto p2c) {
+            constexpr int p2 = decltype(p2c)::value;
+            constexpr int lo = band_lo(kw, p1, p2), cnt = band_count(kw, p1, p2);
+            constexpr int co = Sh::coff(2, s, p1, p2);
+            double v = 0.0;
+            static_for<0, cnt>([&](auto jc) {
+              constexpr int j = decltype(jc)::value;
+              v = fma(p.cw[co + j], y[lo + 2 * j], v);
+            });
+            dst[Sh::tri(p1, p2, NW)] = v;
+          });
+        });
+      }
+    });
+  }
+}
+
+template <class Sh>
+__device__ __forceinline__ void v2_load_fiber(const double* Bbuf, int i, int p1l, int r,
                                               double (&b)[Sh::KTOT_U()]) {
   constexpr int NV = Sh::NV, NW = Sh::NW;
+  int off;
+  if constexpr (Sh::SYM) {
+    const int n2 = r / NW, p2 = r - n2 * NW;   // p1l == p1 (P1T == NW)
+    const int a = p1l < p2 ? p1l : p2, c = p1l < p2 ? p2 : p1l;
+    off = n2 * Sh::NQW + Sh::tri(a, c, NW);
+  } else {
+    off = p1l * NV * NW + r;
+  }
   static_for<0, Sh::S>([&](auto sc) {
     constexpr int s = decltype(sc)::value;
     constexpr int Ku = Sh::K(s, 0);
-    const double* src = Bbuf + Sh::boff(s) + (i * Ku) * Sh::BSTR + p1 * NV * NW + r;  // p1 local
+    const double* src = Bbuf + Sh::boff(s) + (i * Ku) * Sh::BSTR + off;
 #pragma unroll
     for (int k1 = 0; k1 < Ku; ++k1) b[Sh::kuoff(s) + k1] = src[k1 * Sh::BSTR];
   });
@@ -244,7 +345,11 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
                                         double* Bbuf, double* Mbase, AfterA&& after_a) {
   constexpr int S = Sh::S, NU = Sh::NU, NV = Sh::NV, NW = Sh::NW, T = Sh::T, FPT = Sh::FPT;
   const int tid = threadIdx.x;
-  if constexpr (Sh::AALL) {
+  if constexpr (Sh::SYM) {
+    v2_stage_a_sym<Sh>(p, Ibuf, Abuf);
+    __syncthreads();
+    after_a();
+  } else if constexpr (Sh::AALL) {
     v2_stage_a<Sh, 0, NV, 0>(p, Ibuf, Abuf);
     __syncthreads();
     after_a();
@@ -259,7 +364,10 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
       if (t == Sh::NT - 1) after_a();
     }
     for (int pt = 0; pt < Sh::NP1; ++pt) {
-      v2_stage_b<Sh>(p, Abuf, Bbuf, Sh::AALL ? t * T : 0, pt * Sh::P1T);
+      if constexpr (Sh::SYM)
+        v2_stage_b_sym<Sh>(p, Abuf, Bbuf, t * T);
+      else
+        v2_stage_b<Sh>(p, Abuf, Bbuf, Sh::AALL ? t * T : 0, pt * Sh::P1T);
       __syncthreads();
       // ---- stage C
       constexpr int NF = T * Sh::P1T * NV * NW;  // fibers of the sub-tile
