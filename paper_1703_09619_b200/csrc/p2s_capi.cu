@@ -247,7 +247,9 @@ cudaError_t launch_v2(const V2Args& a, const std::vector<double>& packed, cudaSt
     if (b < 1) return cudaErrorInvalidConfiguration;
     blocks_per_sm = b;
   }
-  const int64_t grid = std::min<int64_t>(p.n_units, static_cast<int64_t>(blocks_per_sm) * num_sms);
+  const int64_t grid = Sh::PERSIST
+                           ? std::min<int64_t>(p.n_units, static_cast<int64_t>(blocks_per_sm) * num_sms)
+                           : p.n_units;
   contract_v2_kernel<Sh><<<static_cast<unsigned>(grid), Sh::THREADS, Sh::SMEM, st>>>(p);
   return cudaGetLastError();
 }
@@ -282,18 +284,21 @@ constexpr int kDDD = enc_kind(DD, DD, DD);
 //  P2S_V2_VARIANT=k selects the k-th match (tuning).
 const std::vector<V2Entry>& v2_registry() {
   static const std::vector<V2Entry> reg = {
-      // <NU, NV, NW, T, P1T, PG, threads, minB, flags (1 AALL, 2 ROWLOOP, 4 SYM), FPT, kinds...>
+      // <NU, NV, NW, T, P1T, PG, threads, minB, flags (1 AALL, 2 ROWLOOP, 4 SYM, 8 PERSIST),
+      //  FPT, kinds...>
       make_v2<Shape<4, 4, 4, 4, 4, 4, 256, 2, 4, 1, kPPP>>(),                 // C1
-      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>>(),           // C2
+      make_v2<Shape<6, 6, 6, 2, 6, 2, 224, 2, 0, 2, kPPP, kDDD>>(),           // C2
+      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>>(),
       make_v2<Shape<6, 6, 6, 1, 6, 6, 224, 2, 4, 1, kPPP, kDDD>>(),
-      make_v2<Shape<6, 6, 6, 2, 6, 2, 224, 2, 0, 2, kPPP, kDDD>>(),
-      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>>(),           // C3
-      make_v2<Shape<8, 8, 8, 1, 8, 4, 256, 1, 0, 2, kPPP, kDDD>>(),
+      make_v2<Shape<6, 6, 6, 2, 6, 2, 224, 2, 8, 2, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 8, 4, 256, 1, 0, 2, kPPP, kDDD>>(),           // C3
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 1, kPPP, kDDD>>(),
       make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>>(),          // C4
-      make_v2<Shape<10, 6, 4, 3, 4, 4, 288, 1, 6, 2, kPPP, kDDD>>(),
       make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 1, kPPP, kDDD>>(),
+      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 4, 1, kPPP, kDDD>>(),
       make_v2<Shape<3, 3, 3, 3, 3, 1, 96, 4, 0, 1, kPPP, kDDD>>(),            // test shapes
-      make_v2<Shape<3, 3, 3, 1, 3, 3, 64, 4, 4, 2, kPPP, kDDD>>(),
+      make_v2<Shape<3, 3, 3, 1, 3, 3, 64, 4, 12, 2, kPPP, kDDD>>(),
       make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 2, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
   };
   return reg;
@@ -428,6 +433,7 @@ cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_
   std::memcpy(p.c.cv, cpack.data() + Sh::ctot(0), sizeof(double) * Sh::ctot(1));
   std::memcpy(p.c.cw, cpack.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));
   p.alpha = alpha;
+  p.prefetch_stride = 0;
   std::memcpy(p.tab, mpack.data(), sizeof(double) * Ms::TTOT);
   if (p.c.n_units == 0) return cudaSuccess;
   constexpr size_t smem = FusedLayout<Sh, Ms>::SMEM;
@@ -442,7 +448,9 @@ cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_
     if (b < 1) return cudaErrorInvalidConfiguration;
     blocks_per_sm = b;
   }
-  const int64_t grid = std::min<int64_t>(p.c.n_units, static_cast<int64_t>(blocks_per_sm) * num_sms);
+  const int64_t resident = static_cast<int64_t>(blocks_per_sm) * num_sms;
+  const int64_t grid = Sh::PERSIST ? std::min<int64_t>(p.c.n_units, resident) : p.c.n_units;
+  p.prefetch_stride = resident;
   fill_fused_kernel<Sh, Ms><<<static_cast<unsigned>(grid), Sh::THREADS, smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -475,14 +483,18 @@ const std::vector<FusedEntry>& fused_registry() {
   static const std::vector<FusedEntry> reg = {
       make_fused<Shape<4, 4, 4, 4, 4, 4, 256, 2, 4, 1, kPPP>,
                  MShape<4, 4, 4, 8, 8, 8, 256, kPPP>>(),                              // C1
-      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),                     // C2
       make_fused<Shape<6, 6, 6, 2, 6, 2, 224, 2, 0, 2, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 224, kPPP, kDDD>>(),
-      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 224, kPPP, kDDD>>(),                     // C2
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+      make_fused<Shape<8, 8, 8, 1, 8, 4, 256, 1, 0, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),                     // C3
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>,
+                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),                    // C4
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 1, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
       make_fused<Shape<3, 3, 3, 3, 3, 1, 96, 4, 0, 1, kPPP, kDDD>,
                  MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),                         // tests
       make_fused<Shape<4, 3, 3, 3, 3, 3, 96, 4, 0, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>,

@@ -38,6 +38,10 @@ struct Shape {
   // A is symmetric in (n1, n2) and B in (p1, p2): both are computed and stored
   // for the upper triangle only, A once per unit.
   static constexpr int SYM = (FLAGS_ >> 2) & 1;
+  // PERSIST (bit 3): persistent CTAs loop over units (TMA prefetch of the next
+  // unit's moments); otherwise one CTA per unit (no outer loop, so ptxas cannot
+  // hoist the per-unit constant-bank loads into registers across units).
+  static constexpr int PERSIST = (FLAGS_ >> 3) & 1;
   static constexpr int AALL = (FLAGS_ & 1) | SYM, ROWLOOP = (FLAGS_ >> 1) & 1;
   static constexpr int NQV = NV_ * (NV_ + 1) / 2, NQW = NW_ * (NW_ + 1) / 2;
   static constexpr int tri(int a, int b, int n) { return a * n - a * (a - 1) / 2 + (b - a); }
@@ -144,7 +148,7 @@ template <class Sh, int N1, int CNT, int SLOT0>
 __device__ __forceinline__ void v2_stage_a(const V2Params<Sh>& p, const double* Ibuf, double* Abuf) {
   constexpr int NV = Sh::NV;
   constexpr int FTOT = Sh::fa_off(Sh::S);
-  for (int f = threadIdx.x; f < FTOT; f += Sh::THREADS) {
+  for_items<FTOT, Sh::THREADS>([&](int f) {
     static_for<0, Sh::S>([&](auto sc) {
       constexpr int s = decltype(sc)::value;
       if (f >= Sh::fa_off(s) && f < Sh::fa_off(s) + Sh::fa(s)) {
@@ -174,7 +178,7 @@ __device__ __forceinline__ void v2_stage_a(const V2Params<Sh>& p, const double* 
         });
       }
     });
-  }
+  });
 }
 
 // Stage B for the current tile: item = (s, (i*Ku + k1)*NV + n2, p1) with p1
@@ -185,7 +189,7 @@ __device__ __forceinline__ void v2_stage_b(const V2Params<Sh>& p, const double* 
                                            int aslot0, int p1base) {
   constexpr int NV = Sh::NV, NW = Sh::NW, T = Sh::T;
   constexpr int FTOT = Sh::fb_off(Sh::S);
-  for (int f = threadIdx.x; f < FTOT; f += Sh::THREADS) {
+  for_items<FTOT, Sh::THREADS>([&](int f) {
     static_for<0, Sh::S>([&](auto sc) {
       constexpr int s = decltype(sc)::value;
       if (f >= Sh::fb_off(s) && f < Sh::fb_off(s) + Sh::fb(s)) {
@@ -233,7 +237,7 @@ __device__ __forceinline__ void v2_stage_b(const V2Params<Sh>& p, const double* 
         }
       }
     });
-  }
+  });
 }
 
 // SYM stage A: A_s[k1][tri(n1, n2)][k3] for n1 <= n2, all n1, once per unit.
@@ -241,7 +245,7 @@ template <class Sh>
 __device__ __forceinline__ void v2_stage_a_sym(const V2Params<Sh>& p, const double* Ibuf, double* Abuf) {
   constexpr int NV = Sh::NV;
   constexpr int FTOT = Sh::fa_off(Sh::S);
-  for (int f = threadIdx.x; f < FTOT; f += Sh::THREADS) {
+  for_items<FTOT, Sh::THREADS>([&](int f) {
     static_for<0, Sh::S>([&](auto sc) {
       constexpr int s = decltype(sc)::value;
       if (f >= Sh::fa_off(s) && f < Sh::fa_off(s) + Sh::fa(s)) {
@@ -270,7 +274,7 @@ __device__ __forceinline__ void v2_stage_a_sym(const V2Params<Sh>& p, const doub
         });
       }
     });
-  }
+  });
 }
 
 // SYM stage B: item (s, n2, i*Ku + k1) with k1 fastest (conflict-free odd
@@ -280,7 +284,7 @@ __device__ __forceinline__ void v2_stage_b_sym(const V2Params<Sh>& p, const doub
                                                int n1base) {
   constexpr int NV = Sh::NV, NW = Sh::NW, T = Sh::T, NQW = Sh::NQW;
   constexpr int FTOT = Sh::fb_off(Sh::S);
-  for (int f = threadIdx.x; f < FTOT; f += Sh::THREADS) {
+  for_items<FTOT, Sh::THREADS>([&](int f) {
     static_for<0, Sh::S>([&](auto sc) {
       constexpr int s = decltype(sc)::value;
       if (f >= Sh::fb_off(s) && f < Sh::fb_off(s) + Sh::fb(s)) {
@@ -313,7 +317,7 @@ __device__ __forceinline__ void v2_stage_b_sym(const V2Params<Sh>& p, const doub
         });
       }
     });
-  }
+  });
 }
 
 template <class Sh>
@@ -373,7 +377,7 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
       constexpr int NF = T * Sh::P1T * NV * NW;  // fibers of the sub-tile
       constexpr int NFT = (NF + FPT - 1) / FPT;
       const int64_t rowstep = static_cast<int64_t>(NV * NW) * p.ldM;
-      for (int f0 = tid; f0 < NFT; f0 += Sh::THREADS) {
+      for_items<NFT, Sh::THREADS>([&](int f0) {
         double b[FPT][Sh::KTOT_U()];
         double* out[FPT];
         bool live[FPT];
@@ -423,7 +427,7 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
         } else {
           static_for<0, NU>([&](auto m1c) { row(m1c); });
         }
-      }
+      });
       __syncthreads();
     }  // p1 sub-tiles
   }
@@ -453,25 +457,31 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
   }
   __syncthreads();
   uint32_t phase = 0;
-  for (; unit < p.n_units; unit += gridDim.x) {
+  auto do_unit = [&](auto next_copy) {
     const int64_t e = unit / p.P;
     const int pair = static_cast<int>(unit - e * p.P);
     const int gci = pair / p.nc, gcj = pair - gci * p.nc;
     mbar_wait_parity(bar, phase);
     phase ^= 1u;
     double* Mbase = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt) * p.ldM + gcj * p.Nt;
-    v2_unit<Sh>(p, Ibuf, Abuf, Bbuf, Mbase, [&]() {
-      if (tid == 0) {
-        const int64_t nxt = unit + gridDim.x;
-        if (nxt < p.n_units) {
-          const int64_t e2 = nxt / p.P;
-          const int pair2 = static_cast<int>(nxt - e2 * p.P);
-          fence_proxy_async_smem();
-          mbar_arrive_expect_tx(bar, kIBytes);
-          bulk_g2s(Ibuf, p.I + e2 * p.mom_per_elem + pair2 * Sh::MPP, kIBytes, bar);
+    v2_unit<Sh>(p, Ibuf, Abuf, Bbuf, Mbase, next_copy);
+  };
+  if constexpr (Sh::PERSIST) {
+    for (; unit < p.n_units; unit += gridDim.x)
+      do_unit([&]() {
+        if (tid == 0) {
+          const int64_t nxt = unit + gridDim.x;
+          if (nxt < p.n_units) {
+            const int64_t e2 = nxt / p.P;
+            const int pair2 = static_cast<int>(nxt - e2 * p.P);
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(bar, kIBytes);
+            bulk_g2s(Ibuf, p.I + e2 * p.mom_per_elem + pair2 * Sh::MPP, kIBytes, bar);
+          }
         }
-      }
-    });
+      });
+  } else {
+    if (unit < p.n_units) do_unit([]() {});
   }
 }
 

@@ -17,6 +17,17 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
+// Work items 0..N-1 over THREADS threads as ceil(N/THREADS) unrolled rounds
+// (no runtime loop: keeps ptxas from hoisting per-item constant-bank loads
+// into registers across items).
+template <int N, int THREADS, class F>
+__device__ __forceinline__ void for_items(F&& body) {
+  static_for<0, (N + THREADS - 1) / THREADS>([&](auto rc) {
+    const int f = decltype(rc)::value * THREADS + static_cast<int>(threadIdx.x);
+    if (f < N) body(f);
+  });
+}
+
 // ---------------------------------------------------------------- smem / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

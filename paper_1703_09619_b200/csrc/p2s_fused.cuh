@@ -15,6 +15,7 @@ template <class Sh, class Ms>
 struct FusedParams {
   V2Params<Sh> c;      // contraction part (c.I unused)
   const double* alpha;
+  int64_t prefetch_stride;  // resident CTAs on the GPU (non-persistent launch)
   double tab[Ms::TTOT];
 };
 
@@ -34,16 +35,15 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
   double* Abuf = Ibuf + Sh::MPP;
   double* Bbuf = Abuf + Sh::A_DBL;
   constexpr int slab = Ms::Q(0) * Ms::Q(1) * Ms::Q(2);
-  for (int64_t unit = blockIdx.x; unit < p.c.n_units; unit += gridDim.x) {
+  auto do_unit = [&](int64_t unit, int64_t stride) {
     const int64_t e = unit / p.c.P;
     const int pair = static_cast<int>(unit - e * p.c.P);
     const int gci = pair / p.c.nc, gcj = pair - gci * p.c.nc;
     const double* a = p.alpha + unit * (static_cast<int64_t>(Ms::S) * slab);
-    // warm L2 with the next unit's alpha while this unit is processed
+    // warm L2 with alpha `stride` units ahead while this unit is processed
     if constexpr ((Ms::S * slab) % 2 == 0)  // 16-B granularity of the bulk prefetch
-      if (threadIdx.x == 0 && unit + gridDim.x < p.c.n_units)
-        prefetch_l2(a + static_cast<int64_t>(gridDim.x) * Ms::S * slab,
-                    static_cast<uint32_t>(Ms::S * slab * 8));
+      if (threadIdx.x == 0 && unit + stride < p.c.n_units)
+        prefetch_l2(a + stride * Ms::S * slab, static_cast<uint32_t>(Ms::S * slab * 8));
     static_for<0, Ms::S>([&](auto sc) {
       constexpr int s = decltype(sc)::value;
       moments_unit<Ms, s, Sh::THREADS>(a + s * slab, p.tab, Abuf, Ibuf + Sh::moff(s));
@@ -51,6 +51,12 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     double* Mbase =
         p.c.M + e * p.c.mat_stride + static_cast<int64_t>(gci * p.c.Nt) * p.c.ldM + gcj * p.c.Nt;
     v2_unit<Sh>(p.c, Ibuf, Abuf, Bbuf, Mbase, []() {});
+  };
+  if constexpr (Sh::PERSIST) {
+    for (int64_t unit = blockIdx.x; unit < p.c.n_units; unit += gridDim.x) do_unit(unit, gridDim.x);
+  } else {
+    // one unit per CTA; prefetch for the CTA that runs on this SM slot next
+    if (blockIdx.x < p.c.n_units) do_unit(blockIdx.x, p.prefetch_stride);
   }
 }
 

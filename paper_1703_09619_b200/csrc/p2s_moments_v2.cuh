@@ -107,12 +107,11 @@ __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const
   constexpr int S2 = Ms::S2, S3 = Ms::S3;
   double* T1 = scratch;                    // [KU][QW][S2]
   double* T2 = scratch + Ms::t1_dbl(s);    // [KU*KV][S3]
-  const int tid = threadIdx.x;
   const double* tu = tab + Ms::toff(s, 0);
   const double* tv = tab + Ms::toff(s, 1);
   const double* tw = tab + Ms::toff(s, 2);
 
-  for (int r = tid; r < QW * QV; r += NTHR) {
+  for_items<QW * QV, NTHR>([&](int r) {
     const int q3 = r / QV, q2 = r - (r / QV) * QV;
     double x[QU];
     if constexpr ((QU & 1) == 0) {
@@ -128,24 +127,24 @@ __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const
       for (int q = 0; q < QU; ++q) x[q] = __ldg(a + static_cast<int64_t>(r) * QU + q);
     }
     fold_contract<QU, KU>(x, tu, [&](int k, double v) { T1[(k * QW + q3) * S2 + q2] = v; });
-  }
+  });
   __syncthreads();
-  for (int r = tid; r < KU * QW; r += NTHR) {
+  for_items<KU * QW, NTHR>([&](int r) {
     const int k1 = r / QW, q3 = r - (r / QW) * QW;
     const double* src = T1 + (k1 * QW + q3) * S2;
     double x[QV];
 #pragma unroll
     for (int q = 0; q < QV; ++q) x[q] = src[q];
     fold_contract<QV, KV>(x, tv, [&](int k, double v) { T2[(k1 * KV + k) * S3 + q3] = v; });
-  }
+  });
   __syncthreads();
-  for (int r = tid; r < KU * KV; r += NTHR) {
+  for_items<KU * KV, NTHR>([&](int r) {
     const double* src = T2 + r * S3;
     double x[QW];
 #pragma unroll
     for (int q = 0; q < QW; ++q) x[q] = src[q];
     fold_contract<QW, KW>(x, tw, [&](int k, double v) { Iout[r * KW + k] = v; });
-  }
+  });
   __syncthreads();
 }
 
