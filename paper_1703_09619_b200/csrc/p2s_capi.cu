@@ -284,20 +284,19 @@ constexpr int kDDD = enc_kind(DD, DD, DD);
 //  P2S_V2_VARIANT=k selects the k-th match (tuning).
 const std::vector<V2Entry>& v2_registry() {
   static const std::vector<V2Entry> reg = {
-      // <NU, NV, NW, T, P1T, PG, threads, minB, flags (1 AALL, 2 ROWLOOP, 4 SYM, 8 PERSIST),
-      //  FPT, kinds...>
+      // <NU, NV, NW, T, P1T (= NW), PG (= NW), threads, minB,
+      //  flags (1 AALL, 2 ROWLOOP, 4 SYM, 8 PERSIST), FPT, kinds...>
       make_v2<Shape<4, 4, 4, 4, 4, 4, 256, 2, 4, 1, kPPP>>(),                 // C1
-      make_v2<Shape<6, 6, 6, 2, 6, 2, 224, 2, 0, 2, kPPP, kDDD>>(),           // C2
-      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>>(),
+      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>>(),           // C2
       make_v2<Shape<6, 6, 6, 1, 6, 6, 224, 2, 4, 1, kPPP, kDDD>>(),
-      make_v2<Shape<6, 6, 6, 2, 6, 2, 224, 2, 8, 2, kPPP, kDDD>>(),
-      make_v2<Shape<8, 8, 8, 1, 8, 4, 256, 1, 0, 2, kPPP, kDDD>>(),           // C3
+      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 0, 2, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 1, kPPP, kDDD>>(),           // C3
       make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>>(),
-      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 1, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 12, 2, kPPP, kDDD>>(),
       make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>>(),          // C4
-      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 1, kPPP, kDDD>>(),
       make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 4, 1, kPPP, kDDD>>(),
-      make_v2<Shape<3, 3, 3, 3, 3, 1, 96, 4, 0, 1, kPPP, kDDD>>(),            // test shapes
+      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 1, kPPP, kDDD>>(),
+      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>>(),            // test shapes
       make_v2<Shape<3, 3, 3, 1, 3, 3, 64, 4, 12, 2, kPPP, kDDD>>(),
       make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 2, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
   };
@@ -483,19 +482,19 @@ const std::vector<FusedEntry>& fused_registry() {
   static const std::vector<FusedEntry> reg = {
       make_fused<Shape<4, 4, 4, 4, 4, 4, 256, 2, 4, 1, kPPP>,
                  MShape<4, 4, 4, 8, 8, 8, 256, kPPP>>(),                              // C1
-      make_fused<Shape<6, 6, 6, 2, 6, 2, 224, 2, 0, 2, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 224, kPPP, kDDD>>(),                     // C2
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
-      make_fused<Shape<8, 8, 8, 1, 8, 4, 256, 1, 0, 2, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),                     // C2
+      make_fused<Shape<6, 6, 6, 1, 6, 6, 224, 2, 4, 1, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 224, kPPP, kDDD>>(),
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 1, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),                     // C3
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 4, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),                    // C4
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 1, kPPP, kDDD>,
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
-      make_fused<Shape<3, 3, 3, 3, 3, 1, 96, 4, 0, 1, kPPP, kDDD>,
+      make_fused<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>,
                  MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),                         // tests
       make_fused<Shape<4, 3, 3, 3, 3, 3, 96, 4, 0, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>,
                  MShape<4, 3, 3, 9, 5, 7, 96, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),

@@ -46,8 +46,9 @@ struct Shape {
   static constexpr int NQV = NV_ * (NV_ + 1) / 2, NQW = NW_ * (NW_ + 1) / 2;
   static constexpr int tri(int a, int b, int n) { return a * n - a * (a - 1) / 2 + (b - a); }
   static constexpr int FPT = FPT_, P1T = P1T_, PG = PG_;
-  static constexpr int NPG = P1T_ / PG_;
-  static_assert(P1T_ % PG_ == 0, "p1 group must divide the p1 tile");
+  static constexpr int NPG = 1;
+  static_assert(PG_ == NW_ && P1T_ == NW_,
+                "stage B items cover every (p1, p2) of the tile (no p1 split / sub-tiles)");
   static constexpr int NP1 = NW_ / P1T_;
   static_assert(NW_ % P1T_ == 0, "p1 tile must divide N_w");
   static constexpr int S = sizeof...(TK);
@@ -222,19 +223,7 @@ __device__ __forceinline__ void v2_stage_b(const V2Params<Sh>& p, const double* 
             dst[p1l * NV * NW + p2] = v;
           });
         };
-        if constexpr (Sh::PG == NW) {
-          // one item covers every p1: compile-time p1, no dispatch
-          static_for<0, NW>([&](auto p1c) { emit(p1c, decltype(p1c)::value); });
-        } else {
-#pragma unroll
-          for (int jg = 0; jg < Sh::PG; ++jg) {
-            const int p1l = pg * Sh::PG + jg;
-            const int p1 = p1base + p1l;
-            static_for<0, NW>([&](auto p1c) {
-              if (p1 == decltype(p1c)::value) emit(p1c, p1l);
-            });
-          }
-        }
+        static_for<0, NW>([&](auto p1c) { emit(p1c, decltype(p1c)::value); });
       }
     });
   });
