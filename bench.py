@@ -70,7 +70,8 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index),
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+                 "clocks.mem",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
@@ -84,7 +85,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, mem, reasons = [], [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         with open(self.path) as f:
             for line in f:
@@ -94,6 +95,9 @@ class ClockSampler:
                 try:
                     sm.append(float(parts[0]))
                     mx.append(float(parts[1]))
+                    pw.append(float(parts[2]))
+                    if len(parts) > 8:
+                        mem.append(float(parts[8]))
                 except ValueError:
                     continue
                 for n, v in zip(names, parts[4:8]):
@@ -102,7 +106,9 @@ class ClockSampler:
         os.unlink(self.path)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "sm_mhz_min": min(sm) if sm else None,
+                "power_w_median": statistics.median(pw) if pw else None,
+                "mem_mhz_median": statistics.median(mem) if mem else None}
 
 
 # ---------------------------------------------------------------- CPU oracle baseline
