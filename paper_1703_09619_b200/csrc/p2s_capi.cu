@@ -328,13 +328,16 @@ using mv2_pack_fn = std::vector<double> (*)(const std::vector<double> (*)[3]);
 template <class Ms>
 std::vector<double> pack_mv2(const std::vector<double> (*phi)[3]) {
   // phi[s][d] = [K][nq] full weighted table -> half tables [K][H]
-  std::vector<double> out(static_cast<size_t>(Ms::TTOT), 0.0);
+  std::vector<double> out(static_cast<size_t>(Ms::TALL), 0.0);
   for (int s = 0; s < Ms::S; ++s)
     for (int d = 0; d < 3; ++d) {
       const int K = Ms::K(s, d), Q = Ms::Q(d), H = Ms::H(d);
       for (int k = 0; k < K; ++k)
-        for (int h = 0; h < H; ++h)
-          out[static_cast<size_t>(Ms::toff(s, d) + k * H + h)] = phi[s][d][static_cast<size_t>(k) * Q + h];
+        for (int h = 0; h < H; ++h) {
+          const double v = phi[s][d][static_cast<size_t>(k) * Q + h];
+          out[static_cast<size_t>(Ms::toff(s, d) + k * H + h)] = v;
+          out[static_cast<size_t>(Ms::ttoff(d) + k * H + h)] = v;  // shared (identical rows)
+        }
     }
   return out;
 }
@@ -348,7 +351,7 @@ cudaError_t launch_mv2(const double* alpha, double* I, int64_t n_elem, int P, in
   p.P = P;
   p.n_units = n_elem * P * Ms::S;
   p.mom_per_elem = mom_per_elem;
-  std::memcpy(p.tab, packed.data(), sizeof(double) * Ms::TTOT);
+  std::memcpy(p.tab, packed.data(), sizeof(double) * Ms::TALL);
   if (p.n_units == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -433,7 +436,7 @@ cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_
   std::memcpy(p.c.cw, cpack.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));
   p.alpha = alpha;
   p.prefetch_stride = 0;
-  std::memcpy(p.tab, mpack.data(), sizeof(double) * Ms::TTOT);
+  std::memcpy(p.tab, mpack.data(), sizeof(double) * Ms::TALL);
   if (p.c.n_units == 0) return cudaSuccess;
   constexpr size_t smem = FusedLayout<Sh, Ms>::SMEM;
   static int blocks_per_sm = -1;

@@ -16,14 +16,15 @@ struct FusedParams {
   V2Params<Sh> c;      // contraction part (c.I unused)
   const double* alpha;
   int64_t prefetch_stride;  // resident CTAs on the GPU (non-persistent launch)
-  double tab[Ms::TTOT];
+  double tab[Ms::TALL];
 };
 
 template <class Sh, class Ms>
 struct FusedLayout {
   static_assert(Sh::MPP == Ms::MPP, "moment block layouts differ");
   static constexpr int AB = Sh::A_DBL + Sh::B_DBL;
-  static constexpr int WORK = AB > Ms::scratch_dbl() ? AB : Ms::scratch_dbl();
+  static constexpr int MS = Ms::scratch_all_dbl();
+  static constexpr int WORK = AB > MS ? AB : MS;
   static constexpr size_t SMEM = sizeof(double) * (size_t)(Sh::MPP + WORK);
 };
 
@@ -44,10 +45,7 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     if constexpr ((Ms::S * slab) % 2 == 0)  // 16-B granularity of the bulk prefetch
       if (threadIdx.x == 0 && unit + stride < p.c.n_units)
         prefetch_l2(a + stride * Ms::S * slab, static_cast<uint32_t>(Ms::S * slab * 8));
-    static_for<0, Ms::S>([&](auto sc) {
-      constexpr int s = decltype(sc)::value;
-      moments_unit<Ms, s, Sh::THREADS>(a + s * slab, p.tab, Abuf, Ibuf + Sh::moff(s));
-    });
+    moments_all_terms<Ms, Sh::THREADS>(a, p.tab, Abuf, Ibuf);
     double* Mbase =
         p.c.M + e * p.c.mat_stride + static_cast<int64_t>(gci * p.c.Nt) * p.c.ldM + gcj * p.c.Nt;
     v2_unit<Sh>(p.c, Ibuf, Abuf, Bbuf, Mbase, []() {});

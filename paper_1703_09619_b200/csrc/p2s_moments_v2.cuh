@@ -39,6 +39,29 @@ struct MShape {
     return o;
   }
   static constexpr int TTOT = toff(S - 1, 2) + K(S - 1, 2) * H(2);
+  // shared per-direction half tables (rows 0..KMAX(d)-1) used by moments_all_terms
+  static constexpr int KMAX(int d) {
+    int m = 0;
+    for (int s = 0; s < S; ++s) m = K(s, d) > m ? K(s, d) : m;
+    return m;
+  }
+  static constexpr int ttoff(int d) {
+    int o = TTOT;  // appended after the per-term tables
+    for (int e = 0; e < d; ++e) o += KMAX(e) * H(e);
+    return o;
+  }
+  static constexpr int TALL = ttoff(3);
+  static constexpr int t1off(int s) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) o += K(i, 0) * Q(2) * (Q(1) | 1);
+    return o;
+  }
+  static constexpr int t2off(int s) {
+    int o = t1off(S);
+    for (int i = 0; i < s; ++i) o += K(i, 0) * K(i, 1) * (Q(2) | 1);
+    return o;
+  }
+  static constexpr int scratch_all_dbl() { return (t2off(S) + 1) & ~1; }
   static constexpr int moff(int s) {
     int o = 0;
     for (int i = 0; i < s; ++i) o += K(i, 0) * K(i, 1) * K(i, 2);
@@ -66,7 +89,8 @@ struct MV2Params {
   int64_t n_units;     // E * P * S
   int P;
   int64_t mom_per_elem;
-  double tab[Ms::TTOT];  // per (s, d): [K][H] = w_h P_k(x_h), h < H (x_h <= 0)
+  double tab[Ms::TALL];  // per (s, d): [K][H] = w_h P_k(x_h), h < H (x_h <= 0); then shared
+                         // per-direction tables [KMAX][H]
 };
 
 // Even/odd folded contraction of one register fiber a[Q] against the half
@@ -144,6 +168,176 @@ __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const
 #pragma unroll
     for (int q = 0; q < QW; ++q) x[q] = src[q];
     fold_contract<QW, KW>(x, tw, [&](int k, double v) { Iout[r * KW + k] = v; });
+  });
+  __syncthreads();
+}
+
+// All terms of one (element, pair) at once: the kernel polynomials of every
+// term are the same Legendre P_k (only the count K differs), so one half-table
+// row (loaded once per thread) feeds every term that uses it, and the three
+// passes need three barriers for all terms.  alpha_s slabs are consecutive
+// (a + s * slab); Iout + moff(s) receives I_s.  Requires every term's tables
+// to be row prefixes of term kmax_term(d)'s table (true for Legendre kernels).
+template <class Ms, int NTHR>
+__device__ __forceinline__ void moments_all_terms(const double* __restrict__ a, const double* tab,
+                                                  double* scratch, double* Iout) {
+  constexpr int S = Ms::S;
+  constexpr int QU = Ms::Q(0), QV = Ms::Q(1), QW = Ms::Q(2);
+  constexpr int S2 = Ms::S2, S3 = Ms::S3;
+  constexpr int slab = QU * QV * QW;
+  // per-term scratch: T1_s [KU_s][QW][S2] then T2_s [KU_s*KV_s][S3]
+  auto t1 = [&](int s) { return scratch + Ms::t1off(s); };
+  auto t2 = [&](int s) { return scratch + Ms::t2off(s); };
+  // ---- pass u: thread = row (q_w, q_v) of every term
+  for_items<QW * QV, NTHR>([&](int r) {
+    const int q3 = r / QV, q2 = r - (r / QV) * QV;
+    constexpr int Hf = QU / 2, H = (QU + 1) / 2;
+    double ev[S][Hf > 0 ? Hf : 1], od[S][Hf > 0 ? Hf : 1], mid[S];
+    static_for<0, S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      double x[QU];
+      const double* row = a + s * slab + static_cast<int64_t>(r) * QU;
+      if constexpr ((QU & 1) == 0) {
+#pragma unroll
+        for (int q = 0; q < QU / 2; ++q) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(row) + q);
+          x[2 * q] = v.x;
+          x[2 * q + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < QU; ++q) x[q] = __ldg(row + q);
+      }
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        ev[s][h] = x[h] + x[QU - 1 - h];
+        od[s][h] = x[h] - x[QU - 1 - h];
+      }
+      mid[s] = (QU & 1) ? x[Hf] : 0.0;
+    });
+    const double* tb = tab + Ms::ttoff(0);
+    static_for<0, Ms::KMAX(0)>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      double v[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) v[s] = 0.0;
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        const double c = tb[k * H + h];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 0)) v[s] = fma(c, (k & 1) ? od[s][h] : ev[s][h], v[s]);
+        });
+      }
+      if constexpr ((QU & 1) && (k & 1) == 0) {
+        const double c = tb[k * H + Hf];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 0)) v[s] = fma(c, mid[s], v[s]);
+        });
+      }
+      static_for<0, S>([&](auto sc) {
+        constexpr int s = decltype(sc)::value;
+        if constexpr (k < Ms::K(s, 0)) t1(s)[(k * QW + q3) * S2 + q2] = v[s];
+      });
+    });
+  });
+  __syncthreads();
+  // ---- pass v: thread = (k1, q_w) for every term with k1 < KU_s
+  for_items<Ms::KMAX(0) * QW, NTHR>([&](int r) {
+    const int k1 = r / QW, q3 = r - (r / QW) * QW;
+    constexpr int Hf = QV / 2, H = (QV + 1) / 2;
+    double ev[S][Hf > 0 ? Hf : 1], od[S][Hf > 0 ? Hf : 1], mid[S];
+    static_for<0, S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      const int kk = k1 < Ms::K(s, 0) ? k1 : 0;
+      const double* src = t1(s) + (kk * QW + q3) * S2;
+      double x[QV];
+#pragma unroll
+      for (int q = 0; q < QV; ++q) x[q] = src[q];
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        ev[s][h] = x[h] + x[QV - 1 - h];
+        od[s][h] = x[h] - x[QV - 1 - h];
+      }
+      mid[s] = (QV & 1) ? x[Hf] : 0.0;
+    });
+    const double* tb = tab + Ms::ttoff(1);
+    static_for<0, Ms::KMAX(1)>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      double v[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) v[s] = 0.0;
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        const double c = tb[k * H + h];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 1)) v[s] = fma(c, (k & 1) ? od[s][h] : ev[s][h], v[s]);
+        });
+      }
+      if constexpr ((QV & 1) && (k & 1) == 0) {
+        const double c = tb[k * H + Hf];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 1)) v[s] = fma(c, mid[s], v[s]);
+        });
+      }
+      static_for<0, S>([&](auto sc) {
+        constexpr int s = decltype(sc)::value;
+        if constexpr (k < Ms::K(s, 1))
+          if (k1 < Ms::K(s, 0)) t2(s)[(k1 * Ms::K(s, 1) + k) * S3 + q3] = v[s];
+      });
+    });
+  });
+  __syncthreads();
+  // ---- pass w: thread = (k1, k2) over the largest term's (K_u, K_v) grid
+  for_items<Ms::KMAX(0) * Ms::KMAX(1), NTHR>([&](int r) {
+    const int k1 = r / Ms::KMAX(1), k2 = r - (r / Ms::KMAX(1)) * Ms::KMAX(1);
+    constexpr int Hf = QW / 2, H = (QW + 1) / 2;
+    double ev[S][Hf > 0 ? Hf : 1], od[S][Hf > 0 ? Hf : 1], mid[S];
+    static_for<0, S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      const bool in = k1 < Ms::K(s, 0) && k2 < Ms::K(s, 1);
+      const double* src = t2(s) + (in ? (k1 * Ms::K(s, 1) + k2) : 0) * S3;
+      double x[QW];
+#pragma unroll
+      for (int q = 0; q < QW; ++q) x[q] = src[q];
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        ev[s][h] = x[h] + x[QW - 1 - h];
+        od[s][h] = x[h] - x[QW - 1 - h];
+      }
+      mid[s] = (QW & 1) ? x[Hf] : 0.0;
+    });
+    const double* tb = tab + Ms::ttoff(2);
+    static_for<0, Ms::KMAX(2)>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      double v[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) v[s] = 0.0;
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        const double c = tb[k * H + h];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 2)) v[s] = fma(c, (k & 1) ? od[s][h] : ev[s][h], v[s]);
+        });
+      }
+      if constexpr ((QW & 1) && (k & 1) == 0) {
+        const double c = tb[k * H + Hf];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 2)) v[s] = fma(c, mid[s], v[s]);
+        });
+      }
+      static_for<0, S>([&](auto sc) {
+        constexpr int s = decltype(sc)::value;
+        if constexpr (k < Ms::K(s, 2))
+          if (k1 < Ms::K(s, 0) && k2 < Ms::K(s, 1))
+            Iout[Ms::moff(s) + (k1 * Ms::K(s, 1) + k2) * Ms::K(s, 2) + k] = v[s];
+      });
+    });
   });
   __syncthreads();
 }
