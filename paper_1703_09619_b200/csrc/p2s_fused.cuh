@@ -45,7 +45,10 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     if constexpr ((Ms::S * slab) % 2 == 0)  // 16-B granularity of the bulk prefetch
       if (threadIdx.x == 0 && unit + stride < p.c.n_units)
         prefetch_l2(a + stride * Ms::S * slab, static_cast<uint32_t>(Ms::S * slab * 8));
-    moments_all_terms<Ms, Sh::THREADS>(a, p.tab, Abuf, Ibuf);
+    if constexpr (Ms::WFIRST)
+      moments_all_terms_wfirst<Ms, Sh::THREADS>(a, p.tab, Abuf, Ibuf);
+    else
+      moments_all_terms<Ms, Sh::THREADS>(a, p.tab, Abuf, Ibuf);
     double* Mbase =
         p.c.M + e * p.c.mat_stride + static_cast<int64_t>(gci * p.c.Nt) * p.c.ldM + gcj * p.c.Nt;
     v2_unit<Sh>(p.c, Ibuf, Abuf, Bbuf, Mbase, []() {});

@@ -61,7 +61,22 @@ struct MShape {
     for (int i = 0; i < s; ++i) o += K(i, 0) * K(i, 1) * (Q(2) | 1);
     return o;
   }
-  static constexpr int scratch_all_dbl() { return (t2off(S) + 1) & ~1; }
+  // w-first pass order (moments_all_terms_wfirst)
+  static constexpr int w1off(int s) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) o += K(i, 2) * Q(1) * (Q(0) | 1);
+    return o;
+  }
+  static constexpr int w2off(int s) {
+    int o = w1off(S);
+    for (int i = 0; i < s; ++i) o += K(i, 2) * K(i, 1) * (Q(0) | 1);
+    return o;
+  }
+  // pass order: w first when it is the direction with the fewest kernel polynomials
+  static constexpr bool WFIRST = KMAX(2) < KMAX(0);
+  static constexpr int scratch_all_dbl() {
+    return WFIRST ? (w2off(S) + 1) & ~1 : (t2off(S) + 1) & ~1;
+  }
   static constexpr int moff(int s) {
     int o = 0;
     for (int i = 0; i < s; ++i) o += K(i, 0) * K(i, 1) * K(i, 2);
@@ -336,6 +351,167 @@ __device__ __forceinline__ void moments_all_terms(const double* __restrict__ a, 
         if constexpr (k < Ms::K(s, 2))
           if (k1 < Ms::K(s, 0) && k2 < Ms::K(s, 1))
             Iout[Ms::moff(s) + (k1 * Ms::K(s, 1) + k2) * Ms::K(s, 2) + k] = v[s];
+      });
+    });
+  });
+  __syncthreads();
+}
+
+// Same as moments_all_terms with the passes in the order w, v, u (cheaper and
+// a smaller scratch when K_w < K_u, e.g. C4's (10, 6, 4)):
+//   pass w: thread = (q_v, q_u) column, fiber along q_w (lanes read
+//           consecutive q_u: every load instruction is 256 contiguous bytes)
+//   pass v: thread = (k3, q_u), fiber along q_v of W1[k3][q_v][q_u]
+//   pass u: thread = (k3, k2), fiber along q_u of W2[k3*KV + k2][q_u]
+template <class Ms, int NTHR>
+__device__ __forceinline__ void moments_all_terms_wfirst(const double* __restrict__ a,
+                                                         const double* tab, double* scratch,
+                                                         double* Iout) {
+  constexpr int S = Ms::S;
+  constexpr int QU = Ms::Q(0), QV = Ms::Q(1), QW = Ms::Q(2);
+  constexpr int SU = QU | 1;  // odd row stride over q_u
+  constexpr int slab = QU * QV * QW;
+  auto w1 = [&](int s) { return scratch + Ms::w1off(s); };   // [KW_s][QV][SU]
+  auto w2 = [&](int s) { return scratch + Ms::w2off(s); };   // [KW_s*KV_s][SU]
+  // ---- pass w
+  for_items<QV * QU, NTHR>([&](int r) {
+    constexpr int Hf = QW / 2, H = (QW + 1) / 2;
+    const int q2 = r / QU, q1 = r - (r / QU) * QU;
+    double ev[S][Hf > 0 ? Hf : 1], od[S][Hf > 0 ? Hf : 1], mid[S];
+    static_for<0, S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      const double* col = a + s * slab + r;
+      double x[QW];
+#pragma unroll
+      for (int q = 0; q < QW; ++q) x[q] = __ldg(col + q * (QU * QV));
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        ev[s][h] = x[h] + x[QW - 1 - h];
+        od[s][h] = x[h] - x[QW - 1 - h];
+      }
+      mid[s] = (QW & 1) ? x[Hf] : 0.0;
+    });
+    const double* tb = tab + Ms::ttoff(2);
+    static_for<0, Ms::KMAX(2)>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      double v[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) v[s] = 0.0;
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        const double c = tb[k * H + h];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 2)) v[s] = fma(c, (k & 1) ? od[s][h] : ev[s][h], v[s]);
+        });
+      }
+      if constexpr ((QW & 1) && (k & 1) == 0) {
+        const double c = tb[k * H + Hf];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 2)) v[s] = fma(c, mid[s], v[s]);
+        });
+      }
+      static_for<0, S>([&](auto sc) {
+        constexpr int s = decltype(sc)::value;
+        if constexpr (k < Ms::K(s, 2)) w1(s)[(k * QV + q2) * SU + q1] = v[s];
+      });
+    });
+  });
+  __syncthreads();
+  // ---- pass v
+  for_items<Ms::KMAX(2) * QU, NTHR>([&](int r) {
+    constexpr int Hf = QV / 2, H = (QV + 1) / 2;
+    const int k3 = r / QU, q1 = r - (r / QU) * QU;
+    double ev[S][Hf > 0 ? Hf : 1], od[S][Hf > 0 ? Hf : 1], mid[S];
+    static_for<0, S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      const int kk = k3 < Ms::K(s, 2) ? k3 : 0;
+      const double* src = w1(s) + kk * QV * SU + q1;
+      double x[QV];
+#pragma unroll
+      for (int q = 0; q < QV; ++q) x[q] = src[q * SU];
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        ev[s][h] = x[h] + x[QV - 1 - h];
+        od[s][h] = x[h] - x[QV - 1 - h];
+      }
+      mid[s] = (QV & 1) ? x[Hf] : 0.0;
+    });
+    const double* tb = tab + Ms::ttoff(1);
+    static_for<0, Ms::KMAX(1)>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      double v[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) v[s] = 0.0;
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        const double c = tb[k * H + h];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 1)) v[s] = fma(c, (k & 1) ? od[s][h] : ev[s][h], v[s]);
+        });
+      }
+      if constexpr ((QV & 1) && (k & 1) == 0) {
+        const double c = tb[k * H + Hf];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 1)) v[s] = fma(c, mid[s], v[s]);
+        });
+      }
+      static_for<0, S>([&](auto sc) {
+        constexpr int s = decltype(sc)::value;
+        if constexpr (k < Ms::K(s, 1))
+          if (k3 < Ms::K(s, 2)) w2(s)[(k3 * Ms::K(s, 1) + k) * SU + q1] = v[s];
+      });
+    });
+  });
+  __syncthreads();
+  // ---- pass u
+  for_items<Ms::KMAX(2) * Ms::KMAX(1), NTHR>([&](int r) {
+    constexpr int Hf = QU / 2, H = (QU + 1) / 2;
+    const int k3 = r / Ms::KMAX(1), k2 = r - (r / Ms::KMAX(1)) * Ms::KMAX(1);
+    double ev[S][Hf > 0 ? Hf : 1], od[S][Hf > 0 ? Hf : 1], mid[S];
+    static_for<0, S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      const bool in = k3 < Ms::K(s, 2) && k2 < Ms::K(s, 1);
+      const double* src = w2(s) + (in ? (k3 * Ms::K(s, 1) + k2) : 0) * SU;
+      double x[QU];
+#pragma unroll
+      for (int q = 0; q < QU; ++q) x[q] = src[q];
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        ev[s][h] = x[h] + x[QU - 1 - h];
+        od[s][h] = x[h] - x[QU - 1 - h];
+      }
+      mid[s] = (QU & 1) ? x[Hf] : 0.0;
+    });
+    const double* tb = tab + Ms::ttoff(0);
+    static_for<0, Ms::KMAX(0)>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      double v[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) v[s] = 0.0;
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        const double c = tb[k * H + h];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 0)) v[s] = fma(c, (k & 1) ? od[s][h] : ev[s][h], v[s]);
+        });
+      }
+      if constexpr ((QU & 1) && (k & 1) == 0) {
+        const double c = tb[k * H + Hf];
+        static_for<0, S>([&](auto sc) {
+          constexpr int s = decltype(sc)::value;
+          if constexpr (k < Ms::K(s, 0)) v[s] = fma(c, mid[s], v[s]);
+        });
+      }
+      static_for<0, S>([&](auto sc) {
+        constexpr int s = decltype(sc)::value;
+        if constexpr (k < Ms::K(s, 0))
+          if (k3 < Ms::K(s, 2) && k2 < Ms::K(s, 1))
+            Iout[Ms::moff(s) + (k * Ms::K(s, 1) + k2) * Ms::K(s, 2) + k3] = v[s];
       });
     });
   });
