@@ -489,10 +489,14 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),                     // C2
       make_fused<Shape<6, 6, 6, 1, 6, 6, 224, 2, 4, 1, kPPP, kDDD>,
                  MShape<6, 6, 6, 14, 14, 14, 224, kPPP, kDDD>>(),
-      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>,
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 6, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),                     // C3
-      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 1, kPPP, kDDD>,
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 6, 1, kPPP, kDDD>,
+                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 512, 1, 6, 1, kPPP, kDDD>,
+                 MShape<8, 8, 8, 20, 20, 20, 512, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),                    // C4
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 4, 1, kPPP, kDDD>,
