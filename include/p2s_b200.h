@@ -150,6 +150,43 @@ const char* p2s_version(void);
  * kernel, two-stage specialised, or the runtime-shaped generic kernels). */
 const char* p2s_kernel_path(const p2s_ctx* ctx);
 
+/* ------------------------------------------------------------------------
+ * 2-D Chebyshev mode: the reference's own specialisation (Sec. III;
+ * chebfem, 2-component curl-curl element with E_u = U_m(u) T_n(v), m < M,
+ * n <= N and E_v = T_m(u) U_n(v)), on the GPU, for drop-in parity with
+ * chebfem::compute_kernel_tables / assemble_p2s_element (assembly.hpp:52-56).
+ *   grids   [E][4][nq][nq]  ws, wuu, wuv, wvv of build_element_quad
+ *                           (assembly.cpp:102-106), [i_u][j_v], weights folded
+ *   tables  [E][...]        Ks, Kuu, Kuv, Kvv, row-major [u degree][v degree]
+ *   blocks  [E][...]        Suu, Suv, Svu, Svv, Muu, Muv, Mvu, Mvv, row-major
+ *                           (E_u index m*(N+1)+n, E_v index m*N+n)
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t M, N;  /* orders (chebfem::Orders) */
+  int32_t nq;    /* Gauss-Legendre points per direction */
+} p2s_cheb2d_problem;
+
+typedef struct {
+  int64_t grids_per_elem, tables_per_elem, blocks_per_elem;
+  int64_t table_offset[4];
+  int64_t block_offset[8];
+  int32_t table_rows[4], table_cols[4];
+  int32_t block_rows[8], block_cols[8];
+  int32_t n_eu, n_ev;
+} p2s_cheb2d_sizes;
+
+typedef struct p2s_cheb2d_ctx p2s_cheb2d_ctx;
+
+p2s_status p2s_cheb2d_create(const p2s_cheb2d_problem* spec, int device, p2s_cheb2d_ctx** out);
+void p2s_cheb2d_destroy(p2s_cheb2d_ctx* ctx);
+p2s_status p2s_cheb2d_get_sizes(const p2s_cheb2d_ctx* ctx, p2s_cheb2d_sizes* out);
+/* compute_kernel_tables (assembly.cpp:276-314) for n_elem elements */
+p2s_status p2s_cheb2d_kernel_tables(p2s_cheb2d_ctx* ctx, const double* d_grids, double* d_tables,
+                                    int64_t n_elem, void* stream);
+/* assemble_p2s_element (assembly.cpp:375-474) for n_elem elements */
+p2s_status p2s_cheb2d_assemble(p2s_cheb2d_ctx* ctx, const double* d_tables, double* d_blocks,
+                               int64_t n_elem, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

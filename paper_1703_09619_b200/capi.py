@@ -26,7 +26,9 @@ _STATUS = {0: "P2S_OK", 1: "P2S_INVALID_ARG", 2: "P2S_CUDA_ERROR", 3: "P2S_UNSUP
 EXPORTS = ("p2s_create", "p2s_destroy", "p2s_get_sizes", "p2s_moments", "p2s_contract",
            "p2s_fill", "p2s_fill_host", "p2s_alpha_generate", "p2s_get_tables",
            "p2s_set_profiling", "p2s_get_stage_times", "p2s_shape_supported", "p2s_last_error",
-           "p2s_version", "p2s_kernel_path", "p2s_moments_host", "p2s_contract_host")
+           "p2s_version", "p2s_kernel_path", "p2s_moments_host", "p2s_contract_host",
+           "p2s_cheb2d_create", "p2s_cheb2d_destroy", "p2s_cheb2d_get_sizes",
+           "p2s_cheb2d_kernel_tables", "p2s_cheb2d_assemble")
 
 
 class P2SError(RuntimeError):
@@ -50,6 +52,20 @@ class Problem(C.Structure):
         ("n_terms", C.c_int32),
         ("kind", (C.c_int32 * 3) * MAX_TERMS),
         ("nq", C.c_int32 * 3),
+    ]
+
+
+class Cheb2dProblem(C.Structure):
+    _fields_ = [("M", C.c_int32), ("N", C.c_int32), ("nq", C.c_int32)]
+
+
+class Cheb2dSizes(C.Structure):
+    _fields_ = [
+        ("grids_per_elem", C.c_int64), ("tables_per_elem", C.c_int64),
+        ("blocks_per_elem", C.c_int64), ("table_offset", C.c_int64 * 4),
+        ("block_offset", C.c_int64 * 8), ("table_rows", C.c_int32 * 4),
+        ("table_cols", C.c_int32 * 4), ("block_rows", C.c_int32 * 8),
+        ("block_cols", C.c_int32 * 8), ("n_eu", C.c_int32), ("n_ev", C.c_int32),
     ]
 
 
@@ -104,9 +120,15 @@ def lib():
         L.p2s_version.restype = C.c_char_p
         L.p2s_kernel_path.argtypes = [vp]
         L.p2s_kernel_path.restype = C.c_char_p
+        L.p2s_cheb2d_create.argtypes = [C.POINTER(Cheb2dProblem), C.c_int, C.POINTER(vp)]
+        L.p2s_cheb2d_destroy.argtypes = [vp]
+        L.p2s_cheb2d_destroy.restype = None
+        L.p2s_cheb2d_get_sizes.argtypes = [vp, C.POINTER(Cheb2dSizes)]
+        L.p2s_cheb2d_kernel_tables.argtypes = [vp, vp, vp, i64, vp]
+        L.p2s_cheb2d_assemble.argtypes = [vp, vp, vp, i64, vp]
         for f in EXPORTS:
             if f not in ("p2s_destroy", "p2s_shape_supported", "p2s_last_error", "p2s_version",
-                         "p2s_kernel_path"):
+                         "p2s_kernel_path", "p2s_cheb2d_destroy"):
                 getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -240,3 +262,51 @@ class Context:
         _check(lib().p2s_get_stage_times(self.h, C.byref(a), C.byref(b), C.byref(na), C.byref(nb)))
         return {"ms_moments": a.value, "ms_contract": b.value, "n_moments": na.value,
                 "n_contract": nb.value}
+
+
+TABLE_NAMES = ("Ks", "Kuu", "Kuv", "Kvv")
+BLOCK_NAMES = ("Suu", "Suv", "Svu", "Svv", "Muu", "Muv", "Mvu", "Mvv")
+
+
+class Cheb2dContext:
+    """The reference's 2-D Chebyshev element (chebfem) on the GPU:
+    kernel_tables() ~ compute_kernel_tables, assemble() ~ assemble_p2s_element."""
+
+    def __init__(self, M, N, nq, device: int = 0):
+        self.M, self.N, self.nq = M, N, nq
+        pb = Cheb2dProblem(M, N, nq)
+        h = C.c_void_p()
+        _check(lib().p2s_cheb2d_create(C.byref(pb), device, C.byref(h)))
+        self.h = h
+        sz = Cheb2dSizes()
+        _check(lib().p2s_cheb2d_get_sizes(self.h, C.byref(sz)))
+        self.sizes = sz
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().p2s_cheb2d_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def kernel_tables(self, d_grids, d_tables, n_elem, stream=0):
+        _check(lib().p2s_cheb2d_kernel_tables(self.h, _ptr(d_grids), _ptr(d_tables), n_elem,
+                                              _ptr(stream)))
+
+    def assemble(self, d_tables, d_blocks, n_elem, stream=0):
+        _check(lib().p2s_cheb2d_assemble(self.h, _ptr(d_tables), _ptr(d_blocks), n_elem,
+                                         _ptr(stream)))
+
+    def split_tables(self, flat):
+        sz = self.sizes
+        return {n: flat[sz.table_offset[i]:sz.table_offset[i] + sz.table_rows[i] * sz.table_cols[i]]
+                .reshape(sz.table_rows[i], sz.table_cols[i]) for i, n in enumerate(TABLE_NAMES)}
+
+    def split_blocks(self, flat):
+        sz = self.sizes
+        return {n: flat[sz.block_offset[i]:sz.block_offset[i] + sz.block_rows[i] * sz.block_cols[i]]
+                .reshape(sz.block_rows[i], sz.block_cols[i]) for i, n in enumerate(BLOCK_NAMES)}

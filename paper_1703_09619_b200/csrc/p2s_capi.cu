@@ -785,6 +785,8 @@ p2s_status check_ctx(const p2s_ctx* c) {
 
 }  // namespace
 
+p2s_status p2s_internal_fail(p2s_status st, const std::string& msg) { return fail(st, msg); }
+
 extern "C" {
 
 const char* p2s_last_error(void) { return g_last_error.c_str(); }

@@ -105,4 +105,75 @@ std::vector<double> weighted_kernel_table(int K, const std::vector<double>& node
   return phi;
 }
 
+long double cheb_eval(int fam, int n, long double x) {
+  if (fam == CHEB_T || fam == CHEB_U) {
+    if (n == 0) return 1.0L;
+    long double p = 1.0L, q = (fam == CHEB_T) ? x : 2.0L * x;
+    for (int k = 1; k < n; ++k) {
+      const long double r = 2.0L * x * q - p;
+      p = q;
+      q = r;
+    }
+    return q;
+  }
+  // T^ns_n = (T_n - T_{n mod 2}) / (2 (1 - x^2)) as a T-series:
+  // T^ns_{2s} = -(s T_0 + sum_{m<s} 2(s-m) T_{2m}),  T^ns_{2s+1} = -sum_{q<s} 2(s-q) T_{2q+1}
+  if (n < 2) return 0.0L;
+  std::vector<long double> c(static_cast<size_t>(n - 1), 0.0L);
+  if (n % 2 == 0) {
+    const int s = n / 2;
+    c[0] = -static_cast<long double>(s);
+    for (int m = 1; m < s; ++m) c[static_cast<size_t>(2 * m)] = -2.0L * (s - m);
+  } else {
+    const int s = (n - 1) / 2;
+    for (int q = 0; q < s; ++q) c[static_cast<size_t>(2 * q + 1)] = -2.0L * (s - q);
+  }
+  long double b1 = 0.0L, b2 = 0.0L;
+  for (int k = static_cast<int>(c.size()) - 1; k >= 1; --k) {
+    const long double b = c[static_cast<size_t>(k)] + 2.0L * x * b1 - b2;
+    b2 = b1;
+    b1 = b;
+  }
+  return c[0] + x * b1 - b2;
+}
+
+namespace {
+void add_term(ChebTerm out[2], int& n, double coeff, int fam, int deg) {
+  if (coeff == 0.0) return;
+  for (int i = 0; i < n; ++i)
+    if (out[i].fam == fam && out[i].deg == deg) {
+      out[i].coeff += coeff;
+      if (out[i].coeff == 0.0) {
+        out[i] = out[n - 1];
+        --n;
+      }
+      return;
+    }
+  out[n++] = ChebTerm{coeff, fam, deg};
+}
+}  // namespace
+
+int cheb_product(int fa, int a, int fb, int b, ChebTerm out[2]) {
+  int n = 0;
+  if (fa == CHEB_U && fb == CHEB_U) {
+    // U_a U_b = T^ns_|a-b| - T^ns_{a+b+2}
+    add_term(out, n, 1.0, CHEB_TNS, a > b ? a - b : b - a);
+    add_term(out, n, -1.0, CHEB_TNS, a + b + 2);
+  } else if (fa == CHEB_T && fb == CHEB_T) {
+    // T_a T_b = (T_|a-b| + T_{a+b}) / 2
+    add_term(out, n, 0.5, CHEB_T, a > b ? a - b : b - a);
+    add_term(out, n, 0.5, CHEB_T, a + b);
+  } else {
+    // U_u T_t = (U_{u-t} + U_{u+t}) / 2 with signed U indices
+    const int u = (fa == CHEB_U) ? a : b, t = (fa == CHEB_U) ? b : a;
+    const int k = u - t;
+    if (k >= 0)
+      add_term(out, n, 0.5, CHEB_U, k);
+    else if (k <= -2)
+      add_term(out, n, -0.5, CHEB_U, -k - 2);
+    add_term(out, n, 0.5, CHEB_U, u + t);
+  }
+  return n;
+}
+
 }  // namespace p2s

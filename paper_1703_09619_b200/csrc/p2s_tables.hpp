@@ -57,4 +57,22 @@ std::vector<double> product_to_sum_table(int kind, int N);
 std::vector<double> weighted_kernel_table(int K, const std::vector<double>& nodes,
                                           const std::vector<double>& weights);
 
+// ---------------------------------------------------------------- 2-D Chebyshev mode
+// The reference's own specialisation (chebyshev.hpp / assembly.cpp):
+// families T_n, U_n and the nonsingular T^ns_n, and their <= 2-term exact
+// product-to-sum identities (Eq. (16)).
+enum ChebFamily : int { CHEB_T = 0, CHEB_U = 1, CHEB_TNS = 2 };
+
+// value of family fam, degree n at x (long-double recurrences; T^ns by
+// Clenshaw over its integer T-coefficients, finite at x = +-1)
+long double cheb_eval(int fam, int n, long double x);
+
+struct ChebTerm {
+  double coeff;
+  int fam, deg;
+};
+// product of two T/U polynomials rewritten as <= 2 terms (equal terms merged,
+// zero coefficients dropped); U_{-1} = 0, U_{-k} = -U_{k-2}
+int cheb_product(int fam_a, int a, int fam_b, int b, ChebTerm out[2]);
+
 }  // namespace p2s
