@@ -56,3 +56,18 @@ def test_gpu_reference_known_answers():
     assert abs(b["Muu"][0, 0] - 4.0) <= 4e-13
     assert abs(b["Suu"][1 * 3 + 1, 1 * 3 + 1] - 16 / 3) <= 16 / 3 * 1e-13
     assert np.array_equal(b["Svu"], b["Suv"].T) or O.block_close(b["Svu"], b["Suv"].T, 1e-14)[0]
+
+
+REF_DROPIN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                          "oracle", "_ref", "ref_dropin")
+
+
+@pytest.mark.skipif(not os.path.exists(REF_DROPIN),
+                    reason="oracle/_ref/ref_dropin not built (needs /root/reference at build time)")
+def test_reference_calls_gpu_fill_through_the_c_abi():
+    """The compiled reference fills seeded curved elements through the GPU and
+    checks them with its own element_matrices_close (oracle/refbuild/ref_dropin.cpp)."""
+    import subprocess
+    r = subprocess.run([REF_DROPIN], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "elements pass" in r.stdout
