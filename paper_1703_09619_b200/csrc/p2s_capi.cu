@@ -18,6 +18,7 @@
 #include "p2s_fused.cuh"
 #include "p2s_moments_v2.cuh"
 #include "p2s_kernels.cuh"
+#include "p2s_large.cuh"
 #include "p2s_tables.hpp"
 
 namespace p2s {
@@ -527,6 +528,167 @@ const FusedEntry* find_fused(const p2s_problem& pb) {
   return first;
 }
 
+// ------------------------------------------------------------ large-order registry
+
+struct LargeArgs {
+  const std::vector<double> (*phi)[3];            // [s][d] full tables
+  const std::vector<double>* dense[kMaxTerms][3];  // [s][d] [N][N][K]
+};
+
+struct LargePack {
+  std::vector<double> tab, cu, cvw;
+  double* d_cvw = nullptr;
+};
+
+using large_pack_fn = bool (*)(const LargeArgs&, LargePack&);
+using large_mom_fn = cudaError_t (*)(const double*, double*, int64_t, const LargePack&, cudaStream_t);
+using large_con_fn = cudaError_t (*)(const double*, double*, double*, int64_t, int64_t, int64_t, int,
+                                     int, int, const LargePack&, cudaStream_t);
+
+template <class Ls>
+bool pack_large(const LargeArgs& a, LargePack& out) {
+  out.tab.assign(static_cast<size_t>(Ls::TALL), 0.0);
+  for (int d = 0; d < 3; ++d) {
+    // shared rows: the term with the most kernel polynomials in this direction
+    int sb = 0;
+    for (int s = 0; s < Ls::S; ++s)
+      if (Ls::K(s, d) > Ls::K(sb, d)) sb = s;
+    const int Q = Ls::Q(d), H = Ls::H(d);
+    for (int k = 0; k < Ls::KMAX(d); ++k)
+      for (int h = 0; h < H; ++h)
+        out.tab[static_cast<size_t>(Ls::ttoff(d) + k * H + h)] =
+            a.phi[sb][d][static_cast<size_t>(k) * Q + h];
+  }
+  auto band_pack = [&](int d, std::vector<double>& v, size_t base) {
+    for (int s = 0; s < Ls::S; ++s) {
+      const int K = Ls::K(s, d), kd = Ls::kind(s, d), N = Ls::N(d);
+      const std::vector<double>& C = *a.dense[s][d];
+      for (int x = 0; x < N; ++x)
+        for (int y = 0; y < N; ++y) {
+          const int lo = band_lo(kd, x, y), cnt = band_count(kd, x, y);
+          for (int j = 0; j < cnt; ++j)
+            v[base + static_cast<size_t>(Ls::coff(d, s, x, y) + j)] =
+                C[(static_cast<size_t>(x) * N + y) * K + lo + 2 * j];
+        }
+    }
+  };
+  out.cu.assign(static_cast<size_t>(Ls::ctot(0)), 0.0);
+  band_pack(0, out.cu, 0);
+  out.cvw.assign(static_cast<size_t>(Ls::ctot(1) + Ls::ctot(2)), 0.0);
+  band_pack(1, out.cvw, 0);
+  band_pack(2, out.cvw, static_cast<size_t>(Ls::ctot(1)));
+  if (cudaMalloc(&out.d_cvw, sizeof(double) * out.cvw.size()) != cudaSuccess) return false;
+  return cudaMemcpy(out.d_cvw, out.cvw.data(), sizeof(double) * out.cvw.size(),
+                    cudaMemcpyHostToDevice) == cudaSuccess;
+}
+
+template <class Ls>
+cudaError_t launch_large_moments(const double* alpha, double* I, int64_t n_units, const LargePack& pk,
+                                 cudaStream_t st) {
+  LMomParams<Ls> p;
+  p.alpha = alpha;
+  p.I = I;
+  p.n_units = n_units;
+  std::memcpy(p.tab, pk.tab.data(), sizeof(double) * Ls::TALL);
+  if (n_units == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(large_moments_kernel<Ls>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ls::MOM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  large_moments_kernel<Ls><<<static_cast<unsigned>(n_units * Ls::S * Ls::NCH), 256, Ls::MOM_SMEM, st>>>(p);
+  return cudaGetLastError();
+}
+
+// contraction of n_units units from I (device) via the X scratch (chunks of xchunk units)
+template <class Ls>
+cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t n_units,
+                                  int64_t xchunk, int64_t ldM, int nc, int P, int Nt,
+                                  const LargePack& pk, cudaStream_t st) {
+  static bool attr = false;
+  constexpr size_t vw_smem = large_vw_smem<Ls>();
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(large_vw_kernel<Ls>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vw_smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  LUParams<Ls> up;
+  up.M = M;
+  up.ldM = ldM;
+  up.mat_stride = static_cast<int64_t>(nc) * Nt * ldM;
+  up.nc = nc;
+  up.P = P;
+  up.Nt = Nt;
+  std::memcpy(up.cu, pk.cu.data(), sizeof(double) * Ls::ctot(0));
+  for (int64_t u0 = 0; u0 < n_units; u0 += xchunk) {
+    const int64_t cnt = std::min(xchunk, n_units - u0);
+    LVWParams<Ls> vp;
+    vp.I = I + u0 * Ls::MPP;
+    vp.X = X;
+    vp.cvw = pk.d_cvw;
+    vp.n_units = cnt;
+    large_vw_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), 256, vw_smem, st>>>(vp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // u stage: absolute units u0 .. u0+cnt-1; X holds the chunk
+    up.X = X;
+    up.n_units = cnt;
+    large_u_dispatch<Ls>(up, u0, cnt, st);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+struct LargeEntry {
+  int order[3], nq[3], S;
+  int kinds[kMaxTerms][3];
+  large_pack_fn pack;
+  large_mom_fn moments;
+  large_con_fn contract;
+  int64_t mpp, xpu;
+};
+
+template <class Ls>
+LargeEntry make_large() {
+  LargeEntry r{};
+  for (int d = 0; d < 3; ++d) {
+    r.order[d] = Ls::N(d);
+    r.nq[d] = Ls::Q(d);
+  }
+  r.S = Ls::S;
+  for (int s = 0; s < Ls::S; ++s)
+    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Ls::kind(s, d);
+  r.pack = &pack_large<Ls>;
+  r.moments = &launch_large_moments<Ls>;
+  r.contract = &launch_large_contract<Ls>;
+  r.mpp = Ls::MPP;
+  r.xpu = Ls::XPU;
+  return r;
+}
+
+const std::vector<LargeEntry>& large_registry() {
+  static const std::vector<LargeEntry> reg = {
+      make_large<LShape<16, 16, 16, 36, 36, 36, 8, kPPP, kDDD>>(),   // C5
+      make_large<LShape<5, 4, 3, 8, 8, 6, 4, kPPP, kDDD>>(),         // test shape
+  };
+  return reg;
+}
+
+const LargeEntry* find_large(const p2s_problem& pb) {
+  for (const LargeEntry& r : large_registry()) {
+    bool ok = r.S == pb.n_terms;
+    for (int d = 0; d < 3; ++d) ok = ok && r.order[d] == pb.order[d] && r.nq[d] == pb.nq[d];
+    for (int s = 0; ok && s < r.S; ++s)
+      for (int d = 0; d < 3; ++d) ok = ok && r.kinds[s][d] == pb.kind[s][d];
+    if (ok) return &r;
+  }
+  return nullptr;
+}
+
 // ------------------------------------------------------------ moment launch
 
 template <int KMAX>
@@ -572,6 +734,10 @@ struct p2s_ctx {
   const RegEntry* entry = nullptr;
   const V2Entry* v2 = nullptr;
   const MV2Entry* mv2 = nullptr;
+  const LargeEntry* large = nullptr;
+  LargePack lpack;
+  double* d_X = nullptr;
+  int64_t xchunk = 1;
   const FusedEntry* fused = nullptr;
   std::vector<double> fused_cpack, fused_mpack;
   std::vector<double> mv2_packed;
@@ -674,7 +840,9 @@ p2s_status run_moments(p2s_ctx* c, const double* alpha, double* I, int64_t n, cu
     cudaEventRecord(e0, st);
   }
   cudaError_t err;
-  if (c->mv2 && !c->force_generic)
+  if (c->large)
+    err = c->large->moments(alpha, I, n * p.P, c->lpack, st);
+  else if (c->mv2 && !c->force_generic)
     err = c->mv2->launch(alpha, I, n, p.P, p.mom_per_elem, c->mv2_packed, st);
   else
     err = launch_moments(c->kmax, p, c->mom_smem, st);
@@ -721,7 +889,10 @@ p2s_status run_contract(p2s_ctx* c, const double* I, double* M, int64_t ldM, int
     cudaEventRecord(e0, st);
   }
   cudaError_t err;
-  if (c->v2 && !c->force_generic) {
+  if (c->large) {
+    err = c->large->contract(I, c->d_X, M, n * c->sz.n_pairs, c->xchunk, ldM, c->pb.n_comp,
+                             c->sz.n_pairs, a.Nt, c->lpack, st);
+  } else if (c->v2 && !c->force_generic) {
     V2Args v;
     v.I = I;
     v.M = M;
@@ -795,6 +966,7 @@ const char* p2s_version(void) { return "p2s_b200 0.1 (sm_100a)"; }
 
 const char* p2s_kernel_path(const p2s_ctx* c) {
   if (!c) return "";
+  if (c->large) return "large-order: large_moments_kernel + large_vw_kernel + large_u_kernel";
   if (c->fused) return "fused: fill_fused_kernel (moments + contraction, one persistent kernel)";
   if (c->v2 && !c->force_generic)
     return c->mv2 ? "two-stage: moments_v2_kernel + contract_v2_kernel"
@@ -805,7 +977,7 @@ const char* p2s_kernel_path(const p2s_ctx* c) {
 
 int p2s_shape_supported(const p2s_problem* spec) {
   if (!spec || validate(spec) != P2S_OK) return 0;
-  return find_entry(*spec) != nullptr || find_v2(*spec) != nullptr;
+  return find_entry(*spec) != nullptr || find_v2(*spec) != nullptr || find_large(*spec) != nullptr;
 }
 
 p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
@@ -815,7 +987,8 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
   if (st != P2S_OK) return st;
   const RegEntry* entry = find_entry(*spec);
   const V2Entry* v2e = find_v2(*spec);
-  if (!entry && !v2e)
+  const LargeEntry* lge = find_large(*spec);
+  if (!entry && !v2e && !lge)
     return fail(P2S_UNSUPPORTED_SHAPE, "p2s_create: no compiled contraction kernel for N_u=" +
                                            std::to_string(spec->order[0]) + " with these u-kinds");
   int ndev = 0;
@@ -914,7 +1087,7 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
     msm = std::max(msm, t);
   }
   c->mom_smem = msm * sizeof(double);
-  if (c->mom_smem > 227 * 1024)
+  if (!lge && c->mom_smem > 227 * 1024)
     return fail(P2S_UNSUPPORTED_SHAPE, "moment stage needs more than 227 KB of shared memory");
 
   // contraction plan: G n1-values per CTA, ~256 fibers per CTA
@@ -934,10 +1107,21 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
   c->plan.NG = (Nv + G - 1) / G;
   c->plan.threads = std::min(256, ((G * per_n1 + 31) / 32) * 32);
   c->plan.smem = contract_smem(G);
-  if (!v2e && c->plan.smem > 227 * 1024)
+  if (!v2e && !lge && c->plan.smem > 227 * 1024)
     return fail(P2S_UNSUPPORTED_SHAPE, "contraction stage needs more than 227 KB of shared memory");
-  if (c->sz.moments_per_pair * 8 >= (1 << 20))
+  if (!lge && c->sz.moments_per_pair * 8 >= (1 << 20))
     return fail(P2S_UNSUPPORTED_SHAPE, "moment block above the bulk-copy transaction limit");
+  if (lge) {
+    c->large = lge;
+    LargeArgs la{};
+    la.phi = c->phi;
+    for (int s = 0; s < S; ++s)
+      for (int d = 0; d < 3; ++d) la.dense[s][d] = &c->coef[s][d];
+    if (!lge->pack(la, c->lpack)) return fail(P2S_CUDA_ERROR, "p2s_create: large-path table upload");
+    // X chunk: ~64 MB of triangle-packed intermediates stays L2-resident between stages
+    c->xchunk = std::max<int64_t>(1, (int64_t(64) << 20) / (lge->xpu * 8));
+    P2S_CUDA(cudaMalloc(&c->d_X, sizeof(double) * lge->xpu * c->xchunk));
+  }
 
   // scheduler chunk: moment scratch of ~32 MB stays in L2 between the stages
   const int64_t per = c->sz.moments_per_elem * 8;
@@ -959,6 +1143,8 @@ void p2s_destroy(p2s_ctx* c) {
   for (int d = 0; d < 3; ++d)
     if (c->d_x[d]) cudaFree(c->d_x[d]);
   if (c->d_scratch) cudaFree(c->d_scratch);
+  if (c->d_X) cudaFree(c->d_X);
+  if (c->lpack.d_cvw) cudaFree(c->lpack.d_cvw);
   for (int i = 0; i < 2; ++i) {
     if (c->d_ring_alpha[i]) cudaFree(c->d_ring_alpha[i]);
     if (c->d_ring_M[i]) cudaFree(c->d_ring_M[i]);

@@ -199,3 +199,22 @@ def test_error_paths():
         capi.Context(1, (7, 3, 3), [DP], (5, 5, 5))
     with pytest.raises(capi.InvalidArgument):
         capi.Context(1, (0, 3, 3), [PP], (5, 5, 5))
+
+
+@pytest.mark.parametrize("n_comp", [1, 3])
+def test_large_order_path_small_shape(n_comp):
+    # the three-kernel large-order path (p2s_large.cuh) on a registered small shape
+    ctx = capi.Context(n_comp, (5, 4, 3), [PP, DD], (8, 8, 6))
+    assert ctx.kernel_path.startswith("large-order")
+    _check_case(n_comp, (5, 4, 3), [PP, DD], (8, 8, 6),
+                O.ALPHA_JACOBIAN if n_comp == 3 else O.ALPHA_SINE, 0.5, 3.0, n_elem=5)
+
+
+def test_c5_matches_oracle():
+    # BASELINE config 5 (order 16, 36^3 points): 134 MB per element matrix
+    cfg = CONFIGS["c5"]
+    ctx = capi.Context(**cfg.problem())
+    assert ctx.kernel_path.startswith("large-order")
+    worst = _check_case(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq, cfg.alpha_kind,
+                        cfg.alpha_lo, cfg.alpha_hi, n_elem=2, seed=5, threads=16)
+    assert worst < 1e-12
