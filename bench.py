@@ -270,7 +270,10 @@ def run_b200(args, cfg):
     # dominant kernel: the fused fill kernel (alpha read + M write) when the
     # shape has one, else the contraction kernel (I read + M write)
     fused = stages["n_moments"] == 0 and stages["n_contract"] > 0
-    kname = "fill_fused_kernel" if fused else "contract_v2_kernel"
+    path = ctx.kernel_path
+    kname = ("fill_fused_kernel" if fused else
+             "large_vw_kernel + large_u_kernel" if path.startswith("large") else
+             "contract_v2_kernel" if "contract_v2" in path else "contract_kernel")
     alg_bytes_elem = (counts["bytes_alpha"] + counts["bytes_M"]) if fused else counts["bytes_con"]
     n_con = max(1, stages["n_contract"])
     con_ms_avg = stages["ms_contract"] / n_con
