@@ -214,7 +214,9 @@ __device__ __forceinline__ void large_vw_term(const LVWParams<Ls>& p, int64_t un
   __syncthreads();
   // stage A: Y[tri(n1,n2)][k3], thread = (n1, k3), outputs n2 >= n1 (runtime n1,
   // compile-time n2 via dispatch on n1)
-  for_items<NV * KW, NT>([&](int r) {
+  // runtime loops here (coefficients come from smem, nothing to hoist); unrolled
+  // rounds would multiply the 136-output dispatch code and thrash the I-cache
+  for (int r = threadIdx.x; r < NV * KW; r += NT) {
     const int n1 = r / KW, k3 = r - (r / KW) * KW;
     double x[KV];
 #pragma unroll
@@ -235,11 +237,11 @@ __device__ __forceinline__ void large_vw_term(const LVWParams<Ls>& p, int64_t un
         });
       }
     });
-  });
+  }
   __syncthreads();
   // stage B: X[qv][tri(p1,p2)], thread = (qv, p1)
   double* Xo = p.X + unit * Ls::XPU + Ls::xoff(s) + static_cast<int64_t>(k1) * NQV * NQW;
-  for_items<NQV * NW, NT>([&](int r) {
+  for (int r = threadIdx.x; r < NQV * NW; r += NT) {
     const int p1 = r / NQV, qv = r - (r / NQV) * NQV;   // p1 warp-uniform (dispatch below)
     double y[KW];
 #pragma unroll
@@ -261,7 +263,7 @@ __device__ __forceinline__ void large_vw_term(const LVWParams<Ls>& p, int64_t un
         });
       }
     });
-  });
+  }
 }
 
 template <class Ls>
