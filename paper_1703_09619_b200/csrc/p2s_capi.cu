@@ -488,8 +488,12 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<4, 4, 4, 8, 8, 8, 256, kPPP>>(),                              // C1
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>,
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),                     // C2
-      make_fused<Shape<6, 6, 6, 1, 6, 6, 224, 2, 4, 1, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 224, kPPP, kDDD>>(),
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 160, 2, 4, 3, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 160, kPPP, kDDD>>(),
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 128, 2, 4, 4, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 128, kPPP, kDDD>>(),
+      make_fused<Shape<6, 6, 6, 3, 6, 6, 256, 1, 4, 3, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 6, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),                     // C3
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>,
