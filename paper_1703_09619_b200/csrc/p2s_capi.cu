@@ -488,12 +488,7 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<4, 4, 4, 8, 8, 8, 256, kPPP>>(),                              // C1
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>,
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),                     // C2
-      make_fused<Shape<6, 6, 6, 2, 6, 6, 160, 2, 4, 3, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 160, kPPP, kDDD>>(),
-      make_fused<Shape<6, 6, 6, 2, 6, 6, 128, 2, 4, 4, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 128, kPPP, kDDD>>(),
-      make_fused<Shape<6, 6, 6, 3, 6, 6, 256, 1, 4, 3, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 6, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),                     // C3
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>,
@@ -504,8 +499,14 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<8, 8, 8, 20, 20, 20, 512, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),                    // C4
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 4, 1, kPPP, kDDD>,
+      make_fused<Shape<10, 6, 4, 3, 4, 4, 288, 1, 6, 1, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 1, 6, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 96, 2, 6, 2, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 96, kPPP, kDDD>>(),
+      make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 6, 2, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
       make_fused<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>,
                  MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),                         // tests
       make_fused<Shape<4, 3, 3, 3, 3, 3, 96, 4, 0, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>,
