@@ -184,8 +184,12 @@ def run_b200(args, cfg):
     if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    E = args.n_elem or cfg.n_elem
     ctx = capi.Context(**cfg.problem(), device=local)
+    # C4 / C5 totals (1.1 TB / 4.4 TB of matrices) exceed HBM: a step fills the
+    # largest batch whose alpha + M fit in half of the GPU's memory
+    per_elem = 8 * (ctx.alpha_per_elem + ctx.n_tot * ctx.n_tot)
+    fit = max(1, int(0.5 * torch.cuda.get_device_properties(local).total_memory // per_elem))
+    E = args.n_elem or min(cfg.n_elem, fit)
     st = torch.cuda.current_stream()
     sp = st.cuda_stream
     n_tot = ctx.n_tot
