@@ -194,6 +194,7 @@ struct V2Args {
   int64_t ldM, n_tot, n_elem, mom_per_elem;
   int nc, P, Nt;
   const std::vector<double>* dense[kMaxTerms][3];  // [N][N][K] per term, direction
+  const double* amma;                              // device stage-C A (MMA shapes)
 };
 
 using v2_fn = cudaError_t (*)(const V2Args&, const std::vector<double>&, cudaStream_t, int);
@@ -219,6 +220,31 @@ std::vector<double> pack_v2(const V2Args& a) {
   return out;
 }
 
+// fragment-ordered stage-C A of an MMA shape (empty otherwise)
+template <class Sh>
+std::vector<double> pack_mma(const V2Args& a) {
+  if constexpr (Sh::MMA) {
+    const std::vector<double>* d[kMaxTerms];
+    for (int s = 0; s < Sh::S; ++s) d[s] = a.dense[s][0];
+    return build_mma_a<Sh>(d);
+  } else {
+    return {};
+  }
+}
+
+int vec2_ok(const double* M, int64_t ldM) {
+  return (ldM % 2 == 0 && reinterpret_cast<uintptr_t>(M) % 16 == 0) ? 1 : 0;
+}
+
+template <class Sh>
+constexpr const char* stage_c_desc() {
+  return Sh::MMA     ? "stage C on DMMA"
+         : Sh::PSPLIT ? (Sh::PAIR ? "banded stage C, parity split, paired 16-B stores"
+                                  : "banded stage C, parity split")
+         : Sh::PAIR   ? "banded stage C, paired 16-B stores"
+                      : "banded stage C";
+}
+
 template <class Sh>
 cudaError_t launch_v2(const V2Args& a, const std::vector<double>& packed, cudaStream_t st,
                       int num_sms) {
@@ -232,6 +258,8 @@ cudaError_t launch_v2(const V2Args& a, const std::vector<double>& packed, cudaSt
   p.P = a.P;
   p.Nt = a.Nt;
   p.mom_per_elem = a.mom_per_elem;
+  p.amma = a.amma;
+  p.vec2 = vec2_ok(a.M, a.ldM);
   std::memcpy(p.cu, packed.data(), sizeof(double) * Sh::ctot(0));
   std::memcpy(p.cv, packed.data() + Sh::ctot(0), sizeof(double) * Sh::ctot(1));
   std::memcpy(p.cw, packed.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));
@@ -239,11 +267,12 @@ cudaError_t launch_v2(const V2Args& a, const std::vector<double>& packed, cudaSt
   static int blocks_per_sm = -1;  // per instantiation (kernel attributes are process-wide)
   if (blocks_per_sm < 0) {
     cudaError_t e = cudaFuncSetAttribute(contract_v2_kernel<Sh>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)v2_smem<Sh>());
     if (e != cudaSuccess) return e;
     int b = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, contract_v2_kernel<Sh>, Sh::THREADS,
-                                                      Sh::SMEM);
+                                                      v2_smem<Sh>());
     if (e != cudaSuccess) return e;
     if (b < 1) return cudaErrorInvalidConfiguration;
     blocks_per_sm = b;
@@ -251,7 +280,7 @@ cudaError_t launch_v2(const V2Args& a, const std::vector<double>& packed, cudaSt
   const int64_t grid = Sh::PERSIST
                            ? std::min<int64_t>(p.n_units, static_cast<int64_t>(blocks_per_sm) * num_sms)
                            : p.n_units;
-  contract_v2_kernel<Sh><<<static_cast<unsigned>(grid), Sh::THREADS, Sh::SMEM, st>>>(p);
+  contract_v2_kernel<Sh><<<static_cast<unsigned>(grid), Sh::THREADS, v2_smem<Sh>(), st>>>(p);
   return cudaGetLastError();
 }
 
@@ -261,7 +290,9 @@ struct V2Entry {
   int kinds[kMaxTerms][3];
   v2_fn launch;
   v2_pack_fn pack;
+  v2_pack_fn mma_pack;
   size_t smem;
+  const char* desc;
 };
 
 template <class Sh>
@@ -273,7 +304,9 @@ V2Entry make_v2() {
     for (int d = 0; d < 3; ++d) r.kinds[s][d] = Sh::kind(s, d);
   r.launch = &launch_v2<Sh>;
   r.pack = &pack_v2<Sh>;
-  r.smem = Sh::SMEM;
+  r.mma_pack = &pack_mma<Sh>;
+  r.smem = v2_smem<Sh>();
+  r.desc = stage_c_desc<Sh>();
   return r;
 }
 
@@ -300,6 +333,10 @@ const std::vector<V2Entry>& v2_registry() {
       make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>>(),            // test shapes
       make_v2<Shape<3, 3, 3, 1, 3, 3, 64, 4, 12, 2, kPPP, kDDD>>(),
       make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 2, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+      make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 18, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 20, 1, kPPP, kDDD>>(),
+      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 64, 2, kPPP, kDDD>>(),
+      make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 66, 2, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
   };
   return reg;
 }
@@ -416,12 +453,13 @@ const MV2Entry* find_mv2(const p2s_problem& pb) {
 
 using fused_fn = cudaError_t (*)(const double*, double*, int64_t, int64_t, int64_t, int, int, int,
                                  const std::vector<double>&, const std::vector<double>&,
-                                 cudaStream_t, int);
+                                 const double*, cudaStream_t, int);
 
 template <class Sh, class Ms>
 cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_tot, int64_t n_elem,
                          int nc, int P, int Nt, const std::vector<double>& cpack,
-                         const std::vector<double>& mpack, cudaStream_t st, int num_sms) {
+                         const std::vector<double>& mpack, const double* amma, cudaStream_t st,
+                         int num_sms) {
   FusedParams<Sh, Ms> p;
   p.c.I = nullptr;
   p.c.M = M;
@@ -432,6 +470,8 @@ cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_
   p.c.P = P;
   p.c.Nt = Nt;
   p.c.mom_per_elem = 0;
+  p.c.amma = amma;
+  p.c.vec2 = vec2_ok(M, ldM);
   std::memcpy(p.c.cu, cpack.data(), sizeof(double) * Sh::ctot(0));
   std::memcpy(p.c.cv, cpack.data() + Sh::ctot(0), sizeof(double) * Sh::ctot(1));
   std::memcpy(p.c.cw, cpack.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));
@@ -464,6 +504,8 @@ struct FusedEntry {
   fused_fn launch;
   v2_pack_fn cpack;
   mv2_pack_fn mpack;
+  v2_pack_fn mma_pack;
+  const char* desc;
 };
 
 template <class Sh, class Ms>
@@ -479,36 +521,50 @@ FusedEntry make_fused() {
   r.launch = &launch_fused<Sh, Ms>;
   r.cpack = &pack_v2<Sh>;
   r.mpack = &pack_mv2<Ms>;
+  r.mma_pack = &pack_mma<Sh>;
+  r.desc = stage_c_desc<Sh>();
   return r;
 }
 
+// <Shape: N_u, N_v, N_w, n1 tile, p1 tile, p1 group, threads, min CTAs/SM, flags, FPT, kinds>
+// flags: 1 AALL, 2 ROWLOOP, 4 SYM, 8 PERSIST, 16 MMA (stage C on DMMA), 32 PAIR (16-B
+// stores), 64 PSPLIT (parity-split stage C).  The first match of a problem is the
+// default; P2S_FUSED_VARIANT=k selects the k-th (tuning / A-B measurements, see
+// profiles/README.md for the numbers behind each default).
 const std::vector<FusedEntry>& fused_registry() {
   static const std::vector<FusedEntry> reg = {
       make_fused<Shape<4, 4, 4, 4, 4, 4, 256, 2, 4, 1, kPPP>,
                  MShape<4, 4, 4, 8, 8, 8, 256, kPPP>>(),                              // C1
+      // C2: 0 banded (default), 1 paired stores, 2 parity split, 3 DMMA
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),                     // C2
-
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 36, 2, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 68, 2, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 20, 1, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+      // C3: 0 paired stores (default), 1 banded, 2 parity split + paired, 3 DMMA
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 38, 2, kPPP, kDDD>,
+                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 6, 2, kPPP, kDDD>,
-                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),                     // C3
-      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
-      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 6, 1, kPPP, kDDD>,
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 102, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
-      make_fused<Shape<8, 8, 8, 1, 8, 8, 512, 1, 6, 1, kPPP, kDDD>,
-                 MShape<8, 8, 8, 20, 20, 20, 512, kPPP, kDDD>>(),
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
-                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),                    // C4
-      make_fused<Shape<10, 6, 4, 3, 4, 4, 288, 1, 6, 1, kPPP, kDDD>,
-                 MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 1, 6, 1, kPPP, kDDD>,
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 22, 1, kPPP, kDDD>,
+                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
+      // C4: 0 parity split (default), 1 banded, 2 paired stores, 3 DMMA
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 70, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 96, 2, 6, 2, kPPP, kDDD>,
-                 MShape<10, 6, 4, 16, 16, 16, 96, kPPP, kDDD>>(),
-      make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 6, 2, kPPP, kDDD>,
-                 MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 38, 2, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 22, 1, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
+      // test shapes
       make_fused<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>,
-                 MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),                         // tests
+                 MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),
       make_fused<Shape<4, 3, 3, 3, 3, 3, 96, 4, 0, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>,
                  MShape<4, 3, 3, 9, 5, 7, 96, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
   };
@@ -745,6 +801,8 @@ struct p2s_ctx {
   int64_t xchunk = 1;
   const FusedEntry* fused = nullptr;
   std::vector<double> fused_cpack, fused_mpack;
+  double* d_amma_fused = nullptr;  // stage-C tensor-core A (MMA shapes)
+  double* d_amma_v2 = nullptr;
   std::vector<double> mv2_packed;
   std::vector<double> v2_packed;
   int num_sms = 148;
@@ -908,6 +966,7 @@ p2s_status run_contract(p2s_ctx* c, const double* I, double* M, int64_t ldM, int
     v.nc = c->pb.n_comp;
     v.P = c->sz.n_pairs;
     v.Nt = a.Nt;
+    v.amma = c->d_amma_v2;
     err = c->v2->launch(v, c->v2_packed, st, c->num_sms);
   } else {
     err = c->entry->launch(a, c->plan, st);
@@ -932,7 +991,8 @@ p2s_status run_fill(p2s_ctx* c, const double* alpha, double* M, int64_t ldM, int
     }
     cudaError_t err = c->fused->launch(alpha, M, ldM, c->sz.n_tot, n, c->pb.n_comp, c->sz.n_pairs,
                                        c->pb.order[0] * c->pb.order[1] * c->pb.order[2],
-                                       c->fused_cpack, c->fused_mpack, st, c->num_sms);
+                                       c->fused_cpack, c->fused_mpack, c->d_amma_fused, st,
+                                       c->num_sms);
     if (err != cudaSuccess) return cuda_fail(err, "fill_fused_kernel launch");
     if (c->prof) {
       cudaEventRecord(e1, st);
@@ -972,10 +1032,17 @@ const char* p2s_version(void) { return "p2s_b200 0.1 (sm_100a)"; }
 const char* p2s_kernel_path(const p2s_ctx* c) {
   if (!c) return "";
   if (c->large) return "large-order: large_moments_kernel + large_vw_kernel + large_u_kernel";
-  if (c->fused) return "fused: fill_fused_kernel (moments + contraction, one persistent kernel)";
-  if (c->v2 && !c->force_generic)
-    return c->mv2 ? "two-stage: moments_v2_kernel + contract_v2_kernel"
-                  : "two-stage: moments_kernel + contract_v2_kernel";
+  static thread_local std::string path;
+  if (c->fused) {
+    path = std::string("fused: fill_fused_kernel (moments + contraction; ") + c->fused->desc + ")";
+    return path.c_str();
+  }
+  if (c->v2 && !c->force_generic) {
+    path = std::string(c->mv2 ? "two-stage: moments_v2_kernel + contract_v2_kernel ("
+                              : "two-stage: moments_kernel + contract_v2_kernel (") +
+           c->v2->desc + ")";
+    return path.c_str();
+  }
   return c->mv2 && !c->force_generic ? "two-stage: moments_v2_kernel + contract_kernel"
                                      : "two-stage: moments_kernel + contract_kernel (generic)";
 }
@@ -1070,6 +1137,11 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
       for (int d = 0; d < 3; ++d) v.dense[s][d] = &c->coef[s][d];
     c->fused_cpack = c->fused->cpack(v);
     c->fused_mpack = c->fused->mpack(c->phi);
+    const std::vector<double> A = c->fused->mma_pack(v);
+    if (!A.empty()) {
+      P2S_CUDA(cudaMalloc(&c->d_amma_fused, sizeof(double) * A.size()));
+      P2S_CUDA(cudaMemcpy(c->d_amma_fused, A.data(), sizeof(double) * A.size(), cudaMemcpyHostToDevice));
+    }
   }
   c->mv2 = find_mv2(*spec);
   if (c->mv2) c->mv2_packed = c->mv2->pack(c->phi);
@@ -1078,6 +1150,11 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
     for (int s = 0; s < S; ++s)
       for (int d = 0; d < 3; ++d) v.dense[s][d] = &c->coef[s][d];
     c->v2_packed = v2e->pack(v);
+    const std::vector<double> A = v2e->mma_pack(v);
+    if (!A.empty()) {
+      P2S_CUDA(cudaMalloc(&c->d_amma_v2, sizeof(double) * A.size()));
+      P2S_CUDA(cudaMemcpy(c->d_amma_v2, A.data(), sizeof(double) * A.size(), cudaMemcpyHostToDevice));
+    }
   }
 
   // moment-kernel shared memory
@@ -1150,6 +1227,8 @@ void p2s_destroy(p2s_ctx* c) {
   if (c->d_scratch) cudaFree(c->d_scratch);
   if (c->d_X) cudaFree(c->d_X);
   if (c->lpack.d_cvw) cudaFree(c->lpack.d_cvw);
+  if (c->d_amma_fused) cudaFree(c->d_amma_fused);
+  if (c->d_amma_v2) cudaFree(c->d_amma_v2);
   for (int i = 0; i < 2; ++i) {
     if (c->d_ring_alpha[i]) cudaFree(c->d_ring_alpha[i]);
     if (c->d_ring_M[i]) cudaFree(c->d_ring_M[i]);

@@ -22,6 +22,7 @@
 #pragma once
 
 #include "p2s_kernels.cuh"
+#include "p2s_mma.cuh"
 
 namespace p2s {
 
@@ -42,6 +43,17 @@ struct Shape {
   // unit's moments); otherwise one CTA per unit (no outer loop, so ptxas cannot
   // hoist the per-unit constant-bank loads into registers across units).
   static constexpr int PERSIST = (FLAGS_ >> 3) & 1;
+  // MMA (bit 4): stage C as FP64 tensor-core GEMMs (p2s_mma.cuh) instead of
+  // the banded register form; FPT is unused then.
+  static constexpr int MMA = (FLAGS_ >> 4) & 1;
+  // PAIR (bit 5): a thread's stage-C fibers come in adjacent pairs (f, f+1) of
+  // one matrix row, written with one 16-B store (half the store instructions)
+  static constexpr int PAIR = (FLAGS_ >> 5) & 1;
+  static_assert(!PAIR || (FPT_ % 2 == 0 && (NV_ * NW_) % 2 == 0), "PAIR needs even FPT and rows");
+  // PSPLIT (bit 6): stage C runs the (m1, m2) classes of even and odd m1+m2
+  // one after the other; a class reads only the k1 of one parity, so the
+  // register-resident fiber halves
+  static constexpr int PSPLIT = (FLAGS_ >> 6) & 1;
   static constexpr int AALL = (FLAGS_ & 1) | SYM, ROWLOOP = (FLAGS_ >> 1) & 1;
   static constexpr int NQV = NV_ * (NV_ + 1) / 2, NQW = NW_ * (NW_ + 1) / 2;
   static constexpr int tri(int a, int b, int n) { return a * n - a * (a - 1) / 2 + (b - a); }
@@ -66,6 +78,16 @@ struct Shape {
     for (int s = 0; s < S; ++s) o += K(s, 0);
     return o;
   }
+  // u-kernels of term s in parity class par (k1 = k0 + 2 idx, k0 = (par + shift) % 2)
+  static constexpr int ushift(int s) { return (kind(s, 0) == DP || kind(s, 0) == PD) ? 1 : 0; }
+  static constexpr int uk0(int s, int par) { return (par + ushift(s)) % 2; }
+  static constexpr int ucnt(int s, int par) { return (K(s, 0) - uk0(s, par) + 1) / 2; }
+  static constexpr int kpo(int s, int par) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) o += ucnt(i, par);
+    return o;
+  }
+  static constexpr int KTOT_PAR(int par) { return par < 0 ? KTOT_U() : kpo(S, par); }
   static constexpr int kuoff(int s) {
     int o = 0;
     for (int i = 0; i < s; ++i) o += K(i, 0);
@@ -130,6 +152,20 @@ struct Shape {
   static constexpr size_t SMEM = sizeof(double) * (size_t)(MPP + A_DBL + B_DBL) + 16;
 };
 
+// stage-C tensor-core operands in shared memory (MMA shapes)
+struct MmaSmem {
+  const double* A;
+  const int2* ctab;
+};
+
+template <class Sh>
+__device__ __forceinline__ MmaSmem mma_carve(double* base) {
+  if constexpr (Sh::MMA)
+    return MmaSmem{base, reinterpret_cast<const int2*>(base + MmaMap<Sh>::ATOT)};
+  else
+    return MmaSmem{nullptr, nullptr};
+}
+
 template <class Sh>
 struct V2Params {
   const double* I;
@@ -138,6 +174,8 @@ struct V2Params {
   int64_t n_units;
   int nc, P, Nt;
   int64_t mom_per_elem;
+  const double* amma;  // fragment-ordered stage-C A (MMA shapes), else null
+  int vec2;            // M rows 16-B aligned (even ldM, aligned base): paired stores
   double cu[Sh::ctot(0)];
   double cv[Sh::ctot(1)];
   double cw[Sh::ctot(2)];
@@ -309,9 +347,9 @@ __device__ __forceinline__ void v2_stage_b_sym(const V2Params<Sh>& p, const doub
   });
 }
 
-template <class Sh>
+template <class Sh, int PAR = -1>
 __device__ __forceinline__ void v2_load_fiber(const double* Bbuf, int i, int p1l, int r,
-                                              double (&b)[Sh::KTOT_U()]) {
+                                              double (&b)[Sh::KTOT_PAR(PAR)]) {
   constexpr int NV = Sh::NV, NW = Sh::NW;
   int off;
   if constexpr (Sh::SYM) {
@@ -325,8 +363,14 @@ __device__ __forceinline__ void v2_load_fiber(const double* Bbuf, int i, int p1l
     constexpr int s = decltype(sc)::value;
     constexpr int Ku = Sh::K(s, 0);
     const double* src = Bbuf + Sh::boff(s) + (i * Ku) * Sh::BSTR + off;
+    if constexpr (PAR < 0) {
 #pragma unroll
-    for (int k1 = 0; k1 < Ku; ++k1) b[Sh::kuoff(s) + k1] = src[k1 * Sh::BSTR];
+      for (int k1 = 0; k1 < Ku; ++k1) b[Sh::kuoff(s) + k1] = src[k1 * Sh::BSTR];
+    } else {
+      constexpr int k0 = Sh::uk0(s, PAR);
+#pragma unroll
+      for (int j = 0; j < Sh::ucnt(s, PAR); ++j) b[Sh::kpo(s, PAR) + j] = src[(k0 + 2 * j) * Sh::BSTR];
+    }
   });
 }
 
@@ -335,7 +379,8 @@ __device__ __forceinline__ void v2_load_fiber(const double* Bbuf, int i, int p1l
 // barrier), e.g. to start the next unit's bulk copy into Ibuf.
 template <class Sh, class AfterA>
 __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibuf, double* Abuf,
-                                        double* Bbuf, double* Mbase, AfterA&& after_a) {
+                                        double* Bbuf, double* Mbase, AfterA&& after_a,
+                                        MmaSmem mm = MmaSmem{nullptr, nullptr}) {
   constexpr int S = Sh::S, NU = Sh::NU, NV = Sh::NV, NW = Sh::NW, T = Sh::T, FPT = Sh::FPT;
   const int tid = threadIdx.x;
   if constexpr (Sh::SYM) {
@@ -364,28 +409,55 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
       __syncthreads();
       // ---- stage C
       constexpr int NF = T * Sh::P1T * NV * NW;  // fibers of the sub-tile
-      constexpr int NFT = (NF + FPT - 1) / FPT;
+      // thread items: FPT single fibers, or FPT/2 adjacent pairs (PAIR)
+      constexpr int NFT = Sh::PAIR ? (NF / 2 + FPT / 2 - 1) / (FPT / 2) : (NF + FPT - 1) / FPT;
       const int64_t rowstep = static_cast<int64_t>(NV * NW) * p.ldM;
+      if constexpr (Sh::MMA) {
+        stage_c_mma<Sh>(
+            mm.A, mm.ctab, Bbuf, rowstep, p.vec2,
+            [&](int f) {
+              const int r = f % (NV * NW);
+              const int p1l = (f / (NV * NW)) % Sh::P1T;
+              if constexpr (Sh::SYM) {
+                const int n2 = r / NW, p2 = r - n2 * NW;
+                const int a = p1l < p2 ? p1l : p2, c = p1l < p2 ? p2 : p1l;
+                return n2 * Sh::NQW + Sh::tri(a, c, NW);
+              } else {
+                return p1l * NV * NW + r;
+              }
+            },
+            [&](int f) {
+              const int r = f % (NV * NW);
+              const int ip = f / (NV * NW);
+              const int p1l = ip % Sh::P1T, i = ip / Sh::P1T;
+              const int n1 = t * T + i, p1 = pt * Sh::P1T + p1l;
+              return Mbase + static_cast<int64_t>(n1 * NW + p1) * p.ldM + r;
+            });
+      } else {
+      auto stage_c = [&](auto parc) {
+      constexpr int PAR = decltype(parc)::value;  // -1: all (m1, m2) at once
       for_items<NFT, Sh::THREADS>([&](int f0) {
-        double b[FPT][Sh::KTOT_U()];
+        double b[FPT][Sh::KTOT_PAR(PAR)];
         double* out[FPT];
         bool live[FPT];
 #pragma unroll
         for (int q = 0; q < FPT; ++q) {
-          const int f = f0 + q * NFT;  // f = ((i*P1T + p1l)*NV + n2)*NW + p2
+          // f = ((i*P1T + p1l)*NV + n2)*NW + p2
+          const int f = Sh::PAIR ? 2 * (f0 + (q / 2) * NFT) + (q % 2) : f0 + q * NFT;
           live[q] = f < NF;
           const int fs = live[q] ? f : 0;
           const int r = fs % (NV * NW);
           const int ip = fs / (NV * NW);
           const int p1l = ip % Sh::P1T, i = ip / Sh::P1T;
           const int n1 = t * T + i, p1 = pt * Sh::P1T + p1l;
-          v2_load_fiber<Sh>(Bbuf, i, p1l, r, b[q]);
+          v2_load_fiber<Sh, PAR>(Bbuf, i, p1l, r, b[q]);
           out[q] = Mbase + static_cast<int64_t>(n1 * NW + p1) * p.ldM + r;
         }
         auto row = [&](auto m1c) {
           constexpr int m1 = decltype(m1c)::value;
           static_for<0, NU>([&](auto m2c) {
             constexpr int m2 = decltype(m2c)::value;
+            if constexpr (PAR < 0 || (m1 + m2) % 2 == PAR) {
             double v[FPT];
 #pragma unroll
             for (int q = 0; q < FPT; ++q) v[q] = 0.0;
@@ -398,13 +470,29 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
               static_for<0, cnt>([&](auto jc) {
                 constexpr int j = decltype(jc)::value;
                 const double c = p.cu[co + j];
+                constexpr int bi =
+                    PAR < 0 ? ko + lo + 2 * j : Sh::kpo(s, PAR) + (lo - Sh::uk0(s, PAR)) / 2 + j;
 #pragma unroll
-                for (int q = 0; q < FPT; ++q) v[q] = fma(c, b[q][ko + lo + 2 * j], v[q]);
+                for (int q = 0; q < FPT; ++q) v[q] = fma(c, b[q][bi], v[q]);
               });
             });
+            if constexpr (Sh::PAIR) {
 #pragma unroll
-            for (int q = 0; q < FPT; ++q)
-              if (live[q]) st_cs(out[q] + m1 * rowstep + m2 * (NV * NW), v[q]);
+              for (int q = 0; q < FPT; q += 2) {
+                double* d = out[q] + m1 * rowstep + m2 * (NV * NW);
+                if (p.vec2) {
+                  if (live[q]) st_cs2(d, v[q], v[q + 1]);
+                } else {
+                  if (live[q]) st_cs(d, v[q]);
+                  if (live[q + 1]) st_cs(d + 1, v[q + 1]);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < FPT; ++q)
+                if (live[q]) st_cs(out[q] + m1 * rowstep + m2 * (NV * NW), v[q]);
+            }
+            }  // parity class
           });
         };
         if constexpr (Sh::ROWLOOP) {
@@ -417,9 +505,22 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
           static_for<0, NU>([&](auto m1c) { row(m1c); });
         }
       });
+      };
+      if constexpr (Sh::PSPLIT) {
+        stage_c(std::integral_constant<int, 0>{});
+        stage_c(std::integral_constant<int, 1>{});
+      } else {
+        stage_c(std::integral_constant<int, -1>{});
+      }
+      }  // banded stage C
       __syncthreads();
     }  // p1 sub-tiles
   }
+}
+
+template <class Sh>
+constexpr size_t v2_smem() {
+  return Sh::SMEM + sizeof(double) * static_cast<size_t>(mma_smem_dbl<Sh>());
 }
 
 template <class Sh>
@@ -432,6 +533,9 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
   uint64_t* bar = reinterpret_cast<uint64_t*>(Bbuf + Sh::B_DBL);
   const int tid = threadIdx.x;
   constexpr uint32_t kIBytes = Sh::MPP * 8u;
+  const MmaSmem mm = mma_carve<Sh>(Bbuf + Sh::B_DBL + 2);
+  if constexpr (Sh::MMA)
+    mma_setup<Sh>(p.amma, const_cast<double*>(mm.A), const_cast<int2*>(mm.ctab));
 
   int64_t unit = blockIdx.x;
   if (tid == 0) {
@@ -453,7 +557,7 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     mbar_wait_parity(bar, phase);
     phase ^= 1u;
     double* Mbase = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt) * p.ldM + gcj * p.Nt;
-    v2_unit<Sh>(p, Ibuf, Abuf, Bbuf, Mbase, next_copy);
+    v2_unit<Sh>(p, Ibuf, Abuf, Bbuf, Mbase, next_copy, mm);
   };
   if constexpr (Sh::PERSIST) {
     for (; unit < p.n_units; unit += gridDim.x)

@@ -84,5 +84,9 @@ __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
 // Streaming (evict-first) 8-byte store: element matrices are written once and
 // never re-read by the fill.
 __device__ __forceinline__ void st_cs(double* p, double v) { __stcs(p, v); }
+// 16-B streaming store of two adjacent doubles (p 16-B aligned)
+__device__ __forceinline__ void st_cs2(double* p, double a, double b) {
+  __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
+}
 
 }  // namespace p2s

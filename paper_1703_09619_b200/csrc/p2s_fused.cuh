@@ -25,7 +25,7 @@ struct FusedLayout {
   static constexpr int AB = Sh::A_DBL + Sh::B_DBL;
   static constexpr int MS = Ms::scratch_all_dbl();
   static constexpr int WORK = AB > MS ? AB : MS;
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(Sh::MPP + WORK);
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(Sh::MPP + WORK + mma_smem_dbl<Sh>());
 };
 
 template <class Sh, class Ms>
@@ -35,6 +35,9 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
   double* Ibuf = sm;
   double* Abuf = Ibuf + Sh::MPP;
   double* Bbuf = Abuf + Sh::A_DBL;
+  const MmaSmem mm = mma_carve<Sh>(Abuf + FusedLayout<Sh, Ms>::WORK);
+  if constexpr (Sh::MMA)  // visible to stage C after the moment phase's barriers
+    mma_setup<Sh>(p.c.amma, const_cast<double*>(mm.A), const_cast<int2*>(mm.ctab));
   constexpr int slab = Ms::Q(0) * Ms::Q(1) * Ms::Q(2);
   auto do_unit = [&](int64_t unit, int64_t stride) {
     const int64_t e = unit / p.c.P;
@@ -51,7 +54,7 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
       moments_all_terms<Ms, Sh::THREADS>(a, p.tab, Abuf, Ibuf);
     double* Mbase =
         p.c.M + e * p.c.mat_stride + static_cast<int64_t>(gci * p.c.Nt) * p.c.ldM + gcj * p.c.Nt;
-    v2_unit<Sh>(p.c, Ibuf, Abuf, Bbuf, Mbase, []() {});
+    v2_unit<Sh>(p.c, Ibuf, Abuf, Bbuf, Mbase, []() {}, mm);
   };
   if constexpr (Sh::PERSIST) {
     for (int64_t unit = blockIdx.x; unit < p.c.n_units; unit += gridDim.x) do_unit(unit, gridDim.x);

@@ -218,3 +218,64 @@ def test_c5_matches_oracle():
     worst = _check_case(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq, cfg.alpha_kind,
                         cfg.alpha_lo, cfg.alpha_hi, n_elem=2, seed=5, threads=16)
     assert worst < 1e-12
+
+
+def _select_variant(monkeypatch, problem, env_var, marker):
+    """Set env_var (P2S_FUSED_VARIANT / P2S_V2_VARIANT) to the first registered
+    variant of `problem` whose kernel_path contains `marker`."""
+    for v in range(24):
+        monkeypatch.setenv(env_var, str(v))
+        ctx = capi.Context(*problem)
+        if marker in ctx.kernel_path:
+            return ctx
+    pytest.fail(f"no variant with {marker!r} registered for {problem}")
+
+
+# (config or small case, two-stage?, stage-C variant marker, elements)
+VARIANT_CASES = [
+    ("c2", False, "DMMA", 6),
+    ("c3", False, "DMMA", 3),
+    ("c4", False, "DMMA", 3),
+    ("c2", False, "paired", 6),
+    ("c3", False, "paired", 3),
+    ("c4", False, "paired", 3),
+    ("c2", False, "parity split", 6),
+    ("c3", False, "parity split, paired", 3),
+    ("c4", False, "parity split", 3),
+    ((3, (3, 3, 3), [PP, DD], (6, 6, 6)), True, "parity split", 4),
+    ((1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7)), True, "parity split", 4),
+    ((3, (3, 3, 3), [PP, DD], (6, 6, 6)), True, "DMMA", 4),
+    ((1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7)), True, "DMMA", 4),
+]
+
+
+@pytest.mark.parametrize("case,two_stage,marker,n_elem", VARIANT_CASES,
+                         ids=lambda c: str(c)[:24])
+@pytest.mark.parametrize("odd_ld", [False, True])
+def test_stage_c_variants_match_oracle(case, two_stage, marker, n_elem, odd_ld, monkeypatch):
+    """Stage-C variants: on the FP64 tensor cores (DMMA, p2s_mma.cuh) and with
+    paired 16-B stores -- same bar; even ldM takes the 16-B store path, odd
+    ldM the scalar one."""
+    if isinstance(case, str):
+        cfg = CONFIGS[case]
+        n_comp, order, kinds, nq = cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq
+        ak, lo, hi = cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi
+    else:
+        n_comp, order, kinds, nq = case
+        ak, lo, hi = O.ALPHA_SINE, 0.5, 3.0
+    if two_stage:
+        monkeypatch.setenv("P2S_NO_FUSED", "1")
+    ctx = _select_variant(monkeypatch, (n_comp, order, kinds, nq),
+                          "P2S_V2_VARIANT" if two_stage else "P2S_FUSED_VARIANT", marker)
+    o = oracle_for(n_comp, order, kinds, nq)
+    alpha = o.alpha(ak, lo, hi, 77, 0, n_elem)
+    ld = ctx.n_tot + (1 if odd_ld else 0)
+    Mg = _gpu_fill(ctx, alpha, ld=ld)
+    Mo = o.fill(alpha, threads=8)
+    assert np.isfinite(Mg[:, :, :ctx.n_tot]).all()
+    if odd_ld:
+        assert np.isnan(Mg[:, :, ctx.n_tot:]).all()  # padding column untouched
+    Nt = order[0] * order[1] * order[2]
+    for e in range(n_elem):
+        ok, msg, _ = blocks_close(Mg[e, :, :ctx.n_tot], Mo[e], n_comp, Nt)
+        assert ok, f"element {e}: {msg}"
