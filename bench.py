@@ -48,6 +48,8 @@ def parse():
                     help="seconds of CPU work per CPU-baseline sample / reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ablation", action="store_true",
+                    help="skip the direct-quadrature ablation (p2s_direct_fill, rank 0)")
     ap.add_argument("--seed", type=int, default=20170328)
     return ap.parse_args()
 
@@ -262,6 +264,32 @@ def run_b200(args, cfg):
             dist.destroy_process_group()
         return
 
+    # ---- ablation: the direct-quadrature fill the paper's scheme replaces
+    # (p2s_direct_fill: one FP64 DGEMM per element, pair and term on the tensor
+    # cores), same alpha, outside the timed region
+    ablation = None
+    if not args.no_ablation:
+        dctx = capi.DirectContext(**cfg.problem(), device=local)
+        fma_elem = ctx.n_pairs * len(cfg.kinds) * (cfg.nq[0] * cfg.nq[1] * cfg.nq[2]) * \
+            (n_tot // cfg.n_comp) ** 2
+        NA = int(max(1, min(E, 2.25e12 // fma_elem)))
+        dctx.fill(alpha, M, n_tot, NA, sp)  # warm-up (cuBLAS heuristics)
+        torch.cuda.synchronize()
+        reps = 3
+        ev0.record(st)
+        for _ in range(reps):
+            dctx.fill(alpha, M, n_tot, NA, sp)
+        ev1.record(st)
+        torch.cuda.synchronize()
+        dms = ev0.elapsed_time(ev1) / reps
+        drate = NA / (dms / 1e3)
+        ablation = {"direct_elem_per_s": drate, "elements": NA, "ms_per_batch": dms,
+                    "direct_tflops": 2 * fma_elem * NA / (dms / 1e3) / 1e12,
+                    "p2s_over_direct": (value / world) / drate,
+                    "method": "p2s_direct_fill: W = diag(w alpha) B_trial, cuBLAS DGEMM "
+                              "B_test^T W per (element, pair, term), CUDA events"}
+        dctx.close()
+
     counts = algorithmic_counts(cfg)
     peaks = {}
     try:
@@ -329,6 +357,8 @@ def run_b200(args, cfg):
     }
     if e2e:
         line["e2e"] = e2e
+    if ablation:
+        line["ablation"] = ablation
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         rate, n, dt = cpu_baseline(cfg, args.cpu_seconds, args.seed, threads)

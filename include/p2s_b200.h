@@ -138,6 +138,20 @@ p2s_status p2s_set_profiling(p2s_ctx* ctx, int enable);
 p2s_status p2s_get_stage_times(p2s_ctx* ctx, double* ms_moments, double* ms_contract,
                                int64_t* n_moment_launches, int64_t* n_contract_launches);
 
+/* ---- Direct-quadrature fill (the ablation baseline the paper's scheme replaces) ----
+ * reference: assemble_direct_element (assembly.hpp:50; assembly.cpp:134-274) and
+ * fill_elements(.., Backend::direct, ..) (assembly.hpp:12-15, 82-83).  Same problem
+ * description, alpha and M layouts as p2s_fill; every entry is the full tensor
+ * Gauss-Legendre sum (per element, pair and term one dense FP64 GEMM on the tensor
+ * cores via cuBLAS).  The context holds the tensor basis tables (2 x n_terms x
+ * nq_u nq_v nq_w x N_u N_v N_w doubles) and ~1 GiB of scratch; p2s_direct_fill
+ * calls on one context must not overlap. */
+typedef struct p2s_direct_ctx p2s_direct_ctx;
+p2s_status p2s_direct_create(const p2s_problem* spec, int device, p2s_direct_ctx** out);
+void p2s_direct_destroy(p2s_direct_ctx* ctx);
+p2s_status p2s_direct_fill(p2s_direct_ctx* ctx, const double* d_alpha, double* d_M, int64_t ld_M,
+                           int64_t n_elem, void* stream);
+
 /* 1 if the orders / kinds have a compiled kernel instantiation. */
 int p2s_shape_supported(const p2s_problem* spec);
 

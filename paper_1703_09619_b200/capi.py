@@ -28,7 +28,8 @@ EXPORTS = ("p2s_create", "p2s_destroy", "p2s_get_sizes", "p2s_moments", "p2s_con
            "p2s_set_profiling", "p2s_get_stage_times", "p2s_shape_supported", "p2s_last_error",
            "p2s_version", "p2s_kernel_path", "p2s_moments_host", "p2s_contract_host",
            "p2s_cheb2d_create", "p2s_cheb2d_destroy", "p2s_cheb2d_get_sizes",
-           "p2s_cheb2d_kernel_tables", "p2s_cheb2d_assemble")
+           "p2s_cheb2d_kernel_tables", "p2s_cheb2d_assemble",
+           "p2s_direct_create", "p2s_direct_destroy", "p2s_direct_fill")
 
 
 class P2SError(RuntimeError):
@@ -126,9 +127,13 @@ def lib():
         L.p2s_cheb2d_get_sizes.argtypes = [vp, C.POINTER(Cheb2dSizes)]
         L.p2s_cheb2d_kernel_tables.argtypes = [vp, vp, vp, i64, vp]
         L.p2s_cheb2d_assemble.argtypes = [vp, vp, vp, i64, vp]
+        L.p2s_direct_create.argtypes = [C.POINTER(Problem), C.c_int, C.POINTER(vp)]
+        L.p2s_direct_destroy.argtypes = [vp]
+        L.p2s_direct_destroy.restype = None
+        L.p2s_direct_fill.argtypes = [vp, vp, vp, i64, i64, vp]
         for f in EXPORTS:
             if f not in ("p2s_destroy", "p2s_shape_supported", "p2s_last_error", "p2s_version",
-                         "p2s_kernel_path", "p2s_cheb2d_destroy"):
+                         "p2s_kernel_path", "p2s_cheb2d_destroy", "p2s_direct_destroy"):
                 getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -310,3 +315,29 @@ class Cheb2dContext:
         sz = self.sizes
         return {n: flat[sz.block_offset[i]:sz.block_offset[i] + sz.block_rows[i] * sz.block_cols[i]]
                 .reshape(sz.block_rows[i], sz.block_cols[i]) for i, n in enumerate(BLOCK_NAMES)}
+
+
+class DirectContext:
+    """Direct-quadrature fill (p2s_direct_*): the ablation baseline, reference
+    assemble_direct_element (assembly.hpp:50; assembly.cpp:134-274) in 3-D."""
+
+    def __init__(self, n_comp, order, kinds, nq, device: int = 0):
+        self.problem = make_problem(n_comp, order, kinds, nq)
+        self.n_tot = n_comp * order[0] * order[1] * order[2]
+        h = C.c_void_p()
+        _check(lib().p2s_direct_create(C.byref(self.problem), device, C.byref(h)))
+        self._h = h
+
+    def fill(self, d_alpha, d_M, ld_M: int, n_elem: int, stream=0):
+        _check(lib().p2s_direct_fill(self._h, _ptr(d_alpha), _ptr(d_M), ld_M, n_elem, _ptr(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().p2s_direct_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

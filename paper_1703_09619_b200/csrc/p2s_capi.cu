@@ -544,6 +544,11 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 20, 1, kPPP, kDDD>,
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+      // C2: 4 parity split + paired (FPT 2), 5 same FPT 4
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 100, 2, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 100, 4, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
       // C3: 0 paired stores (default), 1 banded, 2 parity split + paired, 3 DMMA
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 38, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
