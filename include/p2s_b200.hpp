@@ -135,6 +135,27 @@ class Context {
   Problem problem_;
 };
 
+// RAII owner of one p2s_direct_ctx: the direct-quadrature fill (reference
+// assemble_direct_element, assembly.hpp:50), device buffers, same layouts.
+class DirectContext {
+ public:
+  DirectContext(const Problem& pb, int device = 0) {
+    const p2s_problem c = pb.c();
+    check(p2s_direct_create(&c, device, &h_));
+  }
+  ~DirectContext() {
+    if (h_) p2s_direct_destroy(h_);
+  }
+  DirectContext(const DirectContext&) = delete;
+  DirectContext& operator=(const DirectContext&) = delete;
+  void fill(const double* d_alpha, double* d_M, int64_t ld, int64_t n, void* stream = nullptr) {
+    check(p2s_direct_fill(h_, d_alpha, d_M, ld, n, stream));
+  }
+
+ private:
+  p2s_direct_ctx* h_ = nullptr;
+};
+
 // Moment integrals of a batch of elements (reference: KernelTable, assembly.hpp:35-40).
 struct KernelTable {
   Problem problem;
