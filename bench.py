@@ -48,6 +48,8 @@ def parse():
                     help="seconds of CPU work per CPU-baseline sample / reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--basis", default="modal", choices=["modal", "conforming"],
+                    help="element basis (conforming = the reference's conforming change of basis)")
     ap.add_argument("--no-ablation", action="store_true",
                     help="skip the direct-quadrature ablation (p2s_direct_fill, rank 0)")
     ap.add_argument("--seed", type=int, default=20170328)
@@ -186,7 +188,8 @@ def run_b200(args, cfg):
     if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    ctx = capi.Context(**cfg.problem(), device=local)
+    basis = capi.BASIS_CONFORMING if args.basis == "conforming" else capi.BASIS_MODAL
+    ctx = capi.Context(**cfg.problem(), device=local, basis=basis)
     # C4 / C5 totals (1.1 TB / 4.4 TB of matrices) exceed HBM: a step fills the
     # largest batch whose alpha + M fit in half of the GPU's memory
     per_elem = 8 * (ctx.alpha_per_elem + ctx.n_tot * ctx.n_tot)
@@ -269,7 +272,7 @@ def run_b200(args, cfg):
     # cores), same alpha, outside the timed region
     ablation = None
     if not args.no_ablation:
-        dctx = capi.DirectContext(**cfg.problem(), device=local)
+        dctx = capi.DirectContext(**cfg.problem(), device=local, basis=basis)
         fma_elem = ctx.n_pairs * len(cfg.kinds) * (cfg.nq[0] * cfg.nq[1] * cfg.nq[2]) * \
             (n_tot // cfg.n_comp) ** 2
         NA = int(max(1, min(E, 2.25e12 // fma_elem)))
@@ -338,6 +341,7 @@ def run_b200(args, cfg):
                    "kinds": ["PP/DD/DP/PD"[3 * k:3 * k + 2] if isinstance(k, int) else str(k)
                              for k in cfg.kinds],
                    "n_terms": len(cfg.kinds), "nq": list(cfg.nq), "elements_per_rank": E,
+                   "basis": args.basis,
                    "n_tot": n_tot, "parallelism": f"element-partitioned x{world}, no collective",
                    "l2": f"outputs {E * n_tot * n_tot * 8 / 1e9:.1f} GB per step >> 126 MB L2"},
         "clocks": clk,

@@ -75,7 +75,16 @@ typedef struct {
   int32_t n_terms;                       /* N_s (1 .. P2S_MAX_TERMS)            */
   int32_t kind[P2S_MAX_TERMS][3];        /* P2S_PP / DD / DP / PD               */
   int32_t nq[3];                         /* Gauss-Legendre points per direction */
+  int32_t basis;                         /* P2S_BASIS_MODAL / P2S_BASIS_CONFORMING */
 } p2s_problem;
+
+/* Basis of the element matrices (both sides, every direction):
+ *   MODAL       P_0 .. P_{N-1}
+ *   CONFORMING  phi_0 = (P_0 - P_1)/2, phi_1 = (P_0 + P_1)/2, phi_n = P_n - P_{n mod 2}:
+ *               the reference's conforming change of basis (conforming_matrix /
+ *               apply_conforming_transform, assembly.cpp:476-574), folded into the
+ *               product-to-sum tables -- M_conf = T^T M_modal T at no extra cost. */
+enum { P2S_BASIS_MODAL = 0, P2S_BASIS_CONFORMING = 1 };
 
 typedef struct {
   int64_t alpha_per_elem;                /* doubles                              */

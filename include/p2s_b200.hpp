@@ -69,6 +69,7 @@ struct Problem {
   Orders orders;
   std::vector<Term> terms{Term{}};
   std::array<int, 3> nq{8, 8, 8};
+  bool conforming = false;  // conforming basis (reference apply_conforming_transform)
 
   p2s_problem c() const {
     p2s_problem p{};
@@ -83,10 +84,12 @@ struct Problem {
       p.kind[s][2] = static_cast<int>(terms[s].w);
     }
     for (int d = 0; d < 3; ++d) p.nq[d] = nq[d];
+    p.basis = conforming ? P2S_BASIS_CONFORMING : P2S_BASIS_MODAL;
     return p;
   }
   bool same_shape(const Problem& o) const {
-    if (n_comp != o.n_comp || !(orders == o.orders) || nq != o.nq || terms.size() != o.terms.size())
+    if (n_comp != o.n_comp || !(orders == o.orders) || nq != o.nq || terms.size() != o.terms.size() ||
+        conforming != o.conforming)
       return false;
     for (size_t s = 0; s < terms.size(); ++s)
       if (terms[s].u != o.terms[s].u || terms[s].v != o.terms[s].v || terms[s].w != o.terms[s].w)

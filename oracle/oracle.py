@@ -37,6 +37,7 @@ class Problem(C.Structure):
         ("n_terms", C.c_int),
         ("kind", (C.c_int * 3) * MAX_TERMS),
         ("nq", C.c_int * 3),
+        ("basis", C.c_int),
     ]
 
 
@@ -51,6 +52,8 @@ def lib():
         dp = C.POINTER(C.c_double)
         ip = C.POINTER(C.c_int)
         L.por_gauss_legendre.argtypes = [C.c_int, dp, dp]
+        L.por_conforming_matrix.argtypes = [C.c_int, dp]
+        L.por_conforming_matrix.restype = None
         L.por_legendre_eval.argtypes = [C.c_int, C.c_double, dp, dp]
         L.por_kernel_count.argtypes = [C.c_int, C.c_int]
         L.por_kernel_count.restype = C.c_int
@@ -178,11 +181,20 @@ def cheb2d_element(M: int, N: int, nq: int, nodes, ws, wuu, wuv, wvv):
 
 # ---------------------------------------------------------------- 3-D problem
 
+def conforming_matrix(n):
+    """R (n x n) of the reference's conforming_matrix(n-1) (assembly.cpp:476-489):
+    column m = modal coefficients of the conforming basis function phi_m."""
+    R = np.zeros(n * n)
+    lib().por_conforming_matrix(n, _dp(R))
+    return R.reshape(n, n)
+
+
 class Oracle:
     """3-D Legendre p2s problem on the CPU oracle."""
 
-    def __init__(self, n_comp, order, kinds, nq):
+    def __init__(self, n_comp, order, kinds, nq, basis=0):
         pb = Problem()
+        pb.basis = basis
         pb.n_comp = n_comp
         for d in range(3):
             pb.order[d] = order[d]

@@ -367,11 +367,50 @@ struct por_tables {
   long scratch;
 };
 
+void por_conforming_matrix(int n, double* R) {
+  memset(R, 0, sizeof(double) * (size_t)n * n);
+  R[0 * n + 0] = 0.5;
+  R[1 * n + 0] = -0.5;
+  R[0 * n + 1] = 0.5;
+  R[1 * n + 1] = 0.5;
+  for (int k = 2; k < n; ++k) {
+    R[k * n + k] = 1.0;
+    R[(k % 2) * n + k] = -1.0;
+  }
+}
+
+/* out[m][..] = sum_a R[a][m] in[a][..] over rows of length len (apply_conforming_transform,
+ * assembly.cpp:491-574, as a matrix product) */
+static void conform_rows(const double* R, int n, const double* in, double* out, long len) {
+  for (int m = 0; m < n; ++m)
+    for (long j = 0; j < len; ++j) {
+      double s = 0.0;
+      for (int a = 0; a < n; ++a)
+        if (R[a * n + m] != 0.0) s += R[a * n + m] * in[(long)a * len + j];
+      out[(long)m * len + j] = s;
+    }
+}
+
+/* C'[m1][m2][k] = sum_{a,b} R[a][m1] R[b][m2] C[a][b][k] */
+static void conform_coef(int N, int K, double* C) {
+  double* R = (double*)malloc(sizeof(double) * (size_t)N * N);
+  double* T = (double*)malloc(sizeof(double) * (size_t)N * N * K);
+  por_conforming_matrix(N, R);
+  conform_rows(R, N, C, T, (long)N * K);                 /* first index  */
+  for (int m1 = 0; m1 < N; ++m1)                          /* second index */
+    conform_rows(R, N, T + (long)m1 * N * K, C + (long)m1 * N * K, K);
+  free(T);
+  free(R);
+}
+
 por_tables* por_create(const por_problem* pb) {
   if (pb->n_terms < 1 || pb->n_terms > POR_MAX_TERMS) return NULL;
   if (pb->n_comp < 1 || pb->n_comp > 3) return NULL;
   for (int d = 0; d < 3; ++d)
     if (pb->order[d] < 1 || pb->order[d] > 40 || pb->nq[d] < 1 || pb->nq[d] > 96) return NULL;
+  if (pb->basis != 0 && pb->basis != 1) return NULL;
+  for (int d = 0; d < 3 && pb->basis; ++d)
+    if (pb->order[d] < 2) return NULL;
   por_tables* t = (por_tables*)calloc(1, sizeof(por_tables));
   t->pb = *pb;
   t->P = pb->n_comp * pb->n_comp;
@@ -390,6 +429,17 @@ por_tables* por_create(const por_problem* pb) {
         t->bP[d][(long)a * nq + q] = P[a];
         t->bD[d][(long)a * nq + q] = dP[a];
       }
+    }
+    if (pb->basis) {  /* transformed basis values for the direct path */
+      double* R = (double*)malloc(sizeof(double) * (size_t)N * N);
+      double* tmp = (double*)malloc(sizeof(double) * (size_t)N * nq);
+      por_conforming_matrix(N, R);
+      conform_rows(R, N, t->bP[d], tmp, nq);
+      memcpy(t->bP[d], tmp, sizeof(double) * (size_t)N * nq);
+      conform_rows(R, N, t->bD[d], tmp, nq);
+      memcpy(t->bD[d], tmp, sizeof(double) * (size_t)N * nq);
+      free(tmp);
+      free(R);
     }
   }
   long off = 0;
@@ -410,6 +460,7 @@ por_tables* por_create(const por_problem* pb) {
       }
       t->coef[s][d] = (double*)malloc(sizeof(double) * (size_t)N * N * K);
       por_legendre_coef(kind, N, K, t->coef[s][d]);
+      if (pb->basis) conform_coef(N, K, t->coef[s][d]);
       por_dir* pd = &t->term[s].d[d];
       pd->nt = N;
       pd->nr = N;

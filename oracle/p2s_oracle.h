@@ -43,6 +43,7 @@ typedef struct {
   int n_terms;                    /* N_s                                    */
   int kind[POR_MAX_TERMS][3];     /* POR_PP/DD/DP/PD per term, direction   */
   int nq[3];                      /* Gauss-Legendre points per direction   */
+  int basis;                      /* 0 modal, 1 conforming (por_conforming) */
 } por_problem;
 
 /* ---------------- 1-D primitives ---------------- */
@@ -62,6 +63,12 @@ int por_kernel_count(int kind, int N);
  * f_a(x) g_b(x) = sum_k C[a][b][k] P_k(x), f,g = P or P' per kind.
  * Role of product_to_sum (chebyshev.cpp:156-178) for the Legendre family. */
 void por_legendre_coef(int kind, int N, int K, double* C);
+
+/* The reference's conforming change of basis, conforming_matrix(n-1)
+ * (assembly.cpp:476-489): R is n x n, column m holds the modal coefficients of
+ * phi_m: phi_0 = (P_0 - P_1)/2, phi_1 = (P_0 + P_1)/2, phi_m = P_m - P_{m mod 2}.
+ * Row-major R[a*n + m]; n >= 2. */
+void por_conforming_matrix(int n, double* R);
 
 /* ---------------- generic separable engine ---------------- */
 

@@ -101,7 +101,12 @@ void put_case(const char* tag, const Mesh& mesh, const Orders& o, int nq, bool c
   const Mat* pb[8] = {&p2s.Suu, &p2s.Suv, &p2s.Svu, &p2s.Svv, &p2s.Muu, &p2s.Muv, &p2s.Mvu, &p2s.Mvv};
   const Mat* db[8] = {&dir.Suu, &dir.Suv, &dir.Svu, &dir.Svv, &dir.Muu, &dir.Muv, &dir.Mvu, &dir.Mvv};
   for (int b = 0; b < 8; ++b) put_mat((std::string("p2s_") + names[b]).c_str(), *pb[b]);
-  for (int b = 0; b < 8; ++b) put_mat((std::string("direct_") + names[b]).c_str(), *db[b], b < 7);
+  for (int b = 0; b < 8; ++b) put_mat((std::string("direct_") + names[b]).c_str(), *db[b]);
+  // conforming change of basis applied to the p2s blocks (apply_conforming_transform)
+  ElementMatrices conf = p2s;
+  apply_conforming_transform(conf);
+  const Mat* cb[8] = {&conf.Suu, &conf.Suv, &conf.Svu, &conf.Svv, &conf.Muu, &conf.Muv, &conf.Mvu, &conf.Mvv};
+  for (int b = 0; b < 8; ++b) put_mat((std::string("conf_") + names[b]).c_str(), *cb[b], b < 7);
   std::printf("}%s\n", comma ? "," : "");
 }
 
@@ -153,6 +158,14 @@ int main() {
       std::printf("]");
       first = false;
     }
+  std::printf("],\n\"conforming\":[");
+  for (int d = 1; d <= 16; ++d) {
+    const Mat r = conforming_matrix(d);
+    std::printf("%s[", d > 1 ? "," : "");
+    for (int i = 0; i < r.rows(); ++i)
+      for (int j = 0; j < r.cols(); ++j) std::printf("%s%.17g", i + j ? "," : "", r(i, j));
+    std::printf("]");
+  }
   std::printf("],\n\"cases\":[\n");
 
   // known-answer element (test_assembly.cpp:96-140)

@@ -53,7 +53,11 @@ class Problem(C.Structure):
         ("n_terms", C.c_int32),
         ("kind", (C.c_int32 * 3) * MAX_TERMS),
         ("nq", C.c_int32 * 3),
+        ("basis", C.c_int32),
     ]
+
+
+BASIS_MODAL, BASIS_CONFORMING = 0, 1
 
 
 class Cheb2dProblem(C.Structure):
@@ -149,8 +153,9 @@ def _check(status: int):
         raise P2SError(status, msg)
 
 
-def make_problem(n_comp, order, kinds, nq) -> Problem:
+def make_problem(n_comp, order, kinds, nq, basis=BASIS_MODAL) -> Problem:
     pb = Problem()
+    pb.basis = basis
     pb.n_comp = n_comp
     for d in range(3):
         pb.order[d] = order[d]
@@ -165,6 +170,10 @@ def make_problem(n_comp, order, kinds, nq) -> Problem:
 
 def shape_supported(n_comp, order, kinds, nq) -> bool:
     return bool(lib().p2s_shape_supported(C.byref(make_problem(n_comp, order, kinds, nq))))
+
+
+def shape_supported_basis(n_comp, order, kinds, nq, basis) -> bool:
+    return bool(lib().p2s_shape_supported(C.byref(make_problem(n_comp, order, kinds, nq, basis))))
 
 
 def _ptr(t) -> int:
@@ -183,8 +192,8 @@ def _ptr(t) -> int:
 class Context:
     """One p2s_ctx (tables uploaded once) on one device."""
 
-    def __init__(self, n_comp, order, kinds, nq, device: int = 0):
-        self.problem = make_problem(n_comp, order, kinds, nq)
+    def __init__(self, n_comp, order, kinds, nq, device: int = 0, basis: int = BASIS_MODAL):
+        self.problem = make_problem(n_comp, order, kinds, nq, basis)
         self.n_comp = n_comp
         self.order = tuple(order)
         self.kinds = [tuple(k) if isinstance(k, (tuple, list)) else (k, k, k) for k in kinds]
@@ -321,8 +330,8 @@ class DirectContext:
     """Direct-quadrature fill (p2s_direct_*): the ablation baseline, reference
     assemble_direct_element (assembly.hpp:50; assembly.cpp:134-274) in 3-D."""
 
-    def __init__(self, n_comp, order, kinds, nq, device: int = 0):
-        self.problem = make_problem(n_comp, order, kinds, nq)
+    def __init__(self, n_comp, order, kinds, nq, device: int = 0, basis: int = BASIS_MODAL):
+        self.problem = make_problem(n_comp, order, kinds, nq, basis)
         self.n_tot = n_comp * order[0] * order[1] * order[2]
         h = C.c_void_p()
         _check(lib().p2s_direct_create(C.byref(self.problem), device, C.byref(h)))

@@ -132,7 +132,8 @@ std::vector<double> pack_cu(const std::vector<const std::vector<double>*>& dense
         const int lo = band_lo(kd, a, b), cnt = band_count(kd, a, b);
         for (int j = 0; j < cnt; ++j)
           out[static_cast<size_t>(Cfg::coff(s, a, b) + j)] =
-              (*dense[static_cast<size_t>(s)])[(static_cast<size_t>(a) * Cfg::NU + b) * K + lo + 2 * j];
+              (*dense[static_cast<size_t>(s)])[(static_cast<size_t>(a) * Cfg::NU + b) * K + lo +
+                                               band_step(kd, a, b) * j];
       }
   }
   return out;
@@ -172,6 +173,10 @@ const std::vector<RegEntry>& registry() {
       make_entry<10, PP, DD>(),
       make_entry<3, DD>(),          make_entry<3, DP>(),      make_entry<3, PD>(),
       make_entry<4, DP, PD>(),      make_entry<3, PP, DP>(),  make_entry<4, PP, DD, DP, PD>(),
+      // conforming basis (kind | kConforming)
+      make_entry<3, PP | kConforming, DD | kConforming>(), make_entry<4, PP | kConforming>(),
+      make_entry<6, PP | kConforming, DD | kConforming>(),
+      make_entry<4, DP | kConforming, PD | kConforming>(),
   };
   return reg;
 }
@@ -214,7 +219,7 @@ std::vector<double> pack_v2(const V2Args& a) {
           const int co = Sh::coff(d, s, x, y);
           for (int j = 0; j < cnt; ++j)
             out[static_cast<size_t>(base[d] + co + j)] =
-                C[(static_cast<size_t>(x) * N + y) * K + lo + 2 * j];
+                C[(static_cast<size_t>(x) * N + y) * K + lo + band_step(kd, x, y) * j];
         }
     }
   return out;
@@ -312,6 +317,8 @@ V2Entry make_v2() {
 
 constexpr int kPPP = enc_kind(PP, PP, PP);
 constexpr int kDDD = enc_kind(DD, DD, DD);
+constexpr int kCPPP = enc_kind(PP | kConforming, PP | kConforming, PP | kConforming);
+constexpr int kCDDD = enc_kind(DD | kConforming, DD | kConforming, DD | kConforming);
 
 // <N_u, N_v, N_w, n1 tile, p1 tile, threads, min CTAs/SM, A once per unit, fibers per
 //  thread, term kinds...>.  Several variants per shape: the first is the default,
@@ -337,6 +344,9 @@ const std::vector<V2Entry>& v2_registry() {
       make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 20, 1, kPPP, kDDD>>(),
       make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 64, 2, kPPP, kDDD>>(),
       make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 66, 2, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+      // conforming basis
+      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kCPPP, kCDDD>>(),
+      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kCPPP, kCDDD>>(),
   };
   return reg;
 }
@@ -443,8 +453,8 @@ const MV2Entry* find_mv2(const p2s_problem& pb) {
     bool ok = r.S == pb.n_terms;
     for (int d = 0; d < 3; ++d) ok = ok && r.order[d] == pb.order[d] && r.nq[d] == pb.nq[d];
     for (int s = 0; ok && s < r.S; ++s)
-      for (int d = 0; d < 3; ++d) ok = ok && r.kinds[s][d] == pb.kind[s][d];
-    if (ok) return &r;
+      for (int d = 0; d < 3; ++d) ok = ok && r.kinds[s][d] == base_kind(pb.kind[s][d]);
+    if (ok) return &r;  // moments do not depend on the basis
   }
   return nullptr;
 }
@@ -567,6 +577,9 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 22, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
+      // C2 in the conforming basis
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kCPPP, kCDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
       // test shapes
       make_fused<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>,
                  MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),
@@ -604,6 +617,11 @@ struct LargeArgs {
 struct LargePack {
   std::vector<double> tab, cu, cvw;
   double* d_cvw = nullptr;
+  // runtime: parity-split u stage; v/w of chunk i+1 on `aux` overlapping u of
+  // chunk i on the caller's stream (X double-buffered), ordered by events
+  bool ps = true, overlap = true;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_vw[2]{}, ev_u[2]{};
 };
 
 using large_pack_fn = bool (*)(const LargeArgs&, LargePack&);
@@ -634,7 +652,7 @@ bool pack_large(const LargeArgs& a, LargePack& out) {
           const int lo = band_lo(kd, x, y), cnt = band_count(kd, x, y);
           for (int j = 0; j < cnt; ++j)
             v[base + static_cast<size_t>(Ls::coff(d, s, x, y) + j)] =
-                C[(static_cast<size_t>(x) * N + y) * K + lo + 2 * j];
+                C[(static_cast<size_t>(x) * N + y) * K + lo + band_step(kd, x, y) * j];
         }
     }
   };
@@ -689,22 +707,37 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
   up.P = P;
   up.Nt = Nt;
   std::memcpy(up.cu, pk.cu.data(), sizeof(double) * Ls::ctot(0));
-  for (int64_t u0 = 0; u0 < n_units; u0 += xchunk) {
+  // X holds two chunk buffers; chunk i uses buffer i % 2
+  const bool ov = pk.overlap && pk.aux != nullptr;
+  cudaError_t e;
+  if (ov) {
+    if ((e = cudaEventRecord(pk.ev_start, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(pk.aux, pk.ev_start, 0)) != cudaSuccess) return e;  // I ready
+  }
+  int64_t i = 0;
+  for (int64_t u0 = 0; u0 < n_units; u0 += xchunk, ++i) {
     const int64_t cnt = std::min(xchunk, n_units - u0);
+    const int b = static_cast<int>(i % 2);
+    double* Xb = X + (ov ? b : 0) * xchunk * Ls::XPU;
     LVWParams<Ls> vp;
     vp.I = I + u0 * Ls::MPP;
-    vp.X = X;
+    vp.X = Xb;
     vp.cvw = pk.d_cvw;
     vp.n_units = cnt;
-    large_vw_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), 256, vw_smem, st>>>(vp);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    // u stage: absolute units u0 .. u0+cnt-1; X holds the chunk
-    up.X = X;
+    cudaStream_t vs = ov ? pk.aux : st;
+    if (ov && i >= 2 && (e = cudaStreamWaitEvent(pk.aux, pk.ev_u[b], 0)) != cudaSuccess) return e;
+    large_vw_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), 256, vw_smem, vs>>>(vp);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (ov) {
+      if ((e = cudaEventRecord(pk.ev_vw[b], pk.aux)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(st, pk.ev_vw[b], 0)) != cudaSuccess) return e;
+    }
+    // u stage: absolute units u0 .. u0+cnt-1; Xb holds the chunk
+    up.X = Xb;
     up.n_units = cnt;
-    large_u_dispatch<Ls>(up, u0, cnt, st);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    large_u_dispatch<Ls>(up, u0, cnt, pk.ps, st);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (ov && (e = cudaEventRecord(pk.ev_u[b], st)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
@@ -740,6 +773,7 @@ const std::vector<LargeEntry>& large_registry() {
   static const std::vector<LargeEntry> reg = {
       make_large<LShape<16, 16, 16, 36, 36, 36, 8, kPPP, kDDD>>(),   // C5
       make_large<LShape<5, 4, 3, 8, 8, 6, 4, kPPP, kDDD>>(),         // test shape
+      make_large<LShape<5, 4, 3, 8, 8, 6, 4, kCPPP, kCDDD>>(),       // test shape, conforming
   };
   return reg;
 }
@@ -878,7 +912,22 @@ p2s_status validate(const p2s_problem* pb) {
   for (int s = 0; s < pb->n_terms; ++s)
     for (int d = 0; d < 3; ++d)
       if (pb->kind[s][d] < 0 || pb->kind[s][d] > 3) return fail(P2S_INVALID_ARG, "bad kind");
+  if (pb->basis != P2S_BASIS_MODAL && pb->basis != P2S_BASIS_CONFORMING)
+    return fail(P2S_INVALID_ARG, "basis must be P2S_BASIS_MODAL or P2S_BASIS_CONFORMING");
+  if (pb->basis == P2S_BASIS_CONFORMING)
+    for (int d = 0; d < 3; ++d)
+      if (pb->order[d] < 2)  // conforming_matrix needs degree >= 1 (assembly.cpp:478)
+        return fail(P2S_INVALID_ARG, "conforming basis needs order >= 2 in every direction");
   return P2S_OK;
+}
+
+// internal problem: the basis travels as bit 2 of every kind
+p2s_problem effective(const p2s_problem& pb) {
+  p2s_problem e = pb;
+  if (pb.basis == P2S_BASIS_CONFORMING)
+    for (int s = 0; s < pb.n_terms; ++s)
+      for (int d = 0; d < 3; ++d) e.kind[s][d] |= kConforming;
+  return e;
 }
 
 p2s_status run_moments(p2s_ctx* c, const double* alpha, double* I, int64_t n, cudaStream_t st) {
@@ -1052,16 +1101,19 @@ const char* p2s_kernel_path(const p2s_ctx* c) {
                                      : "two-stage: moments_kernel + contract_kernel (generic)";
 }
 
-int p2s_shape_supported(const p2s_problem* spec) {
-  if (!spec || validate(spec) != P2S_OK) return 0;
-  return find_entry(*spec) != nullptr || find_v2(*spec) != nullptr || find_large(*spec) != nullptr;
+int p2s_shape_supported(const p2s_problem* spec_in) {
+  if (!spec_in || validate(spec_in) != P2S_OK) return 0;
+  const p2s_problem eff = effective(*spec_in);
+  return find_entry(eff) != nullptr || find_v2(eff) != nullptr || find_large(eff) != nullptr;
 }
 
-p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
+p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
   if (!out) return fail(P2S_INVALID_ARG, "p2s_create: null out");
   *out = nullptr;
-  p2s_status st = validate(spec);
+  p2s_status st = validate(spec_in);
   if (st != P2S_OK) return st;
+  const p2s_problem eff = effective(*spec_in);
+  const p2s_problem* spec = &eff;
   const RegEntry* entry = find_entry(*spec);
   const V2Entry* v2e = find_v2(*spec);
   const LargeEntry* lge = find_large(*spec);
@@ -1205,9 +1257,20 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out) {
     for (int s = 0; s < S; ++s)
       for (int d = 0; d < 3; ++d) la.dense[s][d] = &c->coef[s][d];
     if (!lge->pack(la, c->lpack)) return fail(P2S_CUDA_ERROR, "p2s_create: large-path table upload");
-    // X chunk: ~64 MB of triangle-packed intermediates stays L2-resident between stages
-    c->xchunk = std::max<int64_t>(1, (int64_t(64) << 20) / (lge->xpu * 8));
-    P2S_CUDA(cudaMalloc(&c->d_X, sizeof(double) * lge->xpu * c->xchunk));
+    // X chunk: ~64 MB of triangle-packed intermediates per buffer (two buffers: the
+    // v/w stage of the next chunk overlaps the u stage of this one)
+    int64_t xmb = 64;
+    if (const char* v = std::getenv("P2S_XCHUNK_MB")) xmb = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("P2S_LARGE_PS")) c->lpack.ps = v[0] != '0';
+    if (const char* v = std::getenv("P2S_LARGE_OVERLAP")) c->lpack.overlap = v[0] != '0';
+    c->xchunk = std::max<int64_t>(1, (xmb << 20) / (lge->xpu * 8));
+    P2S_CUDA(cudaMalloc(&c->d_X, sizeof(double) * lge->xpu * c->xchunk * 2));
+    P2S_CUDA(cudaStreamCreateWithFlags(&c->lpack.aux, cudaStreamNonBlocking));
+    P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_start, cudaEventDisableTiming));
+    for (int b = 0; b < 2; ++b) {
+      P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_vw[b], cudaEventDisableTiming));
+      P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_u[b], cudaEventDisableTiming));
+    }
   }
 
   // scheduler chunk: moment scratch of ~32 MB stays in L2 between the stages
@@ -1232,6 +1295,12 @@ void p2s_destroy(p2s_ctx* c) {
   if (c->d_scratch) cudaFree(c->d_scratch);
   if (c->d_X) cudaFree(c->d_X);
   if (c->lpack.d_cvw) cudaFree(c->lpack.d_cvw);
+  if (c->lpack.aux) cudaStreamDestroy(c->lpack.aux);
+  if (c->lpack.ev_start) cudaEventDestroy(c->lpack.ev_start);
+  for (int b = 0; b < 2; ++b) {
+    if (c->lpack.ev_vw[b]) cudaEventDestroy(c->lpack.ev_vw[b]);
+    if (c->lpack.ev_u[b]) cudaEventDestroy(c->lpack.ev_u[b]);
+  }
   if (c->d_amma_fused) cudaFree(c->d_amma_fused);
   if (c->d_amma_v2) cudaFree(c->d_amma_v2);
   for (int i = 0; i < 2; ++i) {

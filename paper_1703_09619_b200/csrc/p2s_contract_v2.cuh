@@ -26,7 +26,8 @@
 
 namespace p2s {
 
-constexpr int enc_kind(int ku, int kv, int kw) { return ku | (kv << 2) | (kw << 4); }
+// term kinds of a shape: 3 bits per direction (base kind | conforming bit)
+constexpr int enc_kind(int ku, int kv, int kw) { return ku | (kv << 3) | (kw << 6); }
 
 // FLAGS bit 0 (AALL): stage A for all n1 once per unit; bit 1 (ROWLOOP): stage C
 // walks the m1 rows in a runtime loop (bounds the scheduler's window and
@@ -70,7 +71,7 @@ struct Shape {
   static constexpr int N(int d) { return d == 0 ? NU : d == 1 ? NV : NW; }
   static constexpr int kind(int s, int d) {
     const int k[] = {TK...};
-    return (k[s] >> (2 * d)) & 3;
+    return (k[s] >> (3 * d)) & 7;
   }
   static constexpr int K(int s, int d) { return kernel_count(kind(s, d), N(d)); }
   static constexpr int KTOT_U() {
@@ -79,7 +80,15 @@ struct Shape {
     return o;
   }
   // u-kernels of term s in parity class par (k1 = k0 + 2 idx, k0 = (par + shift) % 2)
-  static constexpr int ushift(int s) { return (kind(s, 0) == DP || kind(s, 0) == PD) ? 1 : 0; }
+  static constexpr int ushift(int s) {
+    return (base_kind(kind(s, 0)) == DP || base_kind(kind(s, 0)) == PD) ? 1 : 0;
+  }
+  static constexpr bool any_conforming() {
+    for (int s = 0; s < S; ++s)
+      for (int d = 0; d < 3; ++d)
+        if (conforming(kind(s, d))) return true;
+    return false;
+  }
   static constexpr int uk0(int s, int par) { return (par + ushift(s)) % 2; }
   static constexpr int ucnt(int s, int par) { return (K(s, 0) - uk0(s, par) + 1) / 2; }
   static constexpr int kpo(int s, int par) {
@@ -138,10 +147,12 @@ struct Shape {
   static constexpr bool sym_ok() {
     for (int s = 0; s < S; ++s)
       for (int d = 1; d < 3; ++d)
-        if (kind(s, d) != PP && kind(s, d) != DD) return false;
+        if (base_kind(kind(s, d)) != PP && base_kind(kind(s, d)) != DD) return false;
     return true;
   }
   static_assert(!SYM || (sym_ok() && P1T == NW_), "SYM needs symmetric v/w kinds and P1T == N_w");
+  static_assert(!(PSPLIT || MMA) || !any_conforming(),
+                "parity-split / DMMA stage C need parity bands (modal basis)");
   static constexpr int boff(int s) {
     int o = 0;
     for (int i = 0; i < s; ++i) o += T * K(i, 0) * BSTR;
@@ -210,7 +221,7 @@ __device__ __forceinline__ void v2_stage_a(const V2Params<Sh>& p, const double* 
             double v = 0.0;
             static_for<0, cnt>([&](auto jc) {
               constexpr int j = decltype(jc)::value;
-              v = fma(p.cv[co + j], x[lo + 2 * j], v);
+              v = fma(p.cv[co + j], x[lo + band_step(kv, n1, n2) * j], v);
             });
             As[k1 * Sh::aks(s) + n2 * Kw + k3] = v;
           });
@@ -256,7 +267,7 @@ __device__ __forceinline__ void v2_stage_b(const V2Params<Sh>& p, const double* 
             double v = 0.0;
             static_for<0, cnt>([&](auto jc) {
               constexpr int j = decltype(jc)::value;
-              v = fma(p.cw[co + j], y[lo + 2 * j], v);
+              v = fma(p.cw[co + j], y[lo + band_step(kw, pp1, p2) * j], v);
             });
             dst[p1l * NV * NW + p2] = v;
           });
@@ -294,7 +305,7 @@ __device__ __forceinline__ void v2_stage_a_sym(const V2Params<Sh>& p, const doub
             double v = 0.0;
             static_for<0, cnt>([&](auto jc) {
               constexpr int j = decltype(jc)::value;
-              v = fma(p.cv[co + j], x[lo + 2 * j], v);
+              v = fma(p.cv[co + j], x[lo + band_step(kv, n1, n2) * j], v);
             });
             As[Sh::tri(n1, n2, NV) * Kw] = v;
           });
@@ -337,7 +348,7 @@ __device__ __forceinline__ void v2_stage_b_sym(const V2Params<Sh>& p, const doub
             double v = 0.0;
             static_for<0, cnt>([&](auto jc) {
               constexpr int j = decltype(jc)::value;
-              v = fma(p.cw[co + j], y[lo + 2 * j], v);
+              v = fma(p.cw[co + j], y[lo + band_step(kw, p1, p2) * j], v);
             });
             dst[Sh::tri(p1, p2, NW)] = v;
           });
@@ -471,7 +482,8 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
                 constexpr int j = decltype(jc)::value;
                 const double c = p.cu[co + j];
                 constexpr int bi =
-                    PAR < 0 ? ko + lo + 2 * j : Sh::kpo(s, PAR) + (lo - Sh::uk0(s, PAR)) / 2 + j;
+                    PAR < 0 ? ko + lo + band_step(ku, m1, m2) * j
+                            : Sh::kpo(s, PAR) + (lo - Sh::uk0(s, PAR)) / 2 + j;
 #pragma unroll
                 for (int q = 0; q < FPT; ++q) v[q] = fma(c, b[q][bi], v[q]);
               });

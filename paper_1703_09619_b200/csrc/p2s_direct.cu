@@ -97,6 +97,12 @@ p2s_status p2s_direct_create(const p2s_problem* spec, int device, p2s_direct_ctx
     for (int d = 0; d < 3; ++d)
       if (spec->kind[s][d] < 0 || spec->kind[s][d] > 3)
         return p2s_internal_fail(P2S_INVALID_ARG, "p2s_direct_create: bad kind");
+  if (spec->basis != P2S_BASIS_MODAL && spec->basis != P2S_BASIS_CONFORMING)
+    return p2s_internal_fail(P2S_INVALID_ARG, "p2s_direct_create: bad basis");
+  if (spec->basis == P2S_BASIS_CONFORMING)
+    for (int d = 0; d < 3; ++d)
+      if (spec->order[d] < 2)
+        return p2s_internal_fail(P2S_INVALID_ARG, "conforming basis needs order >= 2");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return p2s_internal_fail(P2S_CUDA_ERROR, "p2s_direct_create: no CUDA device (no CPU fallback)");
@@ -135,11 +141,20 @@ p2s_status p2s_direct_create(const p2s_problem* spec, int device, p2s_direct_ctx
         const int kind = spec->kind[s][d], N = spec->order[d], nq = spec->nq[d];
         const bool deriv = side == 0 ? (kind == p2s::DD || kind == p2s::DP)
                                      : (kind == p2s::DD || kind == p2s::PD);
-        std::vector<long double> P(static_cast<size_t>(N) + 1), dP(static_cast<size_t>(N) + 1);
+        const bool conf = spec->basis == P2S_BASIS_CONFORMING;
+        std::vector<long double> P(static_cast<size_t>(N) + 2), dP(static_cast<size_t>(N) + 2);
         for (int q = 0; q < nq; ++q) {
-          p2s::legendre_ld(N, x[d][q], P.data(), dP.data());
+          p2s::legendre_ld(N + 1, x[d][q], P.data(), dP.data());
           for (int m = 0; m < N; ++m) {
-            long double v = deriv ? dP[m] : P[m];
+            long double v = 0.0L;
+            if (conf) {  // phi_m = sum_i R P_{sup(m, i)} (reference conforming_matrix)
+              for (int i = 0; i < 2; ++i) {
+                const int a = p2s::conf_sup(m, i);
+                v += p2s::conf_r(m, i) * (deriv ? dP[a] : P[a]);
+              }
+            } else {
+              v = deriv ? dP[m] : P[m];
+            }
             if (side == 1) v *= static_cast<long double>(w[d][q]);
             host[o + static_cast<size_t>(m) * nq + q] = static_cast<double>(v);
           }

@@ -207,6 +207,7 @@ struct ContractParams {
 
 __device__ __forceinline__ int dband_lo(int kind, int a, int b) { return band_lo(kind, a, b); }
 __device__ __forceinline__ int dband_hi(int kind, int a, int b) { return band_hi(kind, a, b); }
+__device__ __forceinline__ int dband_step(int kind, int a, int b) { return band_step(kind, a, b); }
 
 // One CTA per (element, pair, group of G n1-values).
 //   load:     the pair's moments I (all terms) -> smem with one bulk copy
@@ -273,10 +274,10 @@ __global__ void __launch_bounds__(256) contract_kernel(const __grid_constant__ C
       const int n1 = g * G + gi;
       double acc = 0.0;
       if (n1 < Nv) {
-        const int lo = dband_lo(kv, n1, n2), hi = dband_hi(kv, n1, n2);
+        const int lo = dband_lo(kv, n1, n2), hi = dband_hi(kv, n1, n2), st = dband_step(kv, n1, n2);
         const double* c = Cv + (n1 * Nv + n2) * Kv;
         const double* src = Is + k1 * Kv * Kw + k3;
-        for (int k2 = lo; k2 <= hi; k2 += 2) acc = fma(c[k2], src[k2 * Kw], acc);
+        for (int k2 = lo; k2 <= hi; k2 += st) acc = fma(c[k2], src[k2 * Kw], acc);
       }
       As[idx] = acc;
     }
@@ -306,10 +307,11 @@ __global__ void __launch_bounds__(256) contract_kernel(const __grid_constant__ C
       const int astride = Nv * Kw;
       const double* As = Abuf + p.a_off[s] + (gi * Ku * Nv + n2) * Kw;
       const double* cw = Ctab + p.cw_off[s] + (p1 * Nw + p2) * Kw;
-      const int lo = dband_lo(p.kind_w[s], p1, p2), hi = dband_hi(p.kind_w[s], p1, p2);
+      const int lo = dband_lo(p.kind_w[s], p1, p2), hi = dband_hi(p.kind_w[s], p1, p2),
+                st = dband_step(p.kind_w[s], p1, p2);
 #pragma unroll
       for (int k1 = 0; k1 < Ku; ++k1) b[ko + k1] = 0.0;
-      for (int k3 = lo; k3 <= hi; k3 += 2) {
+      for (int k3 = lo; k3 <= hi; k3 += st) {
         const double c = cw[k3];
 #pragma unroll
         for (int k1 = 0; k1 < Ku; ++k1) b[ko + k1] = fma(c, As[k1 * astride + k3], b[ko + k1]);
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(256) contract_kernel(const __grid_constant__ C
           constexpr int ko = Cfg::koff(s);
           static_for<0, cnt>([&](auto jc) {
             constexpr int j = decltype(jc)::value;
-            v = fma(p.cu[co + j], b[ko + lo + 2 * j], v);
+            v = fma(p.cu[co + j], b[ko + lo + band_step(kd, m1, m2) * j], v);
           });
         });
         st_cs(out + m1 * rowstep + m2 * colstep, v);

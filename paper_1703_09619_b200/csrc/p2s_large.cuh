@@ -27,7 +27,7 @@ struct LShape {
   static constexpr int H(int d) { return (Q(d) + 1) / 2; }
   static constexpr int kind(int s, int d) {
     const int k[] = {TK...};
-    return (k[s] >> (2 * d)) & 3;
+    return (k[s] >> (3 * d)) & 7;
   }
   static constexpr int K(int s, int d) { return kernel_count(kind(s, d), N(d)); }
   static constexpr int KMAX(int d) {
@@ -61,6 +61,23 @@ struct LShape {
     for (int i = 0; i < s; ++i) o += K(i, 0);
     return o;
   }
+  // u-kernels of term s in the parity class par of m1+m2 (k1 = uk0 + 2 idx)
+  static constexpr int ushift(int s) {
+    return (base_kind(kind(s, 0)) == DP || base_kind(kind(s, 0)) == PD) ? 1 : 0;
+  }
+  static constexpr bool u_conforming() {
+    for (int s = 0; s < S; ++s)
+      if (conforming(kind(s, 0))) return true;
+    return false;
+  }
+  static constexpr int uk0(int s, int par) { return (par + ushift(s)) % 2; }
+  static constexpr int ucnt(int s, int par) { return (K(s, 0) - uk0(s, par) + 1) / 2; }
+  static constexpr int kpo(int s, int par) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) o += ucnt(i, par);
+    return o;
+  }
+  static constexpr int KX(int par) { return par < 0 ? KUTOT() : kpo(S, par); }
   // band-packed coefficients of direction d (as Shape::coff)
   static constexpr int coff(int d, int s, int a, int b) {
     int o = 0;
@@ -89,7 +106,7 @@ struct LShape {
   static constexpr bool sym_ok() {
     for (int s = 0; s < S; ++s)
       for (int d = 1; d < 3; ++d)
-        if (kind(s, d) != PP && kind(s, d) != DD) return false;
+        if (base_kind(kind(s, d)) != PP && base_kind(kind(s, d)) != DD) return false;
     return true;
   }
   static_assert(sym_ok(), "large path needs symmetric v/w kinds (PP / DD)");
@@ -231,7 +248,7 @@ __device__ __forceinline__ void large_vw_term(const LVWParams<Ls>& p, int64_t un
           double v = 0.0;
           static_for<0, cnt>([&](auto jc) {
             constexpr int j = decltype(jc)::value;
-            v = fma(cv[co + j], x[lo + 2 * j], v);
+            v = fma(cv[co + j], x[lo + band_step(kv, a, b) * j], v);
           });
           Y[Ls::tri(a, b, NV) * KW + k3] = v;
         });
@@ -257,7 +274,7 @@ __device__ __forceinline__ void large_vw_term(const LVWParams<Ls>& p, int64_t un
           double v = 0.0;
           static_for<0, cnt>([&](auto jc) {
             constexpr int j = decltype(jc)::value;
-            v = fma(cw[co + j], y[lo + 2 * j], v);
+            v = fma(cw[co + j], y[lo + band_step(kw, a, b) * j], v);
           });
           o[Ls::tri(a, b, NW)] = v;
         });
@@ -293,8 +310,10 @@ struct LUParams {
   double cu[Ls::ctot(0)];
 };
 
-template <class Ls>
-__global__ void __launch_bounds__(Ls::NV * Ls::NW, 1)
+// PS: the (m1, m2) classes of even and odd m1+m2 run one after the other, each
+// holding only the x_s[k1] of its parity (half the registers: 2 CTAs per SM)
+template <class Ls, bool PS>
+__global__ void __launch_bounds__(Ls::NV * Ls::NW, PS ? 2 : 1)
     large_u_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0) {
   constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S, NQV = Ls::NQV, NQW = Ls::NQW;
   const int64_t b = blockIdx.x;
@@ -307,45 +326,69 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, 1)
   const int gci = pair / p.nc, gcj = pair - gci * p.nc;
   const int qv = n1 <= n2 ? Ls::tri(n1, n2, NV) : Ls::tri(n2, n1, NV);
   const int qw = p1 <= p2 ? Ls::tri(p1, p2, NW) : Ls::tri(p2, p1, NW);
-  double x[Ls::KUTOT()];
   const double* Xu = p.X + (unit - unit0) * Ls::XPU + static_cast<int64_t>(qv) * NQW + qw;
-  static_for<0, S>([&](auto sc) {
-    constexpr int s = decltype(sc)::value;
-#pragma unroll
-    for (int k1 = 0; k1 < Ls::K(s, 0); ++k1)
-      x[Ls::kuoff(s) + k1] = __ldg(Xu + Ls::xoff(s) + static_cast<int64_t>(k1) * NQV * NQW);
-  });
   double* out = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt + n1 * NW + p1) * p.ldM +
                 gcj * p.Nt + n2 * NW + p2;
   const int64_t rowstep = static_cast<int64_t>(NV * NW) * p.ldM;
-  auto row = [&](auto m1c) {
-    constexpr int m1 = decltype(m1c)::value;
-    static_for<0, NU>([&](auto m2c) {
-      constexpr int m2 = decltype(m2c)::value;
-      double v = 0.0;
-      static_for<0, S>([&](auto sc) {
-        constexpr int s = decltype(sc)::value;
-        constexpr int ku = Ls::kind(s, 0);
-        constexpr int lo = band_lo(ku, m1, m2), cnt = band_count(ku, m1, m2);
-        constexpr int co = Ls::coff(0, s, m1, m2);
-        static_for<0, cnt>([&](auto jc) {
-          constexpr int j = decltype(jc)::value;
-          v = fma(p.cu[co + j], x[Ls::kuoff(s) + lo + 2 * j], v);
-        });
+  auto run = [&](auto parc) {
+    constexpr int PAR = decltype(parc)::value;  // -1: every (m1, m2)
+    double x[Ls::KX(PAR)];
+    static_for<0, S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+      if constexpr (PAR < 0) {
+#pragma unroll
+        for (int k1 = 0; k1 < Ls::K(s, 0); ++k1)
+          x[Ls::kuoff(s) + k1] = __ldg(Xu + Ls::xoff(s) + static_cast<int64_t>(k1) * NQV * NQW);
+      } else {
+#pragma unroll
+        for (int j = 0; j < Ls::ucnt(s, PAR); ++j)
+          x[Ls::kpo(s, PAR) + j] = __ldg(
+              Xu + Ls::xoff(s) + static_cast<int64_t>(Ls::uk0(s, PAR) + 2 * j) * NQV * NQW);
+      }
+    });
+    auto row = [&](auto m1c) {
+      constexpr int m1 = decltype(m1c)::value;
+      static_for<0, NU>([&](auto m2c) {
+        constexpr int m2 = decltype(m2c)::value;
+        if constexpr (PAR < 0 || (m1 + m2) % 2 == PAR) {
+          double v = 0.0;
+          static_for<0, S>([&](auto sc) {
+            constexpr int s = decltype(sc)::value;
+            constexpr int ku = Ls::kind(s, 0);
+            constexpr int lo = band_lo(ku, m1, m2), cnt = band_count(ku, m1, m2);
+            constexpr int co = Ls::coff(0, s, m1, m2);
+            static_for<0, cnt>([&](auto jc) {
+              constexpr int j = decltype(jc)::value;
+              constexpr int xi = PAR < 0 ? Ls::kuoff(s) + lo + band_step(ku, m1, m2) * j
+                                         : Ls::kpo(s, PAR) + (lo - Ls::uk0(s, PAR)) / 2 + j;
+              v = fma(p.cu[co + j], x[xi], v);
+            });
+          });
+          st_cs(out + m1 * rowstep + m2 * (NV * NW), v);
+        }
       });
-      st_cs(out + m1 * rowstep + m2 * (NV * NW), v);
-    });
-  };
+    };
 #pragma unroll 1
-  for (int m1 = 0; m1 < NU; ++m1)
-    static_for<0, NU>([&](auto m1c) {
-      if (m1 == decltype(m1c)::value) row(m1c);
-    });
+    for (int m1 = 0; m1 < NU; ++m1)
+      static_for<0, NU>([&](auto m1c) {
+        if (m1 == decltype(m1c)::value) row(m1c);
+      });
+  };
+  if constexpr (PS && !Ls::u_conforming()) {
+    run(std::integral_constant<int, 0>{});
+    run(std::integral_constant<int, 1>{});
+  } else {
+    run(std::integral_constant<int, -1>{});
+  }
 }
 
 template <class Ls>
-void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, cudaStream_t st) {
-  large_u_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::NV * Ls::NW), Ls::NV * Ls::NW, 0, st>>>(p, unit0);
+void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>(cnt * Ls::NV * Ls::NW);
+  if (ps)
+    large_u_kernel<Ls, true><<<grid, Ls::NV * Ls::NW, 0, st>>>(p, unit0);
+  else
+    large_u_kernel<Ls, false><<<grid, Ls::NV * Ls::NW, 0, st>>>(p, unit0);
 }
 
 }  // namespace p2s

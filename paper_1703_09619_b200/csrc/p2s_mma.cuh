@@ -34,7 +34,9 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 template <class Sh>
 struct MmaMap {
   static constexpr int NU = Sh::NU, S = Sh::S;
-  static constexpr int shift(int s) { return (Sh::kind(s, 0) == DP || Sh::kind(s, 0) == PD) ? 1 : 0; }
+  static constexpr int shift(int s) {
+    return (base_kind(Sh::kind(s, 0)) == DP || base_kind(Sh::kind(s, 0)) == PD) ? 1 : 0;
+  }
   static constexpr int R(int par) {
     int n = 0;
     for (int a = 0; a < NU; ++a)

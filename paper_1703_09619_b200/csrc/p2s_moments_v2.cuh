@@ -26,7 +26,7 @@ struct MShape {
   static constexpr int H(int d) { return (Q(d) + 1) / 2; }  // half rule incl. centre
   static constexpr int kind(int s, int d) {
     const int k[] = {TK...};
-    return (k[s] >> (2 * d)) & 3;
+    return (k[s] >> (3 * d)) & 7;
   }
   static constexpr int K(int s, int d) { return kernel_count(kind(s, d), N(d)); }
   static constexpr int toff(int s, int d) {  // half-table offsets in the param block

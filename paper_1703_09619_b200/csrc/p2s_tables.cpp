@@ -72,6 +72,34 @@ std::vector<double> product_to_sum_table(int kind, int N) {
   const int KP = (N > K ? N : K) + 1;
   std::vector<long double> P(static_cast<size_t>(nq) * KP), dP(static_cast<size_t>(nq) * KP);
   for (int q = 0; q < nq; ++q) legendre_ld(KP, x[q], &P[q * KP], &dP[q * KP]);
+  if (conforming(kind)) {  // phi_m = sum_i conf_r(m, i) P_{conf_sup(m, i)}: fold R into the basis
+    std::vector<long double> Pc(P.size(), 0.0L), dPc(dP.size(), 0.0L);
+    for (int q = 0; q < nq; ++q)
+      for (int m = 0; m < N; ++m)
+        for (int i = 0; i < 2; ++i) {
+          const int a = conf_sup(m, i);
+          Pc[q * KP + m] += conf_r(m, i) * P[q * KP + a];
+          dPc[q * KP + m] += conf_r(m, i) * dP[q * KP + a];
+        }
+    // the kernel polynomials (index k) stay modal: P_k below
+    std::vector<double> C(static_cast<size_t>(N) * N * K, 0.0);
+    const int bk = base_kind(kind);
+    const bool da = (bk == DD || bk == DP), db = (bk == DD || bk == PD);
+    for (int a = 0; a < N; ++a)
+      for (int b = 0; b < N; ++b) {
+        const int lo = band_lo(kind, a, b), hi = band_hi(kind, a, b), st = band_step(kind, a, b);
+        for (int k = lo; k <= hi && k < K; k += st) {
+          long double s = 0.0L;
+          for (int q = 0; q < nq; ++q) {
+            const long double fa = da ? dPc[q * KP + a] : Pc[q * KP + a];
+            const long double gb = db ? dPc[q * KP + b] : Pc[q * KP + b];
+            s += w[q] * fa * gb * P[q * KP + k];
+          }
+          C[(static_cast<size_t>(a) * N + b) * K + k] = static_cast<double>(s * (2 * k + 1) / 2);
+        }
+      }
+    return C;
+  }
   const bool da = (kind == DD || kind == DP);
   const bool db = (kind == DD || kind == PD);
   std::vector<double> C(static_cast<size_t>(N) * N * K, 0.0);

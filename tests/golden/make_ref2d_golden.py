@@ -59,6 +59,9 @@ def main():
             if isinstance(v, dict) and "rows" in v:
                 el[f"{tag}__{k}"] = np.array(v["data"]).reshape(v["rows"], v["cols"])
     el["tags"] = np.array(tags)
+    # conforming_matrix(d), d = 1..16 (n = d + 1), row-major
+    for d_, r in enumerate(d["conforming"], start=1):
+        el[f"conforming_matrix__{d_ + 1}"] = np.array(r).reshape(d_ + 1, d_ + 1)
     np.savez_compressed(os.path.join(HERE, "ref2d_elements.npz"), **el)
     for f in ("ref2d_quadrature.npz", "ref2d_families.npz", "ref2d_elements.npz"):
         print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -22,5 +22,5 @@ def blocks_close(M_gpu, M_ref, n_comp, Nt, rtol=RTOL):
     return True, "", worst
 
 
-def oracle_for(n_comp, order, kinds, nq):
-    return O.Oracle(n_comp, order, kinds, nq)
+def oracle_for(n_comp, order, kinds, nq, basis=0):
+    return O.Oracle(n_comp, order, kinds, nq, basis)
