@@ -185,8 +185,10 @@ const char* p2s_kernel_path(const p2s_ctx* ctx);
  *                           (E_u index m*(N+1)+n, E_v index m*N+n)
  * ------------------------------------------------------------------------ */
 typedef struct {
-  int32_t M, N;  /* orders (chebfem::Orders) */
-  int32_t nq;    /* Gauss-Legendre points per direction */
+  int32_t M, N;        /* orders (chebfem::Orders) */
+  int32_t nq;          /* Gauss-Legendre points per direction */
+  int32_t conforming;  /* 1: blocks after apply_conforming_transform (assembly.cpp:555-574),
+                          folded into the expansion lists (no extra pass) */
 } p2s_cheb2d_problem;
 
 typedef struct {

@@ -51,9 +51,11 @@ Mat block(const std::vector<double>& flat, const p2s_cheb2d_sizes& sz, int b) {
   return m;
 }
 
-bool check_element(const Mesh& mesh, const Orders& o, const char* tag) {
+// conforming: the GPU folds apply_conforming_transform into its fill; the
+// reference applies it to its own p2s matrices afterwards
+bool check_element(const Mesh& mesh, const Orders& o, const char* tag, bool conforming) {
   const int nq = default_quad_points(o, mesh.elements[0].order);
-  p2s_cheb2d_problem pb{o.M, o.N, nq};
+  p2s_cheb2d_problem pb{o.M, o.N, nq, conforming ? 1 : 0};
   p2s_cheb2d_ctx* ctx = nullptr;
   if (p2s_cheb2d_create(&pb, 0, &ctx) != P2S_OK) {
     std::printf("FAIL %s: create: %s\n", tag, p2s_last_error());
@@ -89,10 +91,11 @@ bool check_element(const Mesh& mesh, const Orders& o, const char* tag) {
   gpu.Muv = block(blocks, sz, 5);
   gpu.Mvu = block(blocks, sz, 6);
   gpu.Mvv = block(blocks, sz, 7);
-  const ElementMatrices ref = assemble_p2s_element(compute_kernel_tables(mesh, 0, o, nq), o);
+  ElementMatrices ref = assemble_p2s_element(compute_kernel_tables(mesh, 0, o, nq), o);
+  if (conforming) apply_conforming_transform(ref);
   std::string msg;
   if (!element_matrices_close(ref, gpu, 1e-12, &msg)) {
-    std::printf("FAIL %s M=%d N=%d: %s\n", tag, o.M, o.N, msg.c_str());
+    std::printf("FAIL %s M=%d N=%d conforming=%d: %s\n", tag, o.M, o.N, conforming, msg.c_str());
     return false;
   }
   return true;
@@ -109,13 +112,16 @@ int main() {
       const Mesh mesh = random_single_element_mesh(rng, order_dist(rng));
       for (int mn = 1; mn <= 8; ++mn) {
         const std::string tag = "seed" + std::to_string(seed) + "/t" + std::to_string(trial);
-        ++n;
-        n_ok += check_element(mesh, Orders{mn, mn}, tag.c_str());
+        for (bool conf : {false, true}) {
+          ++n;
+          n_ok += check_element(mesh, Orders{mn, mn}, tag.c_str(), conf);
+        }
       }
-      for (const auto& mn : {std::pair<int, int>{1, 4}, {5, 2}, {3, 7}}) {
-        ++n;
-        n_ok += check_element(mesh, Orders{mn.first, mn.second}, "aniso");
-      }
+      for (const auto& mn : {std::pair<int, int>{1, 4}, {5, 2}, {3, 7}})
+        for (bool conf : {false, true}) {
+          ++n;
+          n_ok += check_element(mesh, Orders{mn.first, mn.second}, "aniso", conf);
+        }
     }
   }
   // the 16 elements of the paper's Fig.-1 benchmark domain at M = N = 4 and 8
@@ -123,12 +129,14 @@ int main() {
   for (size_t e = 0; e < dom.elements.size(); ++e) {
     Mesh one = dom;
     one.elements = {dom.elements[e]};
-    for (int mn : {4, 8}) {
-      ++n;
-      n_ok += check_element(one, Orders{mn, mn}, "fig1");
-    }
+    for (int mn : {4, 8})
+      for (bool conf : {false, true}) {
+        ++n;
+        n_ok += check_element(one, Orders{mn, mn}, "fig1", conf);
+      }
   }
-  std::printf("ref_dropin: %d / %d elements pass element_matrices_close(reference, gpu, 1e-12)\n",
+  std::printf("ref_dropin: %d / %d elements (modal and conforming) pass "
+              "element_matrices_close(reference, gpu, 1e-12)\n",
               n_ok, n);
   return n_ok == n ? 0 : 1;
 }

@@ -61,7 +61,7 @@ BASIS_MODAL, BASIS_CONFORMING = 0, 1
 
 
 class Cheb2dProblem(C.Structure):
-    _fields_ = [("M", C.c_int32), ("N", C.c_int32), ("nq", C.c_int32)]
+    _fields_ = [("M", C.c_int32), ("N", C.c_int32), ("nq", C.c_int32), ("conforming", C.c_int32)]
 
 
 class Cheb2dSizes(C.Structure):
@@ -286,9 +286,9 @@ class Cheb2dContext:
     """The reference's 2-D Chebyshev element (chebfem) on the GPU:
     kernel_tables() ~ compute_kernel_tables, assemble() ~ assemble_p2s_element."""
 
-    def __init__(self, M, N, nq, device: int = 0):
+    def __init__(self, M, N, nq, device: int = 0, conforming: bool = False):
         self.M, self.N, self.nq = M, N, nq
-        pb = Cheb2dProblem(M, N, nq)
+        pb = Cheb2dProblem(M, N, nq, 1 if conforming else 0)
         h = C.c_void_p()
         _check(lib().p2s_cheb2d_create(C.byref(pb), device, C.byref(h)))
         self.h = h

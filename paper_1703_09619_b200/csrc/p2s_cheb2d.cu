@@ -149,6 +149,58 @@ bool build_csr(int bt, int nt, int br, int nr, int kfam, int K, Csr& out, std::s
   return true;
 }
 
+// The reference's conforming change of basis on one side of a CSR (apply_conforming_
+// transform, assembly.cpp:491-574; R = conforming_matrix, :476-489): entry (a', b')
+// becomes sum_{a, b} R[a][a'] R[b][b'] entry(a, b) over the <= 2 x 2 supports, with
+// the expansion terms merged by kernel index.  ta / tb: transform the test / trial side.
+Csr conform_csr(const Csr& in, int nt, int nr, bool ta, bool tb) {
+  Csr out;
+  out.start.assign(static_cast<size_t>(nt * nr + 1), 0);
+  auto sup = [](bool on, int m, int i, int& idx, double& r) {
+    if (!on) {
+      idx = m;
+      r = 1.0;
+      return i == 0;
+    }
+    idx = conf_sup(m, i);
+    r = conf_r(m, i);
+    return true;
+  };
+  for (int a2 = 0; a2 < nt; ++a2)
+    for (int b2 = 0; b2 < nr; ++b2) {
+      out.start[static_cast<size_t>(a2 * nr + b2)] = static_cast<int>(out.k.size());
+      std::vector<std::pair<int, double>> acc;
+      for (int i = 0; i < 2; ++i) {
+        int a;
+        double ra;
+        if (!sup(ta, a2, i, a, ra)) continue;
+        for (int j = 0; j < 2; ++j) {
+          int b;
+          double rb;
+          if (!sup(tb, b2, j, b, rb)) continue;
+          const size_t ab = static_cast<size_t>(a * nr + b);
+          for (int t = in.start[ab]; t < in.start[ab + 1]; ++t) {
+            const double v = ra * rb * in.c[static_cast<size_t>(t)];
+            bool found = false;
+            for (auto& kv : acc)
+              if (kv.first == in.k[static_cast<size_t>(t)]) {
+                kv.second += v;
+                found = true;
+              }
+            if (!found) acc.emplace_back(in.k[static_cast<size_t>(t)], v);
+          }
+        }
+      }
+      for (const auto& kv : acc)
+        if (kv.second != 0.0) {
+          out.k.push_back(kv.first);
+          out.c.push_back(kv.second);
+        }
+    }
+  out.start[static_cast<size_t>(nt * nr)] = static_cast<int>(out.k.size());
+  return out;
+}
+
 }  // namespace
 
 struct p2s_cheb2d_ctx {
@@ -184,6 +236,8 @@ p2s_status p2s_cheb2d_create(const p2s_cheb2d_problem* spec, int device, p2s_che
   const int M = spec->M, N = spec->N, nq = spec->nq;
   if (M < 1 || N < 1 || M > 64 || N > 64) return p2s_internal_fail(P2S_INVALID_ARG, "orders must be 1..64");
   if (nq < 1 || nq > 128) return p2s_internal_fail(P2S_INVALID_ARG, "nq must be 1..128");
+  if (spec->conforming != 0 && spec->conforming != 1)
+    return p2s_internal_fail(P2S_INVALID_ARG, "conforming must be 0 or 1");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return p2s_internal_fail(P2S_CUDA_ERROR, "p2s_cheb2d_create: no CUDA device (no CPU fallback)");
@@ -243,6 +297,11 @@ p2s_status p2s_cheb2d_create(const p2s_cheb2d_problem* spec, int device, p2s_che
     if (!build_csr(spec8[bi].ut, ntu, spec8[bi].ur, nru, fu[tab], c->params.t[tab].Ku, cu, err) ||
         !build_csr(spec8[bi].vt, ntv, spec8[bi].vr, nrv, fv[tab], c->params.t[tab].Kv, cv, err))
       return p2s_internal_fail(P2S_INVALID_ARG, "p2s_cheb2d_create: " + err);
+    if (spec->conforming) {
+      // E_u = m (N+1) + n: the v index n is transformed; E_v = m N + n: the u index m
+      cv = conform_csr(cv, ntv, nrv, ti == 0, tj == 0);
+      cu = conform_csr(cu, ntu, nru, ti == 1, tj == 1);
+    }
     BlockSpec& b = c->params.b[bi];
     b.rows = ntu * ntv;
     b.cols = nru * nrv;

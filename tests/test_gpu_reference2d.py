@@ -18,10 +18,10 @@ E = np.load(os.path.join(os.path.dirname(__file__), "golden", "ref2d_elements.np
 TAGS = [str(t) for t in E["tags"]]
 
 
-def _run(tag):
+def _run(tag, conforming=False):
     g = lambda k: E[f"{tag}__{k}"]
     M, N, nq = int(g("M")), int(g("N")), int(g("nq"))
-    ctx = capi.Cheb2dContext(M, N, nq)
+    ctx = capi.Cheb2dContext(M, N, nq, conforming=conforming)
     grids = np.stack([g("ws"), g("wuu"), g("wuv"), g("wvv")]).reshape(1, -1)
     dg = torch.from_numpy(np.ascontiguousarray(grids)).cuda()
     dt = torch.full((1, ctx.sizes.tables_per_elem), float("nan"), dtype=torch.float64, device="cuda")
@@ -44,6 +44,16 @@ def test_gpu_reproduces_reference_element(tag):
         # and the reference's direct quadrature (assemble_direct_element)
         ok, ij = O.block_close(v, g("direct_" + k), 1e-10)
         assert ok, (tag, "direct", k, ij)
+
+
+@pytest.mark.parametrize("tag", TAGS)
+def test_gpu_conforming_reproduces_reference_transform(tag):
+    """Conforming mode: the reference's apply_conforming_transform (assembly.cpp:
+    555-574) of its p2s blocks, folded into the GPU fill."""
+    g, _, blocks = _run(tag, conforming=True)
+    for k, v in blocks.items():
+        ok, ij = O.block_close(v, g("conf_" + k), 1e-12)
+        assert ok, (tag, k, ij)
 
 
 def test_gpu_reference_known_answers():
@@ -70,4 +80,4 @@ def test_reference_calls_gpu_fill_through_the_c_abi():
     import subprocess
     r = subprocess.run([REF_DROPIN], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-    assert "elements pass" in r.stdout
+    assert "elements (modal and conforming) pass" in r.stdout
