@@ -161,6 +161,19 @@ void p2s_direct_destroy(p2s_direct_ctx* ctx);
 p2s_status p2s_direct_fill(p2s_direct_ctx* ctx, const double* d_alpha, double* d_M, int64_t ld_M,
                            int64_t n_elem, void* stream);
 
+/* ---- Global scatter-add (the step after the fill: reference assemble_global,
+ * assembly.cpp:594-652) ----
+ * G[gi][gj] += s_i s_j E_e[i][j] over elements e and local DOFs i, j whose free
+ * index dof_free[e][i] is >= 0 (-1 = PEC-constrained, dropped); dof_sign = +-1.
+ * Element e's matrix: d_elem + e*elem_stride, row-major with leading dimension
+ * ld_elem (the p2s_fill output: elem_stride = n_tot*ld_M).  The caller zeroes G
+ * (n_free x n_free, leading dimension ld_G).  FP64 atomics: shared entries add up
+ * in unspecified order (equal to the reference's serial sum up to rounding).
+ * n_local <= 4096. */
+p2s_status p2s_scatter_add(const double* d_elem, int64_t elem_stride, int64_t ld_elem, int32_t n_local,
+                           const int32_t* d_dof_free, const double* d_dof_sign, int64_t n_elem,
+                           double* d_G, int64_t ld_G, void* stream);
+
 /* 1 if the orders / kinds have a compiled kernel instantiation. */
 int p2s_shape_supported(const p2s_problem* spec);
 
@@ -209,6 +222,14 @@ p2s_status p2s_cheb2d_get_sizes(const p2s_cheb2d_ctx* ctx, p2s_cheb2d_sizes* out
 p2s_status p2s_cheb2d_kernel_tables(p2s_cheb2d_ctx* ctx, const double* d_grids, double* d_tables,
                                     int64_t n_elem, void* stream);
 /* assemble_p2s_element (assembly.cpp:375-474) for n_elem elements */
+/* assemble_global (assembly.cpp:594-652) from the eight blocks in place: local DOF
+ * i < n_eu is E_u row i, else E_v row i - n_eu; S from Suu..Svv, M from Muu..Mvv
+ * (build the blocks with conforming = 1 for the reference's assemble_system);
+ * dof_free / dof_sign [E][n_eu + n_ev] from the reference's DofMap (free_index of
+ * element_dofs[e][i].global, and .sign).  The caller zeroes S and M. */
+p2s_status p2s_cheb2d_scatter(const p2s_cheb2d_ctx* ctx, const double* d_blocks, const int32_t* d_dof_free,
+                              const double* d_dof_sign, int64_t n_elem, double* d_S, double* d_M,
+                              int64_t ld_G, void* stream);
 p2s_status p2s_cheb2d_assemble(p2s_cheb2d_ctx* ctx, const double* d_tables, double* d_blocks,
                                int64_t n_elem, void* stream);
 

@@ -11,6 +11,7 @@
 // by tests/test_gpu_reference2d.py.  Exit 0 = every element passed.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <random>
 #include <string>
@@ -18,6 +19,8 @@
 
 #include "chebfem/assembly.hpp"
 #include "chebfem/bench.hpp"
+#include "chebfem/dof_map.hpp"
+#include "chebfem/mesh.hpp"
 #include "chebfem/quadrature.hpp"
 #include "p2s_b200.h"
 
@@ -101,6 +104,83 @@ bool check_element(const Mesh& mesh, const Orders& o, const char* tag, bool conf
   return true;
 }
 
+// The reference's assemble_system (assembly.cpp:702-711) with the fill, the
+// conforming transform and the global scatter on the GPU: connectivity from the
+// reference's build_connectivity, every element's grids in one batched
+// p2s_cheb2d_kernel_tables / p2s_cheb2d_assemble (conforming = 1) call, then
+// p2s_cheb2d_scatter; compared with the reference's global S and M.
+bool check_system(const Mesh& mesh, const Orders& o, const char* tag) {
+  int geom = 1;
+  for (const auto& el : mesh.elements) geom = std::max(geom, el.order);
+  const int nq = default_quad_points(o, geom);
+  const DofMap dm = build_connectivity(mesh, o.M, o.N);
+  const int E = static_cast<int>(mesh.elements.size());
+  p2s_cheb2d_problem pb{o.M, o.N, nq, 1};
+  p2s_cheb2d_ctx* ctx = nullptr;
+  if (p2s_cheb2d_create(&pb, 0, &ctx) != P2S_OK) return false;
+  p2s_cheb2d_sizes sz{};
+  p2s_cheb2d_get_sizes(ctx, &sz);
+  const int n_local = sz.n_eu + sz.n_ev;
+  std::vector<double> grids;
+  std::vector<int32_t> fr;
+  std::vector<double> sg;
+  for (int e = 0; e < E; ++e) {
+    Mesh one = mesh;
+    one.elements = {mesh.elements[static_cast<size_t>(e)]};
+    const std::vector<double> g = coupling_grids(one, nq);
+    grids.insert(grids.end(), g.begin(), g.end());
+    for (int i = 0; i < n_local; ++i) {
+      const DofMap::LocalDof& d = dm.element_dofs[static_cast<size_t>(e)][static_cast<size_t>(i)];
+      fr.push_back(dm.free_index[static_cast<size_t>(d.global)]);
+      sg.push_back(d.sign);
+    }
+  }
+  const int nf = dm.n_free;
+  double *dg, *dt, *db, *dS, *dM, *dsg;
+  int32_t* dfr;
+  cudaMalloc(&dg, sizeof(double) * grids.size());
+  cudaMalloc(&dt, sizeof(double) * sz.tables_per_elem * E);
+  cudaMalloc(&db, sizeof(double) * sz.blocks_per_elem * E);
+  cudaMalloc(&dS, sizeof(double) * nf * nf);
+  cudaMalloc(&dM, sizeof(double) * nf * nf);
+  cudaMalloc(&dfr, sizeof(int32_t) * fr.size());
+  cudaMalloc(&dsg, sizeof(double) * sg.size());
+  cudaMemcpy(dg, grids.data(), sizeof(double) * grids.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dfr, fr.data(), sizeof(int32_t) * fr.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dsg, sg.data(), sizeof(double) * sg.size(), cudaMemcpyHostToDevice);
+  cudaMemset(dS, 0, sizeof(double) * nf * nf);
+  cudaMemset(dM, 0, sizeof(double) * nf * nf);
+  bool ok = p2s_cheb2d_kernel_tables(ctx, dg, dt, E, nullptr) == P2S_OK &&
+            p2s_cheb2d_assemble(ctx, dt, db, E, nullptr) == P2S_OK &&
+            p2s_cheb2d_scatter(ctx, db, dfr, dsg, E, dS, dM, nf, nullptr) == P2S_OK;
+  ElementMatrices gpu, ref;
+  gpu.orders = ref.orders = o;
+  gpu.Suu = Mat(nf, nf);
+  gpu.Muu = Mat(nf, nf);
+  ok = ok &&
+       cudaMemcpy(gpu.Suu.data().data(), dS, sizeof(double) * nf * nf, cudaMemcpyDeviceToHost) == cudaSuccess &&
+       cudaMemcpy(gpu.Muu.data().data(), dM, sizeof(double) * nf * nf, cudaMemcpyDeviceToHost) == cudaSuccess;
+  for (void* p : {static_cast<void*>(dg), static_cast<void*>(dt), static_cast<void*>(db),
+                  static_cast<void*>(dS), static_cast<void*>(dM), static_cast<void*>(dfr),
+                  static_cast<void*>(dsg)})
+    cudaFree(p);
+  p2s_cheb2d_destroy(ctx);
+  if (!ok) {
+    std::printf("FAIL system %s: GPU call failed: %s\n", tag, p2s_last_error());
+    return false;
+  }
+  const GlobalSystem sys = assemble_system(mesh, o, Backend::p2s, nq, 1);
+  ref.Suu = sys.S;
+  ref.Muu = sys.M;
+  std::string msg;
+  // the reference's own comparator on (S, M) carried in the Suu / Muu slots
+  if (!element_matrices_close(ref, gpu, 1e-12, &msg)) {
+    std::printf("FAIL system %s M=%d N=%d: %s\n", tag, o.M, o.N, msg.c_str());
+    return false;
+  }
+  return true;
+}
+
 }  // namespace
 
 int main() {
@@ -135,8 +215,18 @@ int main() {
         n_ok += check_element(one, Orders{mn, mn}, "fig1", conf);
       }
   }
+  // full pipeline: connectivity + GPU fill + conforming + GPU scatter vs assemble_system
+  int s_ok = 0, s_n = 0;
+  for (int nx : {2, 4})
+    for (int mn : {2, 4, 6}) {
+      ++s_n;
+      s_ok += check_system(generate_benchmark_domain(nx, nx, 4), Orders{mn, mn}, "benchmark");
+    }
+  ++s_n;
+  s_ok += check_system(generate_benchmark_domain(3, 2, 3), Orders{3, 5}, "benchmark-aniso");
+  std::printf("ref_dropin: %d / %d global systems (assemble_system on GPU) pass\n", s_ok, s_n);
   std::printf("ref_dropin: %d / %d elements (modal and conforming) pass "
               "element_matrices_close(reference, gpu, 1e-12)\n",
               n_ok, n);
-  return n_ok == n ? 0 : 1;
+  return (n_ok == n && s_ok == s_n) ? 0 : 1;
 }

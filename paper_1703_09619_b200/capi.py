@@ -29,7 +29,8 @@ EXPORTS = ("p2s_create", "p2s_destroy", "p2s_get_sizes", "p2s_moments", "p2s_con
            "p2s_version", "p2s_kernel_path", "p2s_moments_host", "p2s_contract_host",
            "p2s_cheb2d_create", "p2s_cheb2d_destroy", "p2s_cheb2d_get_sizes",
            "p2s_cheb2d_kernel_tables", "p2s_cheb2d_assemble",
-           "p2s_direct_create", "p2s_direct_destroy", "p2s_direct_fill")
+           "p2s_direct_create", "p2s_direct_destroy", "p2s_direct_fill",
+           "p2s_scatter_add", "p2s_cheb2d_scatter")
 
 
 class P2SError(RuntimeError):
@@ -135,6 +136,8 @@ def lib():
         L.p2s_direct_destroy.argtypes = [vp]
         L.p2s_direct_destroy.restype = None
         L.p2s_direct_fill.argtypes = [vp, vp, vp, i64, i64, vp]
+        L.p2s_scatter_add.argtypes = [vp, i64, i64, C.c_int32, vp, vp, i64, vp, i64, vp]
+        L.p2s_cheb2d_scatter.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp]
         for f in EXPORTS:
             if f not in ("p2s_destroy", "p2s_shape_supported", "p2s_last_error", "p2s_version",
                          "p2s_kernel_path", "p2s_cheb2d_destroy", "p2s_direct_destroy"):
@@ -315,6 +318,11 @@ class Cheb2dContext:
         _check(lib().p2s_cheb2d_assemble(self.h, _ptr(d_tables), _ptr(d_blocks), n_elem,
                                          _ptr(stream)))
 
+    def scatter(self, d_blocks, d_dof_free, d_dof_sign, n_elem, d_S, d_M, ld_G, stream=0):
+        """assemble_global (assembly.cpp:594-652) from the eight blocks, on the device."""
+        _check(lib().p2s_cheb2d_scatter(self.h, _ptr(d_blocks), _ptr(d_dof_free), _ptr(d_dof_sign),
+                                        n_elem, _ptr(d_S), _ptr(d_M), ld_G, _ptr(stream)))
+
     def split_tables(self, flat):
         sz = self.sizes
         return {n: flat[sz.table_offset[i]:sz.table_offset[i] + sz.table_rows[i] * sz.table_cols[i]]
@@ -350,3 +358,11 @@ class DirectContext:
             self.close()
         except Exception:
             pass
+
+
+def scatter_add(d_elem, elem_stride, ld_elem, n_local, d_dof_free, d_dof_sign, n_elem, d_G, ld_G,
+                stream=0):
+    """Global scatter-add G[gi][gj] += s_i s_j E[i][j] (reference assemble_global,
+    assembly.cpp:594-652) on the device."""
+    _check(lib().p2s_scatter_add(_ptr(d_elem), elem_stride, ld_elem, n_local, _ptr(d_dof_free),
+                                 _ptr(d_dof_sign), n_elem, _ptr(d_G), ld_G, _ptr(stream)))

@@ -228,6 +228,19 @@ bool upload(p2s_cheb2d_ctx* c, const std::vector<T>& v, const T** out) {
 
 }  // namespace
 
+bool p2s_cheb2d_block_layout(const p2s_cheb2d_ctx* c, int64_t off[8], int rows[8], int cols[8],
+                             int* n_eu, int* n_ev) {
+  if (!c) return false;
+  for (int q = 0; q < 8; ++q) {
+    off[q] = c->sz.block_offset[q];
+    rows[q] = c->sz.block_rows[q];
+    cols[q] = c->sz.block_cols[q];
+  }
+  *n_eu = c->sz.n_eu;
+  *n_ev = c->sz.n_ev;
+  return true;
+}
+
 extern "C" {
 
 p2s_status p2s_cheb2d_create(const p2s_cheb2d_problem* spec, int device, p2s_cheb2d_ctx** out) {

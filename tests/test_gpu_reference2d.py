@@ -81,3 +81,4 @@ def test_reference_calls_gpu_fill_through_the_c_abi():
     r = subprocess.run([REF_DROPIN], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "elements (modal and conforming) pass" in r.stdout
+    assert "global systems (assemble_system on GPU) pass" in r.stdout
