@@ -136,6 +136,31 @@ p2s_status p2s_alpha_generate(p2s_ctx* ctx, int alpha_kind, double lo, double hi
                               uint64_t seed, int64_t e0, int64_t n_elem, double* d_alpha,
                               void* stream);
 
+/* ---- Element geometry instead of sampled alpha ----
+ * A geometry record of P2S_GEOM_DOUBLES doubles per element: the 8 corners of the
+ * hexahedron's trilinear map X[c][d] (corner c at reference (+-1, +-1, +-1), bit d
+ * of c = sign along d) and the material (a, b, c, phi) of
+ * alpha_mat = 1 + 0.3 sin(a u + b v + c w + phi).  The coupling factors are the
+ * P2S_ALPHA_JACOBIAN family: alpha_mat detJ (J^T J)^-1 (even terms) and
+ * alpha_mat (J^T J)/detJ (odd terms), per component pair -- the 3-D analogue of
+ * build_element_quad (assembly.cpp:51-119).
+ *   p2s_geometry_generate    seeded records (harness; p2s_alpha_generate(JACOBIAN)
+ *                            is alpha_from_geometry of these records, bit for bit)
+ *   p2s_alpha_from_geometry  alpha [E][P][S][nq_w][nq_v][nq_u] from records
+ *   p2s_fill_geometry        the fill straight from records: alpha of a chunk of
+ *                            elements is produced into an L2-resident double buffer
+ *                            on an internal stream while the fill consumes the
+ *                            other, so alpha never round-trips through HBM; equal
+ *                            bit for bit to p2s_fill(p2s_alpha_from_geometry(...)).
+ *                            Not re-entrant on one context (internal buffers). */
+#define P2S_GEOM_DOUBLES 28
+p2s_status p2s_geometry_generate(p2s_ctx* ctx, double lo, double hi, uint64_t seed, int64_t e0,
+                                 int64_t n_elem, double* d_geom, void* stream);
+p2s_status p2s_alpha_from_geometry(p2s_ctx* ctx, const double* d_geom, int64_t n_elem, double* d_alpha,
+                                   void* stream);
+p2s_status p2s_fill_geometry(p2s_ctx* ctx, const double* d_geom, double* d_M, int64_t ld_M, int64_t n_elem,
+                             void* stream);
+
 /* Host copies of the uploaded tables: phi = w_q P_k(x_q) as [K][nq],
  * coef = [N][N][K]; nodes/weights [nq].  Any pointer may be NULL. */
 p2s_status p2s_get_tables(const p2s_ctx* ctx, int term, int dir, double* phi, double* coef,

@@ -30,7 +30,8 @@ EXPORTS = ("p2s_create", "p2s_destroy", "p2s_get_sizes", "p2s_moments", "p2s_con
            "p2s_cheb2d_create", "p2s_cheb2d_destroy", "p2s_cheb2d_get_sizes",
            "p2s_cheb2d_kernel_tables", "p2s_cheb2d_assemble",
            "p2s_direct_create", "p2s_direct_destroy", "p2s_direct_fill",
-           "p2s_scatter_add", "p2s_cheb2d_scatter")
+           "p2s_scatter_add", "p2s_cheb2d_scatter",
+           "p2s_geometry_generate", "p2s_alpha_from_geometry", "p2s_fill_geometry")
 
 
 class P2SError(RuntimeError):
@@ -136,6 +137,9 @@ def lib():
         L.p2s_direct_destroy.argtypes = [vp]
         L.p2s_direct_destroy.restype = None
         L.p2s_direct_fill.argtypes = [vp, vp, vp, i64, i64, vp]
+        L.p2s_geometry_generate.argtypes = [vp, C.c_double, C.c_double, C.c_uint64, i64, i64, vp, vp]
+        L.p2s_alpha_from_geometry.argtypes = [vp, vp, i64, vp, vp]
+        L.p2s_fill_geometry.argtypes = [vp, vp, vp, i64, i64, vp]
         L.p2s_scatter_add.argtypes = [vp, i64, i64, C.c_int32, vp, vp, i64, vp, i64, vp]
         L.p2s_cheb2d_scatter.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp]
         for f in EXPORTS:
@@ -240,6 +244,17 @@ class Context:
 
     def fill(self, d_alpha, d_M, ld_M, n_elem, stream=0):
         _check(lib().p2s_fill(self.h, _ptr(d_alpha), _ptr(d_M), ld_M, n_elem, _ptr(stream)))
+
+    GEOM_DOUBLES = 28
+
+    def geometry_generate(self, lo, hi, seed, e0, n_elem, d_geom, stream=0):
+        _check(lib().p2s_geometry_generate(self.h, lo, hi, seed, e0, n_elem, _ptr(d_geom), _ptr(stream)))
+
+    def alpha_from_geometry(self, d_geom, n_elem, d_alpha, stream=0):
+        _check(lib().p2s_alpha_from_geometry(self.h, _ptr(d_geom), n_elem, _ptr(d_alpha), _ptr(stream)))
+
+    def fill_geometry(self, d_geom, d_M, ld_M, n_elem, stream=0):
+        _check(lib().p2s_fill_geometry(self.h, _ptr(d_geom), _ptr(d_M), ld_M, n_elem, _ptr(stream)))
 
     def fill_host(self, h_alpha, h_M, ld_M, n_elem):
         _check(lib().p2s_fill_host(self.h, _ptr(h_alpha), _ptr(h_M), ld_M, n_elem))

@@ -22,6 +22,11 @@
 #include "p2s_tables.hpp"
 
 namespace p2s {
+cudaError_t launch_geometry(double* geom, double lo, double hi, uint64_t seed, int64_t e0, int64_t n,
+                            cudaStream_t stream);
+cudaError_t launch_alpha_geometry_fast(double* alpha, const double* geom, const double* const x[3],
+                                       const int nq[3], int nc, int S, int64_t n, int64_t per_elem,
+                                       cudaStream_t stream);
 cudaError_t launch_alpha(double* alpha, const double* const x[3], const int nq[3], int nc, int S,
                          int kind, double lo, double hi, uint64_t seed, int64_t e0, int64_t n,
                          int64_t per_elem, cudaStream_t stream);
@@ -465,12 +470,17 @@ using fused_fn = cudaError_t (*)(const double*, double*, int64_t, int64_t, int64
                                  const std::vector<double>&, const std::vector<double>&,
                                  const double*, cudaStream_t, int);
 
-template <class Sh, class Ms>
+// GEO: `alpha` is the geometry records and the kernel computes the coupling
+// factors itself (xq = the GL nodes u, v, w in mpack's tail, see pack_fused_geo)
+template <class Sh, class Ms, bool GEO = false>
 cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_tot, int64_t n_elem,
                          int nc, int P, int Nt, const std::vector<double>& cpack,
                          const std::vector<double>& mpack, const double* amma, cudaStream_t st,
                          int num_sms) {
   FusedParams<Sh, Ms> p;
+  p.geom = GEO ? alpha : nullptr;
+  if constexpr (GEO)
+    std::memcpy(p.xq, mpack.data() + Ms::TALL, sizeof(double) * (Ms::Q(0) + Ms::Q(1) + Ms::Q(2)));
   p.c.I = nullptr;
   p.c.M = M;
   p.c.ldM = ldM;
@@ -492,11 +502,12 @@ cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_
   constexpr size_t smem = FusedLayout<Sh, Ms>::SMEM;
   static int blocks_per_sm = -1;
   if (blocks_per_sm < 0) {
-    cudaError_t e = cudaFuncSetAttribute(fill_fused_kernel<Sh, Ms>,
+    cudaError_t e = cudaFuncSetAttribute(fill_fused_kernel<Sh, Ms, GEO>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fill_fused_kernel<Sh, Ms>, Sh::THREADS, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fill_fused_kernel<Sh, Ms, GEO>, Sh::THREADS,
+                                                      smem);
     if (e != cudaSuccess) return e;
     if (b < 1) return cudaErrorInvalidConfiguration;
     blocks_per_sm = b;
@@ -504,7 +515,7 @@ cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_
   const int64_t resident = static_cast<int64_t>(blocks_per_sm) * num_sms;
   const int64_t grid = Sh::PERSIST ? std::min<int64_t>(p.c.n_units, resident) : p.c.n_units;
   p.prefetch_stride = resident;
-  fill_fused_kernel<Sh, Ms><<<static_cast<unsigned>(grid), Sh::THREADS, smem, st>>>(p);
+  fill_fused_kernel<Sh, Ms, GEO><<<static_cast<unsigned>(grid), Sh::THREADS, smem, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -512,13 +523,14 @@ struct FusedEntry {
   int order[3], nq[3], S;
   int kinds[kMaxTerms][3];
   fused_fn launch;
+  fused_fn launch_geo;  // coupling factors from geometry records (nullptr: not compiled)
   v2_pack_fn cpack;
   mv2_pack_fn mpack;
   v2_pack_fn mma_pack;
   const char* desc;
 };
 
-template <class Sh, class Ms>
+template <class Sh, class Ms, bool WITH_GEO = false>
 FusedEntry make_fused() {
   FusedEntry r{};
   for (int d = 0; d < 3; ++d) {
@@ -529,6 +541,8 @@ FusedEntry make_fused() {
   for (int s = 0; s < Sh::S; ++s)
     for (int d = 0; d < 3; ++d) r.kinds[s][d] = Sh::kind(s, d);
   r.launch = &launch_fused<Sh, Ms>;
+  r.launch_geo = nullptr;
+  if constexpr (WITH_GEO) r.launch_geo = &launch_fused<Sh, Ms, true>;
   r.cpack = &pack_v2<Sh>;
   r.mpack = &pack_mv2<Ms>;
   r.mma_pack = &pack_mma<Sh>;
@@ -545,9 +559,10 @@ const std::vector<FusedEntry>& fused_registry() {
   static const std::vector<FusedEntry> reg = {
       make_fused<Shape<4, 4, 4, 4, 4, 4, 256, 2, 4, 1, kPPP>,
                  MShape<4, 4, 4, 8, 8, 8, 256, kPPP>>(),                              // C1
-      // C2: 0 banded (default), 1 paired stores, 2 parity split, 3 DMMA
+      // C2: 0 banded (default, also compiled in geometry mode), 1 paired stores,
+      // 2 parity split, 3 DMMA
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>, true>(),
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 36, 2, kPPP, kDDD>,
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 68, 2, kPPP, kDDD>,
@@ -860,6 +875,14 @@ struct p2s_ctx {
   double* d_ring_alpha[2]{};
   double* d_ring_M[2]{};
   cudaEvent_t ev_h2d[2]{}, ev_comp[2]{}, ev_d2h[2]{};
+  // geometry fill: alpha of a chunk of elements generated into an L2-sized
+  // double buffer on s_geo while the fill consumes the other buffer
+  int64_t geo_chunk = 0;
+  bool geo_fused = false;  // P2S_GEO_FUSED=1: coupling factors computed inside the fused
+                           // kernel (compiled for C2) instead of the L2 double buffer
+  double* d_geo_alpha[2]{};
+  cudaStream_t s_geo = nullptr;
+  cudaEvent_t ev_geo_start = nullptr, ev_ga[2]{}, ev_gf[2]{};
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -1200,6 +1223,7 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
       P2S_CUDA(cudaMemcpy(c->d_amma_fused, A.data(), sizeof(double) * A.size(), cudaMemcpyHostToDevice));
     }
   }
+  if (const char* v = std::getenv("P2S_GEO_FUSED")) c->geo_fused = v[0] == '1';
   c->mv2 = find_mv2(*spec);
   if (c->mv2) c->mv2_packed = c->mv2->pack(c->phi);
   if (v2e) {
@@ -1302,6 +1326,13 @@ void p2s_destroy(p2s_ctx* c) {
     if (c->lpack.ev_u[b]) cudaEventDestroy(c->lpack.ev_u[b]);
   }
   if (c->d_amma_fused) cudaFree(c->d_amma_fused);
+  for (int b = 0; b < 2; ++b) {
+    if (c->d_geo_alpha[b]) cudaFree(c->d_geo_alpha[b]);
+    if (c->ev_ga[b]) cudaEventDestroy(c->ev_ga[b]);
+    if (c->ev_gf[b]) cudaEventDestroy(c->ev_gf[b]);
+  }
+  if (c->ev_geo_start) cudaEventDestroy(c->ev_geo_start);
+  if (c->s_geo) cudaStreamDestroy(c->s_geo);
   if (c->d_amma_v2) cudaFree(c->d_amma_v2);
   for (int i = 0; i < 2; ++i) {
     if (c->d_ring_alpha[i]) cudaFree(c->d_ring_alpha[i]);
@@ -1458,6 +1489,82 @@ p2s_status p2s_alpha_generate(p2s_ctx* c, int kind, double lo, double hi, uint64
   cudaError_t err = launch_alpha(d_alpha, xs, c->pb.nq, c->pb.n_comp, c->pb.n_terms, kind, lo, hi,
                                  seed, e0, n, c->sz.alpha_per_elem, static_cast<cudaStream_t>(stream));
   if (err != cudaSuccess) return cuda_fail(err, "alpha_kernel launch");
+  return P2S_OK;
+}
+
+p2s_status p2s_geometry_generate(p2s_ctx* c, double lo, double hi, uint64_t seed, int64_t e0, int64_t n,
+                                 double* d_geom, void* stream) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (n < 0 || (n > 0 && !d_geom)) return fail(P2S_INVALID_ARG, "p2s_geometry_generate: bad buffer");
+  P2S_CUDA(cudaSetDevice(c->device));
+  cudaError_t err = launch_geometry(d_geom, lo, hi, seed, e0, n, static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "geometry_kernel launch");
+  return P2S_OK;
+}
+
+p2s_status p2s_alpha_from_geometry(p2s_ctx* c, const double* d_geom, int64_t n, double* d_alpha,
+                                   void* stream) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (n < 0 || (n > 0 && (!d_geom || !d_alpha)))
+    return fail(P2S_INVALID_ARG, "p2s_alpha_from_geometry: bad buffer");
+  P2S_CUDA(cudaSetDevice(c->device));
+  const double* xs[3] = {c->d_x[0], c->d_x[1], c->d_x[2]};
+  cudaError_t err = launch_alpha_geometry_fast(d_alpha, d_geom, xs, c->pb.nq, c->pb.n_comp, c->pb.n_terms,
+                                               n, c->sz.alpha_per_elem, static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "alpha_geometry_kernel launch");
+  return P2S_OK;
+}
+
+p2s_status p2s_fill_geometry(p2s_ctx* c, const double* d_geom, double* d_M, int64_t ld_M, int64_t n,
+                             void* stream) {
+  if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
+  if (n < 0 || ld_M < c->sz.n_tot) return fail(P2S_INVALID_ARG, "p2s_fill_geometry: bad sizes");
+  if (n == 0) return P2S_OK;
+  if (!d_geom || !d_M) return fail(P2S_INVALID_ARG, "p2s_fill_geometry: null buffer");
+  P2S_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (c->fused && c->fused->launch_geo && c->geo_fused) {
+    // one kernel: the moment phase computes the coupling factors from the records
+    std::vector<double> mp = c->fused_mpack;
+    for (int d = 0; d < 3; ++d) mp.insert(mp.end(), c->x[d].begin(), c->x[d].end());
+    cudaError_t err = c->fused->launch_geo(d_geom, d_M, ld_M, c->sz.n_tot, n, c->pb.n_comp, c->sz.n_pairs,
+                                           c->pb.order[0] * c->pb.order[1] * c->pb.order[2],
+                                           c->fused_cpack, mp, c->d_amma_fused, st, c->num_sms);
+    if (err != cudaSuccess) return cuda_fail(err, "fill_fused_kernel (geometry) launch");
+    return P2S_OK;
+  }
+  if (!c->s_geo) {  // lazily: two alpha buffers of ~48 MB (L2), a stream, events
+    const int64_t per = c->sz.alpha_per_elem * 8;
+    int64_t mb = 48;
+    if (const char* v = std::getenv("P2S_GEO_CHUNK_MB")) mb = std::max(1, std::atoi(v));
+    c->geo_chunk = std::max<int64_t>(1, (mb << 20) / per);
+    for (int b = 0; b < 2; ++b) {
+      P2S_CUDA(cudaMalloc(&c->d_geo_alpha[b], static_cast<size_t>(per * c->geo_chunk)));
+      P2S_CUDA(cudaEventCreateWithFlags(&c->ev_ga[b], cudaEventDisableTiming));
+      P2S_CUDA(cudaEventCreateWithFlags(&c->ev_gf[b], cudaEventDisableTiming));
+    }
+    P2S_CUDA(cudaEventCreateWithFlags(&c->ev_geo_start, cudaEventDisableTiming));
+    P2S_CUDA(cudaStreamCreateWithFlags(&c->s_geo, cudaStreamNonBlocking));
+  }
+  const double* xs[3] = {c->d_x[0], c->d_x[1], c->d_x[2]};
+  const int64_t mstride = static_cast<int64_t>(c->sz.n_tot) * ld_M;
+  P2S_CUDA(cudaEventRecord(c->ev_geo_start, st));
+  P2S_CUDA(cudaStreamWaitEvent(c->s_geo, c->ev_geo_start, 0));
+  int64_t i = 0;
+  for (int64_t e0 = 0; e0 < n; e0 += c->geo_chunk, ++i) {
+    const int64_t cnt = std::min(c->geo_chunk, n - e0);
+    const int b = static_cast<int>(i % 2);
+    if (i >= 2) P2S_CUDA(cudaStreamWaitEvent(c->s_geo, c->ev_gf[b], 0));  // buffer b free
+    cudaError_t err = launch_alpha_geometry_fast(c->d_geo_alpha[b], d_geom + e0 * 28, xs, c->pb.nq,
+                                                 c->pb.n_comp, c->pb.n_terms, cnt, c->sz.alpha_per_elem,
+                                                 c->s_geo);
+    if (err != cudaSuccess) return cuda_fail(err, "alpha_geometry_kernel launch");
+    P2S_CUDA(cudaEventRecord(c->ev_ga[b], c->s_geo));
+    P2S_CUDA(cudaStreamWaitEvent(st, c->ev_ga[b], 0));
+    const p2s_status s2 = run_fill(c, c->d_geo_alpha[b], d_M + e0 * mstride, ld_M, cnt, st);
+    if (s2 != P2S_OK) return s2;
+    P2S_CUDA(cudaEventRecord(c->ev_gf[b], st));
+  }
   return P2S_OK;
 }
 

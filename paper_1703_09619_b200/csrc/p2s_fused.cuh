@@ -15,6 +15,8 @@ template <class Sh, class Ms>
 struct FusedParams {
   V2Params<Sh> c;      // contraction part (c.I unused)
   const double* alpha;
+  const double* geom;  // GEO kernels: element geometry records (28 doubles each)
+  double xq[Ms::Q(0) + Ms::Q(1) + Ms::Q(2)];  // GL nodes u, v, w (GEO kernels)
   int64_t prefetch_stride;  // resident CTAs on the GPU (non-persistent launch)
   double tab[Ms::TALL];
 };
@@ -28,7 +30,9 @@ struct FusedLayout {
   static constexpr size_t SMEM = sizeof(double) * (size_t)(Sh::MPP + WORK + mma_smem_dbl<Sh>());
 };
 
-template <class Sh, class Ms>
+// GEO: the moment phase computes the coupling factors from the element's
+// geometry record (p2s_fill_geometry) instead of reading alpha from HBM.
+template <class Sh, class Ms, bool GEO = false>
 __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     fill_fused_kernel(const __grid_constant__ FusedParams<Sh, Ms> p) {
   extern __shared__ __align__(16) double sm[];
@@ -44,6 +48,13 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     const int pair = static_cast<int>(unit - e * p.c.P);
     const int gci = pair / p.c.nc, gcj = pair - gci * p.c.nc;
     const double* a = p.alpha + unit * (static_cast<int64_t>(Ms::S) * slab);
+    if constexpr (GEO) {
+      __shared__ GeoUnit geo;
+      geo_unit_setup(p.geom + e * 28, gci, gcj, &geo);
+      __syncthreads();
+      static_assert(!Ms::WFIRST, "geometry mode uses the u-first pass order");
+      moments_all_terms<Ms, Sh::THREADS, true>(nullptr, p.tab, Abuf, Ibuf, &geo, p.xq);
+    } else {
     // warm L2 with alpha `stride` units ahead while this unit is processed
     if constexpr ((Ms::S * slab) % 2 == 0)  // 16-B granularity of the bulk prefetch
       if (threadIdx.x == 0 && unit + stride < p.c.n_units)
@@ -52,6 +63,7 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
       moments_all_terms_wfirst<Ms, Sh::THREADS>(a, p.tab, Abuf, Ibuf);
     else
       moments_all_terms<Ms, Sh::THREADS>(a, p.tab, Abuf, Ibuf);
+    }
     double* Mbase =
         p.c.M + e * p.c.mat_stride + static_cast<int64_t>(gci * p.c.Nt) * p.c.ldM + gcj * p.c.Nt;
     v2_unit<Sh>(p.c, Ibuf, Abuf, Bbuf, Mbase, []() {}, mm);

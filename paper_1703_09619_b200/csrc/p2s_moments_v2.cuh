@@ -187,15 +187,118 @@ __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const
   __syncthreads();
 }
 
+// Element geometry for coupling factors computed in place of loaded alpha
+// (p2s_fill_geometry): the trilinear map in polynomial form (A[m][c], monomial
+// bit d = factor r_d), the material (a, b, c, phi) and the unit's component pair.
+struct GeoUnit {
+  double A[8][3];
+  double mat[4];
+  int gi, gj;
+};
+
+// Per CTA: record (include/p2s_b200.h layout) -> GeoUnit in shared memory.
+__device__ __forceinline__ void geo_unit_setup(const double* __restrict__ rec, int gi, int gj, GeoUnit* g) {
+  if (threadIdx.x < 24) {
+    const int m = threadIdx.x / 3, comp = threadIdx.x % 3;
+    double acc = 0.0;
+    for (int c = 0; c < 8; ++c) {
+      double sgn = 1.0;
+      for (int d = 0; d < 3; ++d)
+        if ((m >> d) & 1) sgn *= ((c >> d) & 1) ? 1.0 : -1.0;
+      acc += sgn * __ldg(rec + c * 3 + comp);
+    }
+    g->A[m][comp] = 0.125 * acc;
+  } else if (threadIdx.x < 28) {
+    g->mat[threadIdx.x - 24] = __ldg(rec + threadIdx.x);
+  } else if (threadIdx.x == 28) {
+    g->gi = gi;
+    g->gj = gj;
+  }
+}
+
+// Coupling factors of one row (v, w) at the u nodes xu[], folded like a loaded
+// alpha row: even terms alpha_mat detJ (J^T J)^-1_{gi gj}, odd terms
+// alpha_mat (J^T J)_{gi gj} / detJ.  Along a row the Jacobian is linear in u.
+template <int S, int QU>
+__device__ __forceinline__ void geo_row(const GeoUnit& g, double v, double w, const double* xu,
+                                        double (&ev)[S][QU / 2 > 0 ? QU / 2 : 1],
+                                        double (&od)[S][QU / 2 > 0 ? QU / 2 : 1], double (&mid)[S]) {
+  constexpr int Hf = QU / 2;
+  double J0[3], J1a[3], J1b[3], J2a[3], J2b[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    J0[c] = g.A[1][c] + v * g.A[3][c] + w * g.A[5][c] + v * w * g.A[7][c];
+    J1a[c] = g.A[2][c] + w * g.A[6][c];
+    J1b[c] = g.A[3][c] + w * g.A[7][c];
+    J2a[c] = g.A[4][c] + v * g.A[6][c];
+    J2b[c] = g.A[5][c] + v * g.A[7][c];
+  }
+  const double sarg = g.mat[1] * v + g.mat[2] * w + g.mat[3];
+  // pair code 3 gi + gj -> (G / cofactor) entry; G symmetric
+  const int pc = g.gi * 3 + g.gj;
+  auto at = [&](double u, double& mass, double& curl) {
+    double J[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      J[c][0] = J0[c];
+      J[c][1] = J1a[c] + u * J1b[c];
+      J[c][2] = J2a[c] + u * J2b[c];
+    }
+    const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                       J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                       J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    const double G00 = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
+    const double G11 = J[0][1] * J[0][1] + J[1][1] * J[1][1] + J[2][1] * J[2][1];
+    const double G22 = J[0][2] * J[0][2] + J[1][2] * J[1][2] + J[2][2] * J[2][2];
+    const double G01 = J[0][0] * J[0][1] + J[1][0] * J[1][1] + J[2][0] * J[2][1];
+    const double G02 = J[0][0] * J[0][2] + J[1][0] * J[1][2] + J[2][0] * J[2][2];
+    const double G12 = J[0][1] * J[0][2] + J[1][1] * J[1][2] + J[2][1] * J[2][2];
+    double gsel, csel;
+    switch (pc) {  // warp-uniform
+      case 0: gsel = G00; csel = G11 * G22 - G12 * G12; break;
+      case 4: gsel = G11; csel = G00 * G22 - G02 * G02; break;
+      case 8: gsel = G22; csel = G00 * G11 - G01 * G01; break;
+      case 1: case 3: gsel = G01; csel = G02 * G12 - G01 * G22; break;
+      case 2: case 6: gsel = G02; csel = G01 * G12 - G02 * G11; break;
+      default: gsel = G12; csel = G02 * G01 - G00 * G12; break;
+    }
+    const double am = (1.0 + 0.3 * sin(g.mat[0] * u + sarg)) / det;
+    mass = am * csel;  // alpha_mat detJ cof(G) / det(G), det(G) = detJ^2
+    curl = am * gsel;
+  };
+#pragma unroll
+  for (int h = 0; h < Hf; ++h) {
+    double m1, c1, m2, c2;
+    at(xu[h], m1, c1);
+    at(xu[QU - 1 - h], m2, c2);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      ev[s][h] = (s % 2 == 0) ? m1 + m2 : c1 + c2;
+      od[s][h] = (s % 2 == 0) ? m1 - m2 : c1 - c2;
+    }
+  }
+  if constexpr ((QU & 1) != 0) {
+    double m, c;
+    at(xu[Hf], m, c);
+#pragma unroll
+    for (int s = 0; s < S; ++s) mid[s] = (s % 2 == 0) ? m : c;
+  } else {
+#pragma unroll
+    for (int s = 0; s < S; ++s) mid[s] = 0.0;
+  }
+}
+
 // All terms of one (element, pair) at once: the kernel polynomials of every
 // term are the same Legendre P_k (only the count K differs), so one half-table
 // row (loaded once per thread) feeds every term that uses it, and the three
 // passes need three barriers for all terms.  alpha_s slabs are consecutive
 // (a + s * slab); Iout + moff(s) receives I_s.  Requires every term's tables
 // to be row prefixes of term kmax_term(d)'s table (true for Legendre kernels).
-template <class Ms, int NTHR>
+template <class Ms, int NTHR, bool GEO = false>
 __device__ __forceinline__ void moments_all_terms(const double* __restrict__ a, const double* tab,
-                                                  double* scratch, double* Iout) {
+                                                  double* scratch, double* Iout,
+                                                  const GeoUnit* geo = nullptr,
+                                                  const double* xq = nullptr) {
   constexpr int S = Ms::S;
   constexpr int QU = Ms::Q(0), QV = Ms::Q(1), QW = Ms::Q(2);
   constexpr int S2 = Ms::S2, S3 = Ms::S3;
@@ -208,6 +311,9 @@ __device__ __forceinline__ void moments_all_terms(const double* __restrict__ a, 
     const int q3 = r / QV, q2 = r - (r / QV) * QV;
     constexpr int Hf = QU / 2, H = (QU + 1) / 2;
     double ev[S][Hf > 0 ? Hf : 1], od[S][Hf > 0 ? Hf : 1], mid[S];
+    if constexpr (GEO) {  // coupling factors from the element geometry (xq = u, v, w nodes)
+      geo_row<S, QU>(*geo, xq[QU + q2], xq[QU + QV + q3], xq, ev, od, mid);
+    } else
     static_for<0, S>([&](auto sc) {
       constexpr int s = decltype(sc)::value;
       double x[QU];
