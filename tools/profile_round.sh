@@ -1,0 +1,21 @@
+#!/bin/bash
+# Round evidence on one B200 (run under gpurun from the repo root):
+#   1. default bench line (driver command) + wall time, 2. reference arm,
+#   3. ncu launch list of the bench command, 4. ncu --set full (raw CSV) of the
+#   dominant kernel per config.  Outputs in gpurun_out/; copy summaries to profiles/.
+set -u
+mkdir -p gpurun_out
+R=${ROUND:-r1}
+t0=$(date +%s.%N); python bench.py > gpurun_out/${R}_bench_default.json 2> gpurun_out/${R}_bench_default.err; t1=$(date +%s.%N); echo "bench.py default wall: $(echo "$t1 - $t0" | bc) s" >> gpurun_out/${R}_bench_default.err
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${R}_bench_reference.json 2> gpurun_out/${R}_bench_reference.err
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 \
+    --csv --log-file gpurun_out/${R}_launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+    --no-e2e > gpurun_out/${R}_launches_c2.log 2>&1
+for c in c2 c3 c4; do
+  ncu --set full --clock-control none -k regex:fill_fused -s 3 -c 1 --csv --page raw python bench.py --config $c \
+      --steps 1 --warmup 3 --n-elem 2048 --no-cpu-baseline --no-e2e --no-ablation \
+      > gpurun_out/${R}_ncu_${c}_fused_raw.csv 2> /dev/null
+done
+ncu --set full --clock-control none -k regex:large_u_kernel -s 2 -c 1 --csv --page raw python bench.py --config c5 \
+    --steps 1 --warmup 1 --n-elem 32 --no-cpu-baseline --no-e2e --no-ablation > gpurun_out/${R}_ncu_c5_u_raw.csv 2> /dev/null
+ls -la gpurun_out/${R}_*
