@@ -161,6 +161,8 @@ def _check(status: int):
 
 
 def make_problem(n_comp, order, kinds, nq, basis=BASIS_MODAL) -> Problem:
+    if not 1 <= len(kinds) <= MAX_TERMS:  # the C struct holds MAX_TERMS terms
+        raise InvalidArgument(INVALID_ARG, f"n_terms must be 1..{MAX_TERMS}")
     pb = Problem()
     pb.basis = basis
     pb.n_comp = n_comp

@@ -1,0 +1,130 @@
+"""Edge cases of every entry point (the reference's own tests cover empty
+batches, argument validation and thread-count independence):
+empty batches are no-ops that touch nothing, ragged batch sizes that straddle
+the internal chunkings, grids beyond 65535 CTAs, and the argument limits."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_1703_09619_b200 import capi
+from paper_1703_09619_b200.capi import BASIS_CONFORMING, DD, PP
+from paper_1703_09619_b200.configs import CONFIGS
+
+from helpers import blocks_close, oracle_for
+
+pytestmark = pytest.mark.gpu
+
+
+def _nan(*shape):
+    return torch.full(shape, float("nan"), dtype=torch.float64, device="cuda")
+
+
+def test_empty_batches_touch_nothing():
+    cfg = CONFIGS["c2"]
+    ctx = capi.Context(**cfg.problem())
+    sp = torch.cuda.current_stream().cuda_stream
+    a = _nan(1, ctx.alpha_per_elem)
+    I = _nan(1, ctx.moments_per_elem)
+    M = _nan(1, ctx.n_tot, ctx.n_tot)
+    ctx.fill(a, M, ctx.n_tot, 0, sp)
+    ctx.moments(a, I, 0, sp)
+    ctx.contract(I, M, ctx.n_tot, 0, sp)
+    ctx.alpha_generate(O.ALPHA_JACOBIAN, 0.5, 3.0, 1, 0, 0, a, sp)
+    ctx.fill_geometry(a, M, ctx.n_tot, 0, sp)
+    ha = np.full((1, ctx.alpha_per_elem), np.nan)
+    hM = np.full((1, ctx.n_tot, ctx.n_tot), np.nan)
+    ctx.fill_host(ha, hM, ctx.n_tot, 0)
+    d = capi.DirectContext(**cfg.problem())
+    d.fill(a, M, ctx.n_tot, 0, sp)
+    c2d = capi.Cheb2dContext(3, 3, 8)
+    c2d.kernel_tables(a, I, 0)
+    c2d.assemble(I, M, 0)
+    torch.cuda.synchronize()
+    assert torch.isnan(M).all() and torch.isnan(I).all() and torch.isnan(a).all()
+    assert np.isnan(hM).all()
+
+
+@pytest.mark.parametrize("path_env", [{}, {"P2S_NO_FUSED": "1"}, {"P2S_FORCE_GENERIC": "1",
+                                                                   "P2S_NO_FUSED": "1"}])
+@pytest.mark.parametrize("n", [1, 7, 33])
+def test_ragged_batches_match_oracle(n, path_env, monkeypatch):
+    for k, v in path_env.items():
+        monkeypatch.setenv(k, v)
+    pb = (3, (3, 3, 3), [PP, DD], (6, 6, 6))
+    ctx = capi.Context(*pb)
+    o = oracle_for(*pb)
+    alpha = o.alpha(O.ALPHA_JACOBIAN, 0.5, 3.0, 13, 0, n)
+    M = _nan(n, ctx.n_tot, ctx.n_tot)
+    ctx.fill(torch.from_numpy(alpha).cuda(), M, ctx.n_tot, n, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    Mo = o.fill(alpha, threads=8)
+    for e in range(n):
+        ok, msg, _ = blocks_close(M[e].cpu().numpy(), Mo[e], 3, 27)
+        assert ok, (e, msg)
+
+
+def test_host_path_across_ring_chunks():
+    """p2s_fill_host pipelines 256 MB chunks through a 2-slot ring: 80 C2 elements
+    straddle a chunk boundary (76 per chunk)."""
+    cfg = CONFIGS["c2"]
+    ctx = capi.Context(**cfg.problem())
+    n = 80
+    o = oracle_for(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
+    alpha = o.alpha(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 3, 0, n)
+    hM = np.full((n, ctx.n_tot, ctx.n_tot), np.nan)
+    ctx.fill_host(alpha, hM, ctx.n_tot, n)
+    d = torch.from_numpy(alpha).cuda()
+    M = _nan(n, ctx.n_tot, ctx.n_tot)
+    ctx.fill(d, M, ctx.n_tot, n, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(hM, M.cpu().numpy())
+    Mo = o.fill(alpha[[0, 75, 76, 79]], threads=8)
+    for i, e in enumerate([0, 75, 76, 79]):
+        ok, msg, _ = blocks_close(hM[e], Mo[i], cfg.n_comp, 216)
+        assert ok, (e, msg)
+
+
+@pytest.mark.parametrize("env", [{}, {"P2S_NO_FUSED": "1"}])
+def test_grid_beyond_65535_ctas(env, monkeypatch):
+    """70 000 C1 elements: one CTA per (element, pair) unit in the fused kernel,
+    70 000 moment CTAs in the two-stage path."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = CONFIGS["c1"]
+    ctx = capi.Context(**cfg.problem())
+    n = 70000
+    sp = torch.cuda.current_stream().cuda_stream
+    a = torch.empty((n, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")
+    ctx.alpha_generate(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 5, 0, n, a, sp)
+    M = _nan(n, ctx.n_tot, ctx.n_tot)
+    ctx.fill(a, M, ctx.n_tot, n, sp)
+    torch.cuda.synchronize()
+    assert not torch.isnan(M).any()
+    o = oracle_for(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
+    pick = [0, 65535, 69999]
+    Mo = o.fill(a[pick].cpu().numpy(), threads=4)
+    for i, e in enumerate(pick):
+        ok, msg, _ = blocks_close(M[e].cpu().numpy(), Mo[i], 1, 64)
+        assert ok, (e, msg)
+
+
+@pytest.mark.parametrize("bad", [
+    dict(n_comp=4), dict(n_comp=0), dict(order=(33, 3, 3)), dict(nq=(65, 4, 4)), dict(nq=(4, 0, 4)),
+    dict(kinds=[4]), dict(kinds=[PP, DD, PP, DD, PP]), dict(basis=2),
+    dict(basis=BASIS_CONFORMING, order=(1, 2, 2)),
+])
+def test_argument_limits(bad):
+    args = dict(n_comp=1, order=(3, 3, 3), kinds=[PP], nq=(4, 4, 4), basis=0)
+    args.update(bad)
+    with pytest.raises(capi.InvalidArgument):
+        capi.Context(args["n_comp"], args["order"], args["kinds"], args["nq"], basis=args["basis"])
+    with pytest.raises(capi.InvalidArgument):
+        capi.DirectContext(args["n_comp"], args["order"], args["kinds"], args["nq"], basis=args["basis"])
+
+
+def test_unsupported_orders_report_unsupported_shape():
+    # valid problem, no compiled contraction for N_u = 11 with these u-kinds
+    assert not capi.shape_supported(1, (11, 3, 3), [PP], (12, 4, 4))
+    with pytest.raises(capi.UnsupportedShape):
+        capi.Context(1, (11, 3, 3), [PP], (12, 4, 4))
