@@ -470,16 +470,17 @@ using fused_fn = cudaError_t (*)(const double*, double*, int64_t, int64_t, int64
                                  const std::vector<double>&, const std::vector<double>&,
                                  const double*, cudaStream_t, int);
 
-// GEO: `alpha` is the geometry records and the kernel computes the coupling
-// factors itself (xq = the GL nodes u, v, w in mpack's tail, see pack_fused_geo)
-template <class Sh, class Ms, bool GEO = false>
+// GEO > 0: `alpha` is the geometry records and the kernel computes the coupling
+// factors itself (xq = the GL nodes u, v, w appended to mpack); GEO == 2 launches
+// one thread-block cluster of P CTAs per element (non-portable size for P = 9)
+template <class Sh, class Ms, int GEO = 0>
 cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_tot, int64_t n_elem,
                          int nc, int P, int Nt, const std::vector<double>& cpack,
                          const std::vector<double>& mpack, const double* amma, cudaStream_t st,
                          int num_sms) {
   FusedParams<Sh, Ms> p;
   p.geom = GEO ? alpha : nullptr;
-  if constexpr (GEO)
+  if constexpr (GEO != 0)
     std::memcpy(p.xq, mpack.data() + Ms::TALL, sizeof(double) * (Ms::Q(0) + Ms::Q(1) + Ms::Q(2)));
   p.c.I = nullptr;
   p.c.M = M;
@@ -499,12 +500,17 @@ cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_
   p.prefetch_stride = 0;
   std::memcpy(p.tab, mpack.data(), sizeof(double) * Ms::TALL);
   if (p.c.n_units == 0) return cudaSuccess;
-  constexpr size_t smem = FusedLayout<Sh, Ms>::SMEM;
+  constexpr size_t smem = FusedLayout<Sh, Ms, GEO>::SMEM;
   static int blocks_per_sm = -1;
   if (blocks_per_sm < 0) {
     cudaError_t e = cudaFuncSetAttribute(fill_fused_kernel<Sh, Ms, GEO>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    if constexpr (GEO == 2) {
+      e = cudaFuncSetAttribute(fill_fused_kernel<Sh, Ms, GEO>,
+                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
     int b = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fill_fused_kernel<Sh, Ms, GEO>, Sh::THREADS,
                                                       smem);
@@ -515,6 +521,21 @@ cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_
   const int64_t resident = static_cast<int64_t>(blocks_per_sm) * num_sms;
   const int64_t grid = Sh::PERSIST ? std::min<int64_t>(p.c.n_units, resident) : p.c.n_units;
   p.prefetch_stride = resident;
+  if constexpr (GEO == 2) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(p.c.n_units));
+    cfg.blockDim = dim3(Sh::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(P);  // one element per cluster
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fill_fused_kernel<Sh, Ms, GEO>, p);
+  }
   fill_fused_kernel<Sh, Ms, GEO><<<static_cast<unsigned>(grid), Sh::THREADS, smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -523,7 +544,8 @@ struct FusedEntry {
   int order[3], nq[3], S;
   int kinds[kMaxTerms][3];
   fused_fn launch;
-  fused_fn launch_geo;  // coupling factors from geometry records (nullptr: not compiled)
+  fused_fn launch_geo;          // coupling factors from geometry records, per unit
+  fused_fn launch_geo_cluster;  // ... shared per element through a cluster (DSMEM)
   v2_pack_fn cpack;
   mv2_pack_fn mpack;
   v2_pack_fn mma_pack;
@@ -541,8 +563,11 @@ FusedEntry make_fused() {
   for (int s = 0; s < Sh::S; ++s)
     for (int d = 0; d < 3; ++d) r.kinds[s][d] = Sh::kind(s, d);
   r.launch = &launch_fused<Sh, Ms>;
-  r.launch_geo = nullptr;
-  if constexpr (WITH_GEO) r.launch_geo = &launch_fused<Sh, Ms, true>;
+  r.launch_geo = r.launch_geo_cluster = nullptr;
+  if constexpr (WITH_GEO) {
+    r.launch_geo = &launch_fused<Sh, Ms, 1>;
+    r.launch_geo_cluster = &launch_fused<Sh, Ms, 2>;
+  }
   r.cpack = &pack_v2<Sh>;
   r.mpack = &pack_mv2<Ms>;
   r.mma_pack = &pack_mma<Sh>;
@@ -878,8 +903,9 @@ struct p2s_ctx {
   // geometry fill: alpha of a chunk of elements generated into an L2-sized
   // double buffer on s_geo while the fill consumes the other buffer
   int64_t geo_chunk = 0;
-  bool geo_fused = false;  // P2S_GEO_FUSED=1: coupling factors computed inside the fused
-                           // kernel (compiled for C2) instead of the L2 double buffer
+  int geo_mode = 0;  // P2S_GEO_MODE: 0 alpha via the L2 double buffer (default, fastest);
+                     // 1 per-unit recomputation inside the fused kernel; 2 one cluster per
+                     // element sharing the per-point geometry through DSMEM
   double* d_geo_alpha[2]{};
   cudaStream_t s_geo = nullptr;
   cudaEvent_t ev_geo_start = nullptr, ev_ga[2]{}, ev_gf[2]{};
@@ -1223,7 +1249,7 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
       P2S_CUDA(cudaMemcpy(c->d_amma_fused, A.data(), sizeof(double) * A.size(), cudaMemcpyHostToDevice));
     }
   }
-  if (const char* v = std::getenv("P2S_GEO_FUSED")) c->geo_fused = v[0] == '1';
+  if (const char* v = std::getenv("P2S_GEO_MODE")) c->geo_mode = std::atoi(v);
   c->mv2 = find_mv2(*spec);
   if (c->mv2) c->mv2_packed = c->mv2->pack(c->phi);
   if (v2e) {
@@ -1523,13 +1549,17 @@ p2s_status p2s_fill_geometry(p2s_ctx* c, const double* d_geom, double* d_M, int6
   if (!d_geom || !d_M) return fail(P2S_INVALID_ARG, "p2s_fill_geometry: null buffer");
   P2S_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (c->fused && c->fused->launch_geo && c->geo_fused) {
-    // one kernel: the moment phase computes the coupling factors from the records
+  const fused_fn geo_launch = !c->fused              ? nullptr
+                             : c->geo_mode == 2     ? c->fused->launch_geo_cluster
+                             : c->geo_mode == 1     ? c->fused->launch_geo
+                                                    : nullptr;
+  if (geo_launch) {
+    // one kernel: the moment phase gets the coupling factors from the records
     std::vector<double> mp = c->fused_mpack;
     for (int d = 0; d < 3; ++d) mp.insert(mp.end(), c->x[d].begin(), c->x[d].end());
-    cudaError_t err = c->fused->launch_geo(d_geom, d_M, ld_M, c->sz.n_tot, n, c->pb.n_comp, c->sz.n_pairs,
-                                           c->pb.order[0] * c->pb.order[1] * c->pb.order[2],
-                                           c->fused_cpack, mp, c->d_amma_fused, st, c->num_sms);
+    cudaError_t err = geo_launch(d_geom, d_M, ld_M, c->sz.n_tot, n, c->pb.n_comp, c->sz.n_pairs,
+                                 c->pb.order[0] * c->pb.order[1] * c->pb.order[2], c->fused_cpack, mp,
+                                 c->d_amma_fused, st, c->num_sms);
     if (err != cudaSuccess) return cuda_fail(err, "fill_fused_kernel (geometry) launch");
     return P2S_OK;
   }

@@ -294,7 +294,9 @@ __device__ __forceinline__ void geo_row(const GeoUnit& g, double v, double w, co
 // passes need three barriers for all terms.  alpha_s slabs are consecutive
 // (a + s * slab); Iout + moff(s) receives I_s.  Requires every term's tables
 // to be row prefixes of term kmax_term(d)'s table (true for Legendre kernels).
-template <class Ms, int NTHR, bool GEO = false>
+// SRC: 0 alpha in global memory (read-only path), 1 coupling factors computed
+// from the unit's geometry (geo, xq), 2 alpha in shared memory (cluster mode)
+template <class Ms, int NTHR, int SRC = 0>
 __device__ __forceinline__ void moments_all_terms(const double* __restrict__ a, const double* tab,
                                                   double* scratch, double* Iout,
                                                   const GeoUnit* geo = nullptr,
@@ -311,7 +313,7 @@ __device__ __forceinline__ void moments_all_terms(const double* __restrict__ a, 
     const int q3 = r / QV, q2 = r - (r / QV) * QV;
     constexpr int Hf = QU / 2, H = (QU + 1) / 2;
     double ev[S][Hf > 0 ? Hf : 1], od[S][Hf > 0 ? Hf : 1], mid[S];
-    if constexpr (GEO) {  // coupling factors from the element geometry (xq = u, v, w nodes)
+    if constexpr (SRC == 1) {  // coupling factors from the element geometry (xq = u, v, w nodes)
       geo_row<S, QU>(*geo, xq[QU + q2], xq[QU + QV + q3], xq, ev, od, mid);
     } else
     static_for<0, S>([&](auto sc) {
@@ -321,13 +323,14 @@ __device__ __forceinline__ void moments_all_terms(const double* __restrict__ a, 
       if constexpr ((QU & 1) == 0) {
 #pragma unroll
         for (int q = 0; q < QU / 2; ++q) {
-          const double2 v = __ldg(reinterpret_cast<const double2*>(row) + q);
+          const double2 v = SRC == 2 ? reinterpret_cast<const double2*>(row)[q]
+                                     : __ldg(reinterpret_cast<const double2*>(row) + q);
           x[2 * q] = v.x;
           x[2 * q + 1] = v.y;
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < QU; ++q) x[q] = __ldg(row + q);
+        for (int q = 0; q < QU; ++q) x[q] = SRC == 2 ? row[q] : __ldg(row + q);
       }
 #pragma unroll
       for (int h = 0; h < Hf; ++h) {

@@ -43,13 +43,14 @@ def test_alpha_from_geometry_equals_seeded_jacobian_alpha():
     np.testing.assert_allclose(a1.cpu().numpy(), ah, rtol=1e-13, atol=1e-14)
 
 
-@pytest.mark.parametrize("chunked", [True, False])
-def test_fill_geometry_matches_two_step_fill_and_oracle(chunked, monkeypatch):
-    """Chunked (default): alpha via the L2 double buffer -- bit-identical to
-    p2s_fill(p2s_alpha_from_geometry(...)); fused (P2S_GEO_FUSED=1): the moment
-    phase computes alpha from the records.  Both against the oracle on host alpha."""
-    if not chunked:
-        monkeypatch.setenv("P2S_GEO_FUSED", "1")
+@pytest.mark.parametrize("mode", [2, 1, 0])
+def test_fill_geometry_matches_two_step_fill_and_oracle(mode, monkeypatch):
+    """P2S_GEO_MODE 0 (default): alpha via the L2 double buffer -- bit-identical to
+    p2s_fill(p2s_alpha_from_geometry(...)); 1: each pair's CTA recomputes the
+    geometry; 2: one cluster of 9 CTAs per element shares the per-point geometry
+    through DSMEM.  All against the oracle on host alpha."""
+    monkeypatch.setenv("P2S_GEO_MODE", str(mode))
+    chunked = mode == 0
     cfg, ctx = _ctx("c2")
     assert "fused" in ctx.kernel_path
     n = 150  # > 2 chunks of the internal alpha double buffer
