@@ -14,11 +14,7 @@
 #include <vector>
 
 #include "../../include/p2s_b200.h"
-#include "p2s_contract_v2.cuh"
-#include "p2s_fused.cuh"
-#include "p2s_moments_v2.cuh"
-#include "p2s_kernels.cuh"
-#include "p2s_large.cuh"
+#include "p2s_registry.hpp"
 #include "p2s_tables.hpp"
 
 namespace p2s {
@@ -52,139 +48,9 @@ p2s_status cuda_fail(cudaError_t err, const char* where) {
   } while (0)
 
 using namespace p2s;
+using namespace p2s::reg;
 
-// ------------------------------------------------------------ contraction registry
-
-struct ContractArgs {
-  const double* I;
-  double* M;
-  int64_t ldM, n_tot, n_elem;
-  int nc, P, Nv, Nw, Nt;
-  int S;
-  int Kv[kMaxTerms], Kw[kMaxTerms], kind_v[kMaxTerms], kind_w[kMaxTerms];
-  int64_t mom_per_elem, mom_per_pair, mom_off[kMaxTerms];
-  const double* Cv[kMaxTerms];
-  const double* Cw[kMaxTerms];
-  const double* cu_packed;  // host, Cfg-packed
-};
-
-struct Plan {  // per-context launch geometry of the contraction
-  int G, NG, threads;
-  size_t smem;
-};
-
-using contract_fn = cudaError_t (*)(const ContractArgs&, const Plan&, cudaStream_t);
-
-template <class Cfg>
-cudaError_t launch_contract(const ContractArgs& a, const Plan& pl, cudaStream_t st) {
-  ContractParams<Cfg> p;
-  std::memset(&p, 0, sizeof(p));
-  p.I = a.I;
-  p.M = a.M;
-  p.ldM = a.ldM;
-  p.mat_stride = a.n_tot * a.ldM;
-  p.nc = a.nc;
-  p.P = a.P;
-  p.Nv = a.Nv;
-  p.Nw = a.Nw;
-  p.Nt = a.Nt;
-  p.G = pl.G;
-  p.NG = pl.NG;
-  p.mom_per_elem = a.mom_per_elem;
-  p.mom_per_pair = a.mom_per_pair;
-  p.i_doubles = static_cast<int>(a.mom_per_pair);
-  int ao = 0, co = 0;
-  for (int s = 0; s < Cfg::S; ++s) {
-    p.Kv[s] = a.Kv[s];
-    p.Kw[s] = a.Kw[s];
-    p.kind_v[s] = a.kind_v[s];
-    p.kind_w[s] = a.kind_w[s];
-    p.mom_off[s] = static_cast<int>(a.mom_off[s]);
-    p.a_off[s] = ao;
-    ao += pl.G * Cfg::K(s) * a.Nv * a.Kw[s];
-    p.cv_off[s] = co;
-    co += a.Nv * a.Nv * a.Kv[s];
-    p.cw_off[s] = co;
-    co += a.Nw * a.Nw * a.Kw[s];
-    p.Cv[s] = a.Cv[s];
-    p.Cw[s] = a.Cw[s];
-  }
-  p.a_doubles = (ao + 1) & ~1;
-  p.c_doubles = (co + 1) & ~1;
-  std::memcpy(p.cu, a.cu_packed, sizeof(double) * Cfg::CTOT);
-  const int64_t n_cta = a.n_elem * a.P * pl.NG;
-  p.n_cta = n_cta;
-  if (n_cta == 0) return cudaSuccess;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(contract_kernel<Cfg>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  contract_kernel<Cfg><<<static_cast<unsigned>(n_cta), pl.threads, pl.smem, st>>>(p);
-  return cudaGetLastError();
-}
-
-template <class Cfg>
-std::vector<double> pack_cu(const std::vector<const std::vector<double>*>& dense) {
-  // dense[s] = [NU][NU][K_s]
-  std::vector<double> out(static_cast<size_t>(Cfg::CTOT), 0.0);
-  for (int s = 0; s < Cfg::S; ++s) {
-    const int K = Cfg::K(s), kd = Cfg::kind(s);
-    for (int a = 0; a < Cfg::NU; ++a)
-      for (int b = 0; b < Cfg::NU; ++b) {
-        const int lo = band_lo(kd, a, b), cnt = band_count(kd, a, b);
-        for (int j = 0; j < cnt; ++j)
-          out[static_cast<size_t>(Cfg::coff(s, a, b) + j)] =
-              (*dense[static_cast<size_t>(s)])[(static_cast<size_t>(a) * Cfg::NU + b) * K + lo +
-                                               band_step(kd, a, b) * j];
-      }
-  }
-  return out;
-}
-
-struct RegEntry {
-  int NU, S;
-  int kinds[kMaxTerms];
-  contract_fn launch;
-  std::vector<double> (*pack)(const std::vector<const std::vector<double>*>&);
-  int ktot;
-};
-
-template <int NU, int... KINDS>
-RegEntry make_entry() {
-  using Cfg = UCfg<NU, KINDS...>;
-  RegEntry r{};
-  r.NU = NU;
-  r.S = Cfg::S;
-  const int ks[] = {KINDS...};
-  for (int s = 0; s < Cfg::S; ++s) r.kinds[s] = ks[s];
-  r.launch = &launch_contract<Cfg>;
-  r.pack = &pack_cu<Cfg>;
-  r.ktot = Cfg::KTOT;
-  return r;
-}
-
-// Compiled shapes: (N_u, u-kind of each term).  The v / w orders, kinds,
-// component count and quadrature sizes are runtime parameters.
-const std::vector<RegEntry>& registry() {
-  static const std::vector<RegEntry> reg = {
-      make_entry<1, PP>(),          make_entry<2, PP>(),      make_entry<3, PP>(),
-      make_entry<4, PP>(),          make_entry<5, PP>(),      make_entry<6, PP>(),
-      make_entry<8, PP>(),          make_entry<10, PP>(),
-      make_entry<2, PP, DD>(),      make_entry<3, PP, DD>(),  make_entry<4, PP, DD>(),
-      make_entry<5, PP, DD>(),      make_entry<6, PP, DD>(),  make_entry<8, PP, DD>(),
-      make_entry<10, PP, DD>(),
-      make_entry<3, DD>(),          make_entry<3, DP>(),      make_entry<3, PD>(),
-      make_entry<4, DP, PD>(),      make_entry<3, PP, DP>(),  make_entry<4, PP, DD, DP, PD>(),
-      // conforming basis (kind | kConforming)
-      make_entry<3, PP | kConforming, DD | kConforming>(), make_entry<4, PP | kConforming>(),
-      make_entry<6, PP | kConforming, DD | kConforming>(),
-      make_entry<4, DP | kConforming, PD | kConforming>(),
-  };
-  return reg;
-}
+// ------------------------------------------------------------ registry lookup
 
 const RegEntry* find_entry(const p2s_problem& pb) {
   for (const RegEntry& r : registry()) {
@@ -196,165 +62,6 @@ const RegEntry* find_entry(const p2s_problem& pb) {
   return nullptr;
 }
 
-// ------------------------------------------------------------ shape-specialised registry
-
-struct V2Args {
-  const double* I;
-  double* M;
-  int64_t ldM, n_tot, n_elem, mom_per_elem;
-  int nc, P, Nt;
-  const std::vector<double>* dense[kMaxTerms][3];  // [N][N][K] per term, direction
-  const double* amma;                              // device stage-C A (MMA shapes)
-};
-
-using v2_fn = cudaError_t (*)(const V2Args&, const std::vector<double>&, cudaStream_t, int);
-using v2_pack_fn = std::vector<double> (*)(const V2Args&);
-
-template <class Sh>
-std::vector<double> pack_v2(const V2Args& a) {
-  std::vector<double> out(static_cast<size_t>(Sh::ctot(0) + Sh::ctot(1) + Sh::ctot(2)), 0.0);
-  const int base[3] = {0, Sh::ctot(0), Sh::ctot(0) + Sh::ctot(1)};
-  for (int d = 0; d < 3; ++d)
-    for (int s = 0; s < Sh::S; ++s) {
-      const int K = Sh::K(s, d), kd = Sh::kind(s, d), N = Sh::N(d);
-      const std::vector<double>& C = *a.dense[s][d];
-      for (int x = 0; x < N; ++x)
-        for (int y = 0; y < N; ++y) {
-          const int lo = band_lo(kd, x, y), cnt = band_count(kd, x, y);
-          const int co = Sh::coff(d, s, x, y);
-          for (int j = 0; j < cnt; ++j)
-            out[static_cast<size_t>(base[d] + co + j)] =
-                C[(static_cast<size_t>(x) * N + y) * K + lo + band_step(kd, x, y) * j];
-        }
-    }
-  return out;
-}
-
-// fragment-ordered stage-C A of an MMA shape (empty otherwise)
-template <class Sh>
-std::vector<double> pack_mma(const V2Args& a) {
-  if constexpr (Sh::MMA) {
-    const std::vector<double>* d[kMaxTerms];
-    for (int s = 0; s < Sh::S; ++s) d[s] = a.dense[s][0];
-    return build_mma_a<Sh>(d);
-  } else {
-    return {};
-  }
-}
-
-int vec2_ok(const double* M, int64_t ldM) {
-  return (ldM % 2 == 0 && reinterpret_cast<uintptr_t>(M) % 16 == 0) ? 1 : 0;
-}
-
-template <class Sh>
-constexpr const char* stage_c_desc() {
-  return Sh::MMA     ? "stage C on DMMA"
-         : Sh::PSPLIT ? (Sh::PAIR ? "banded stage C, parity split, paired 16-B stores"
-                                  : "banded stage C, parity split")
-         : Sh::PAIR   ? "banded stage C, paired 16-B stores"
-                      : "banded stage C";
-}
-
-template <class Sh>
-cudaError_t launch_v2(const V2Args& a, const std::vector<double>& packed, cudaStream_t st,
-                      int num_sms) {
-  V2Params<Sh> p;
-  p.I = a.I;
-  p.M = a.M;
-  p.ldM = a.ldM;
-  p.mat_stride = a.n_tot * a.ldM;
-  p.n_units = a.n_elem * a.P;
-  p.nc = a.nc;
-  p.P = a.P;
-  p.Nt = a.Nt;
-  p.mom_per_elem = a.mom_per_elem;
-  p.amma = a.amma;
-  p.vec2 = vec2_ok(a.M, a.ldM);
-  std::memcpy(p.cu, packed.data(), sizeof(double) * Sh::ctot(0));
-  std::memcpy(p.cv, packed.data() + Sh::ctot(0), sizeof(double) * Sh::ctot(1));
-  std::memcpy(p.cw, packed.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));
-  if (p.n_units == 0) return cudaSuccess;
-  static int blocks_per_sm = -1;  // per instantiation (kernel attributes are process-wide)
-  if (blocks_per_sm < 0) {
-    cudaError_t e = cudaFuncSetAttribute(contract_v2_kernel<Sh>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)v2_smem<Sh>());
-    if (e != cudaSuccess) return e;
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, contract_v2_kernel<Sh>, Sh::THREADS,
-                                                      v2_smem<Sh>());
-    if (e != cudaSuccess) return e;
-    if (b < 1) return cudaErrorInvalidConfiguration;
-    blocks_per_sm = b;
-  }
-  const int64_t grid = Sh::PERSIST
-                           ? std::min<int64_t>(p.n_units, static_cast<int64_t>(blocks_per_sm) * num_sms)
-                           : p.n_units;
-  contract_v2_kernel<Sh><<<static_cast<unsigned>(grid), Sh::THREADS, v2_smem<Sh>(), st>>>(p);
-  return cudaGetLastError();
-}
-
-struct V2Entry {
-  int order[3];
-  int S;
-  int kinds[kMaxTerms][3];
-  v2_fn launch;
-  v2_pack_fn pack;
-  v2_pack_fn mma_pack;
-  size_t smem;
-  const char* desc;
-};
-
-template <class Sh>
-V2Entry make_v2() {
-  V2Entry r{};
-  for (int d = 0; d < 3; ++d) r.order[d] = Sh::N(d);
-  r.S = Sh::S;
-  for (int s = 0; s < Sh::S; ++s)
-    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Sh::kind(s, d);
-  r.launch = &launch_v2<Sh>;
-  r.pack = &pack_v2<Sh>;
-  r.mma_pack = &pack_mma<Sh>;
-  r.smem = v2_smem<Sh>();
-  r.desc = stage_c_desc<Sh>();
-  return r;
-}
-
-constexpr int kPPP = enc_kind(PP, PP, PP);
-constexpr int kDDD = enc_kind(DD, DD, DD);
-constexpr int kCPPP = enc_kind(PP | kConforming, PP | kConforming, PP | kConforming);
-constexpr int kCDDD = enc_kind(DD | kConforming, DD | kConforming, DD | kConforming);
-
-// <N_u, N_v, N_w, n1 tile, p1 tile, threads, min CTAs/SM, A once per unit, fibers per
-//  thread, term kinds...>.  Several variants per shape: the first is the default,
-//  P2S_V2_VARIANT=k selects the k-th match (tuning).
-const std::vector<V2Entry>& v2_registry() {
-  static const std::vector<V2Entry> reg = {
-      // <NU, NV, NW, T, P1T (= NW), PG (= NW), threads, minB,
-      //  flags (1 AALL, 2 ROWLOOP, 4 SYM, 8 PERSIST), FPT, kinds...>
-      make_v2<Shape<4, 4, 4, 4, 4, 4, 256, 2, 4, 1, kPPP>>(),                 // C1
-      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>>(),           // C2
-      make_v2<Shape<6, 6, 6, 1, 6, 6, 224, 2, 4, 1, kPPP, kDDD>>(),
-      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 0, 2, kPPP, kDDD>>(),
-      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 1, kPPP, kDDD>>(),           // C3
-      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>>(),
-      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 12, 2, kPPP, kDDD>>(),
-      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>>(),          // C4
-      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 4, 1, kPPP, kDDD>>(),
-      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 1, kPPP, kDDD>>(),
-      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>>(),            // test shapes
-      make_v2<Shape<3, 3, 3, 1, 3, 3, 64, 4, 12, 2, kPPP, kDDD>>(),
-      make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 2, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
-      make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 18, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
-      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 20, 1, kPPP, kDDD>>(),
-      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 64, 2, kPPP, kDDD>>(),
-      make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 66, 2, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
-      // conforming basis
-      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kCPPP, kCDDD>>(),
-      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kCPPP, kCDDD>>(),
-  };
-  return reg;
-}
 
 const V2Entry* find_v2(const p2s_problem& pb) {
   int want = 0, seen = 0;
@@ -372,86 +79,6 @@ const V2Entry* find_v2(const p2s_problem& pb) {
   return first;
 }
 
-// ------------------------------------------------------------ shape-specialised moments
-
-using mv2_fn = cudaError_t (*)(const double*, double*, int64_t, int, int64_t,
-                               const std::vector<double>&, cudaStream_t);
-using mv2_pack_fn = std::vector<double> (*)(const std::vector<double> (*)[3]);
-
-template <class Ms>
-std::vector<double> pack_mv2(const std::vector<double> (*phi)[3]) {
-  // phi[s][d] = [K][nq] full weighted table -> half tables [K][H]
-  std::vector<double> out(static_cast<size_t>(Ms::TALL), 0.0);
-  for (int s = 0; s < Ms::S; ++s)
-    for (int d = 0; d < 3; ++d) {
-      const int K = Ms::K(s, d), Q = Ms::Q(d), H = Ms::H(d);
-      for (int k = 0; k < K; ++k)
-        for (int h = 0; h < H; ++h) {
-          const double v = phi[s][d][static_cast<size_t>(k) * Q + h];
-          out[static_cast<size_t>(Ms::toff(s, d) + k * H + h)] = v;
-          out[static_cast<size_t>(Ms::ttoff(d) + k * H + h)] = v;  // shared (identical rows)
-        }
-    }
-  return out;
-}
-
-template <class Ms>
-cudaError_t launch_mv2(const double* alpha, double* I, int64_t n_elem, int P, int64_t mom_per_elem,
-                       const std::vector<double>& packed, cudaStream_t st) {
-  MV2Params<Ms> p;
-  p.alpha = alpha;
-  p.I = I;
-  p.P = P;
-  p.n_units = n_elem * P * Ms::S;
-  p.mom_per_elem = mom_per_elem;
-  std::memcpy(p.tab, packed.data(), sizeof(double) * Ms::TALL);
-  if (p.n_units == 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(moments_v2_kernel<Ms>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ms::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  moments_v2_kernel<Ms><<<static_cast<unsigned>(p.n_units), Ms::THREADS, Ms::SMEM, st>>>(p);
-  return cudaGetLastError();
-}
-
-struct MV2Entry {
-  int order[3], nq[3], S;
-  int kinds[kMaxTerms][3];
-  mv2_fn launch;
-  mv2_pack_fn pack;
-};
-
-template <class Ms>
-MV2Entry make_mv2() {
-  MV2Entry r{};
-  for (int d = 0; d < 3; ++d) {
-    r.order[d] = Ms::N(d);
-    r.nq[d] = Ms::Q(d);
-  }
-  r.S = Ms::S;
-  for (int s = 0; s < Ms::S; ++s)
-    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Ms::kind(s, d);
-  r.launch = &launch_mv2<Ms>;
-  r.pack = &pack_mv2<Ms>;
-  return r;
-}
-
-// <N_u, N_v, N_w, nq_u, nq_v, nq_w, threads, term kinds...>
-const std::vector<MV2Entry>& mv2_registry() {
-  static const std::vector<MV2Entry> reg = {
-      make_mv2<MShape<4, 4, 4, 8, 8, 8, 128, kPPP>>(),                    // C1
-      make_mv2<MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),           // C2
-      make_mv2<MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),           // C3
-      make_mv2<MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>>(),          // C4
-      make_mv2<MShape<3, 3, 3, 6, 6, 6, 128, kPPP, kDDD>>(),              // test shapes
-      make_mv2<MShape<4, 3, 3, 9, 5, 7, 128, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
-      make_mv2<MShape<5, 5, 5, 9, 9, 9, 128, kPPP, kDDD>>(),
-  };
-  return reg;
-}
 
 const MV2Entry* find_mv2(const p2s_problem& pb) {
   for (const MV2Entry& r : mv2_registry()) {
@@ -464,170 +91,6 @@ const MV2Entry* find_mv2(const p2s_problem& pb) {
   return nullptr;
 }
 
-// ------------------------------------------------------------ fused fill registry
-
-using fused_fn = cudaError_t (*)(const double*, double*, int64_t, int64_t, int64_t, int, int, int,
-                                 const std::vector<double>&, const std::vector<double>&,
-                                 const double*, cudaStream_t, int);
-
-// GEO > 0: `alpha` is the geometry records and the kernel computes the coupling
-// factors itself (xq = the GL nodes u, v, w appended to mpack); GEO == 2 launches
-// one thread-block cluster of P CTAs per element (non-portable size for P = 9)
-template <class Sh, class Ms, int GEO = 0>
-cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_tot, int64_t n_elem,
-                         int nc, int P, int Nt, const std::vector<double>& cpack,
-                         const std::vector<double>& mpack, const double* amma, cudaStream_t st,
-                         int num_sms) {
-  FusedParams<Sh, Ms> p;
-  p.geom = GEO ? alpha : nullptr;
-  if constexpr (GEO != 0)
-    std::memcpy(p.xq, mpack.data() + Ms::TALL, sizeof(double) * (Ms::Q(0) + Ms::Q(1) + Ms::Q(2)));
-  p.c.I = nullptr;
-  p.c.M = M;
-  p.c.ldM = ldM;
-  p.c.mat_stride = n_tot * ldM;
-  p.c.n_units = n_elem * P;
-  p.c.nc = nc;
-  p.c.P = P;
-  p.c.Nt = Nt;
-  p.c.mom_per_elem = 0;
-  p.c.amma = amma;
-  p.c.vec2 = vec2_ok(M, ldM);
-  std::memcpy(p.c.cu, cpack.data(), sizeof(double) * Sh::ctot(0));
-  std::memcpy(p.c.cv, cpack.data() + Sh::ctot(0), sizeof(double) * Sh::ctot(1));
-  std::memcpy(p.c.cw, cpack.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));
-  p.alpha = alpha;
-  p.prefetch_stride = 0;
-  std::memcpy(p.tab, mpack.data(), sizeof(double) * Ms::TALL);
-  if (p.c.n_units == 0) return cudaSuccess;
-  constexpr size_t smem = FusedLayout<Sh, Ms, GEO>::SMEM;
-  static int blocks_per_sm = -1;
-  if (blocks_per_sm < 0) {
-    cudaError_t e = cudaFuncSetAttribute(fill_fused_kernel<Sh, Ms, GEO>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    if constexpr (GEO == 2) {
-      e = cudaFuncSetAttribute(fill_fused_kernel<Sh, Ms, GEO>,
-                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-    }
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fill_fused_kernel<Sh, Ms, GEO>, Sh::THREADS,
-                                                      smem);
-    if (e != cudaSuccess) return e;
-    if (b < 1) return cudaErrorInvalidConfiguration;
-    blocks_per_sm = b;
-  }
-  const int64_t resident = static_cast<int64_t>(blocks_per_sm) * num_sms;
-  const int64_t grid = Sh::PERSIST ? std::min<int64_t>(p.c.n_units, resident) : p.c.n_units;
-  p.prefetch_stride = resident;
-  if constexpr (GEO == 2) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(p.c.n_units));
-    cfg.blockDim = dim3(Sh::THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = static_cast<unsigned>(P);  // one element per cluster
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, fill_fused_kernel<Sh, Ms, GEO>, p);
-  }
-  fill_fused_kernel<Sh, Ms, GEO><<<static_cast<unsigned>(grid), Sh::THREADS, smem, st>>>(p);
-  return cudaGetLastError();
-}
-
-struct FusedEntry {
-  int order[3], nq[3], S;
-  int kinds[kMaxTerms][3];
-  fused_fn launch;
-  fused_fn launch_geo;          // coupling factors from geometry records, per unit
-  fused_fn launch_geo_cluster;  // ... shared per element through a cluster (DSMEM)
-  v2_pack_fn cpack;
-  mv2_pack_fn mpack;
-  v2_pack_fn mma_pack;
-  const char* desc;
-};
-
-template <class Sh, class Ms, bool WITH_GEO = false>
-FusedEntry make_fused() {
-  FusedEntry r{};
-  for (int d = 0; d < 3; ++d) {
-    r.order[d] = Sh::N(d);
-    r.nq[d] = Ms::Q(d);
-  }
-  r.S = Sh::S;
-  for (int s = 0; s < Sh::S; ++s)
-    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Sh::kind(s, d);
-  r.launch = &launch_fused<Sh, Ms>;
-  r.launch_geo = r.launch_geo_cluster = nullptr;
-  if constexpr (WITH_GEO) {
-    r.launch_geo = &launch_fused<Sh, Ms, 1>;
-    r.launch_geo_cluster = &launch_fused<Sh, Ms, 2>;
-  }
-  r.cpack = &pack_v2<Sh>;
-  r.mpack = &pack_mv2<Ms>;
-  r.mma_pack = &pack_mma<Sh>;
-  r.desc = stage_c_desc<Sh>();
-  return r;
-}
-
-// <Shape: N_u, N_v, N_w, n1 tile, p1 tile, p1 group, threads, min CTAs/SM, flags, FPT, kinds>
-// flags: 1 AALL, 2 ROWLOOP, 4 SYM, 8 PERSIST, 16 MMA (stage C on DMMA), 32 PAIR (16-B
-// stores), 64 PSPLIT (parity-split stage C).  The first match of a problem is the
-// default; P2S_FUSED_VARIANT=k selects the k-th (tuning / A-B measurements, see
-// profiles/README.md for the numbers behind each default).
-const std::vector<FusedEntry>& fused_registry() {
-  static const std::vector<FusedEntry> reg = {
-      make_fused<Shape<4, 4, 4, 4, 4, 4, 256, 2, 4, 1, kPPP>,
-                 MShape<4, 4, 4, 8, 8, 8, 256, kPPP>>(),                              // C1
-      // C2: 0 banded (default, also compiled in geometry mode), 1 paired stores,
-      // 2 parity split, 3 DMMA
-      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>, true>(),
-      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 36, 2, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
-      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 68, 2, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
-      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 20, 1, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
-      // C2: 4 parity split + paired (FPT 2), 5 same FPT 4
-      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 100, 2, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
-      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 100, 4, kPPP, kDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
-      // C3: 0 paired stores (default), 1 banded, 2 parity split + paired, 3 DMMA
-      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 38, 2, kPPP, kDDD>,
-                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
-      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 6, 2, kPPP, kDDD>,
-                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
-      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 102, 2, kPPP, kDDD>,
-                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
-      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 22, 1, kPPP, kDDD>,
-                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
-      // C4: 0 parity split (default), 1 banded, 2 paired stores, 3 DMMA
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 70, 1, kPPP, kDDD>,
-                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
-                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 38, 2, kPPP, kDDD>,
-                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
-      make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 22, 1, kPPP, kDDD>,
-                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
-      // C2 in the conforming basis
-      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kCPPP, kCDDD>,
-                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
-      // test shapes
-      make_fused<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>,
-                 MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),
-      make_fused<Shape<4, 3, 3, 3, 3, 3, 96, 4, 0, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>,
-                 MShape<4, 3, 3, 9, 5, 7, 96, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
-  };
-  return reg;
-}
 
 const FusedEntry* find_fused(const p2s_problem& pb) {
   if (const char* v = std::getenv("P2S_NO_FUSED"))
@@ -647,176 +110,6 @@ const FusedEntry* find_fused(const p2s_problem& pb) {
   return first;
 }
 
-// ------------------------------------------------------------ large-order registry
-
-struct LargeArgs {
-  const std::vector<double> (*phi)[3];            // [s][d] full tables
-  const std::vector<double>* dense[kMaxTerms][3];  // [s][d] [N][N][K]
-};
-
-struct LargePack {
-  std::vector<double> tab, cu, cvw;
-  double* d_cvw = nullptr;
-  // runtime: parity-split u stage; v/w of chunk i+1 on `aux` overlapping u of
-  // chunk i on the caller's stream (X double-buffered), ordered by events
-  bool ps = true, overlap = true;
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_vw[2]{}, ev_u[2]{};
-};
-
-using large_pack_fn = bool (*)(const LargeArgs&, LargePack&);
-using large_mom_fn = cudaError_t (*)(const double*, double*, int64_t, const LargePack&, cudaStream_t);
-using large_con_fn = cudaError_t (*)(const double*, double*, double*, int64_t, int64_t, int64_t, int,
-                                     int, int, const LargePack&, cudaStream_t);
-
-template <class Ls>
-bool pack_large(const LargeArgs& a, LargePack& out) {
-  out.tab.assign(static_cast<size_t>(Ls::TALL), 0.0);
-  for (int d = 0; d < 3; ++d) {
-    // shared rows: the term with the most kernel polynomials in this direction
-    int sb = 0;
-    for (int s = 0; s < Ls::S; ++s)
-      if (Ls::K(s, d) > Ls::K(sb, d)) sb = s;
-    const int Q = Ls::Q(d), H = Ls::H(d);
-    for (int k = 0; k < Ls::KMAX(d); ++k)
-      for (int h = 0; h < H; ++h)
-        out.tab[static_cast<size_t>(Ls::ttoff(d) + k * H + h)] =
-            a.phi[sb][d][static_cast<size_t>(k) * Q + h];
-  }
-  auto band_pack = [&](int d, std::vector<double>& v, size_t base) {
-    for (int s = 0; s < Ls::S; ++s) {
-      const int K = Ls::K(s, d), kd = Ls::kind(s, d), N = Ls::N(d);
-      const std::vector<double>& C = *a.dense[s][d];
-      for (int x = 0; x < N; ++x)
-        for (int y = 0; y < N; ++y) {
-          const int lo = band_lo(kd, x, y), cnt = band_count(kd, x, y);
-          for (int j = 0; j < cnt; ++j)
-            v[base + static_cast<size_t>(Ls::coff(d, s, x, y) + j)] =
-                C[(static_cast<size_t>(x) * N + y) * K + lo + band_step(kd, x, y) * j];
-        }
-    }
-  };
-  out.cu.assign(static_cast<size_t>(Ls::ctot(0)), 0.0);
-  band_pack(0, out.cu, 0);
-  out.cvw.assign(static_cast<size_t>(Ls::ctot(1) + Ls::ctot(2)), 0.0);
-  band_pack(1, out.cvw, 0);
-  band_pack(2, out.cvw, static_cast<size_t>(Ls::ctot(1)));
-  if (cudaMalloc(&out.d_cvw, sizeof(double) * out.cvw.size()) != cudaSuccess) return false;
-  return cudaMemcpy(out.d_cvw, out.cvw.data(), sizeof(double) * out.cvw.size(),
-                    cudaMemcpyHostToDevice) == cudaSuccess;
-}
-
-template <class Ls>
-cudaError_t launch_large_moments(const double* alpha, double* I, int64_t n_units, const LargePack& pk,
-                                 cudaStream_t st) {
-  LMomParams<Ls> p;
-  p.alpha = alpha;
-  p.I = I;
-  p.n_units = n_units;
-  std::memcpy(p.tab, pk.tab.data(), sizeof(double) * Ls::TALL);
-  if (n_units == 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(large_moments_kernel<Ls>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ls::MOM_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  large_moments_kernel<Ls><<<static_cast<unsigned>(n_units * Ls::S * Ls::NCH), 256, Ls::MOM_SMEM, st>>>(p);
-  return cudaGetLastError();
-}
-
-// contraction of n_units units from I (device) via the X scratch (chunks of xchunk units)
-template <class Ls>
-cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t n_units,
-                                  int64_t xchunk, int64_t ldM, int nc, int P, int Nt,
-                                  const LargePack& pk, cudaStream_t st) {
-  static bool attr = false;
-  constexpr size_t vw_smem = large_vw_smem<Ls>();
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(large_vw_kernel<Ls>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vw_smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  LUParams<Ls> up;
-  up.M = M;
-  up.ldM = ldM;
-  up.mat_stride = static_cast<int64_t>(nc) * Nt * ldM;
-  up.nc = nc;
-  up.P = P;
-  up.Nt = Nt;
-  std::memcpy(up.cu, pk.cu.data(), sizeof(double) * Ls::ctot(0));
-  // X holds two chunk buffers; chunk i uses buffer i % 2
-  const bool ov = pk.overlap && pk.aux != nullptr;
-  cudaError_t e;
-  if (ov) {
-    if ((e = cudaEventRecord(pk.ev_start, st)) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(pk.aux, pk.ev_start, 0)) != cudaSuccess) return e;  // I ready
-  }
-  int64_t i = 0;
-  for (int64_t u0 = 0; u0 < n_units; u0 += xchunk, ++i) {
-    const int64_t cnt = std::min(xchunk, n_units - u0);
-    const int b = static_cast<int>(i % 2);
-    double* Xb = X + (ov ? b : 0) * xchunk * Ls::XPU;
-    LVWParams<Ls> vp;
-    vp.I = I + u0 * Ls::MPP;
-    vp.X = Xb;
-    vp.cvw = pk.d_cvw;
-    vp.n_units = cnt;
-    cudaStream_t vs = ov ? pk.aux : st;
-    if (ov && i >= 2 && (e = cudaStreamWaitEvent(pk.aux, pk.ev_u[b], 0)) != cudaSuccess) return e;
-    large_vw_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), 256, vw_smem, vs>>>(vp);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (ov) {
-      if ((e = cudaEventRecord(pk.ev_vw[b], pk.aux)) != cudaSuccess) return e;
-      if ((e = cudaStreamWaitEvent(st, pk.ev_vw[b], 0)) != cudaSuccess) return e;
-    }
-    // u stage: absolute units u0 .. u0+cnt-1; Xb holds the chunk
-    up.X = Xb;
-    up.n_units = cnt;
-    large_u_dispatch<Ls>(up, u0, cnt, pk.ps, st);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (ov && (e = cudaEventRecord(pk.ev_u[b], st)) != cudaSuccess) return e;
-  }
-  return cudaSuccess;
-}
-
-struct LargeEntry {
-  int order[3], nq[3], S;
-  int kinds[kMaxTerms][3];
-  large_pack_fn pack;
-  large_mom_fn moments;
-  large_con_fn contract;
-  int64_t mpp, xpu;
-};
-
-template <class Ls>
-LargeEntry make_large() {
-  LargeEntry r{};
-  for (int d = 0; d < 3; ++d) {
-    r.order[d] = Ls::N(d);
-    r.nq[d] = Ls::Q(d);
-  }
-  r.S = Ls::S;
-  for (int s = 0; s < Ls::S; ++s)
-    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Ls::kind(s, d);
-  r.pack = &pack_large<Ls>;
-  r.moments = &launch_large_moments<Ls>;
-  r.contract = &launch_large_contract<Ls>;
-  r.mpp = Ls::MPP;
-  r.xpu = Ls::XPU;
-  return r;
-}
-
-const std::vector<LargeEntry>& large_registry() {
-  static const std::vector<LargeEntry> reg = {
-      make_large<LShape<16, 16, 16, 36, 36, 36, 8, kPPP, kDDD>>(),   // C5
-      make_large<LShape<5, 4, 3, 8, 8, 6, 4, kPPP, kDDD>>(),         // test shape
-      make_large<LShape<5, 4, 3, 8, 8, 6, 4, kCPPP, kCDDD>>(),       // test shape, conforming
-  };
-  return reg;
-}
 
 const LargeEntry* find_large(const p2s_problem& pb) {
   for (const LargeEntry& r : large_registry()) {
@@ -829,32 +122,6 @@ const LargeEntry* find_large(const p2s_problem& pb) {
   return nullptr;
 }
 
-// ------------------------------------------------------------ moment launch
-
-template <int KMAX>
-cudaError_t launch_moments_k(const MomentParams& p, size_t smem, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(moments_kernel<KMAX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  moments_kernel<KMAX><<<static_cast<unsigned>(p.n_units), 256, smem, st>>>(p);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_moments(int kmax, const MomentParams& p, size_t smem, cudaStream_t st) {
-  if (p.n_units == 0) return cudaSuccess;
-  switch (kmax) {
-    case 8: return launch_moments_k<8>(p, smem, st);
-    case 12: return launch_moments_k<12>(p, smem, st);
-    case 16: return launch_moments_k<16>(p, smem, st);
-    case 20: return launch_moments_k<20>(p, smem, st);
-    case 24: return launch_moments_k<24>(p, smem, st);
-    default: return launch_moments_k<32>(p, smem, st);
-  }
-}
 
 }  // namespace
 

@@ -15,6 +15,7 @@
 #pragma once
 
 #include "p2s_kernels.cuh"
+#include "p2s_moments_v2.cuh"  // fold_contract
 
 namespace p2s {
 

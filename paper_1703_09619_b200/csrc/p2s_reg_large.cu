@@ -1,0 +1,162 @@
+// p2s_reg_large.cu -- large-order registry (C5: large_moments_kernel, large_vw_kernel, large_u_kernel).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include <cstdint>
+
+#include "p2s_large.cuh"
+#include "p2s_reg_common.cuh"
+
+namespace p2s {
+namespace reg {
+
+// ------------------------------------------------------------ large-order registry
+
+
+template <class Ls>
+bool pack_large(const LargeArgs& a, LargePack& out) {
+  out.tab.assign(static_cast<size_t>(Ls::TALL), 0.0);
+  for (int d = 0; d < 3; ++d) {
+    // shared rows: the term with the most kernel polynomials in this direction
+    int sb = 0;
+    for (int s = 0; s < Ls::S; ++s)
+      if (Ls::K(s, d) > Ls::K(sb, d)) sb = s;
+    const int Q = Ls::Q(d), H = Ls::H(d);
+    for (int k = 0; k < Ls::KMAX(d); ++k)
+      for (int h = 0; h < H; ++h)
+        out.tab[static_cast<size_t>(Ls::ttoff(d) + k * H + h)] =
+            a.phi[sb][d][static_cast<size_t>(k) * Q + h];
+  }
+  auto band_pack = [&](int d, std::vector<double>& v, size_t base) {
+    for (int s = 0; s < Ls::S; ++s) {
+      const int K = Ls::K(s, d), kd = Ls::kind(s, d), N = Ls::N(d);
+      const std::vector<double>& C = *a.dense[s][d];
+      for (int x = 0; x < N; ++x)
+        for (int y = 0; y < N; ++y) {
+          const int lo = band_lo(kd, x, y), cnt = band_count(kd, x, y);
+          for (int j = 0; j < cnt; ++j)
+            v[base + static_cast<size_t>(Ls::coff(d, s, x, y) + j)] =
+                C[(static_cast<size_t>(x) * N + y) * K + lo + band_step(kd, x, y) * j];
+        }
+    }
+  };
+  out.cu.assign(static_cast<size_t>(Ls::ctot(0)), 0.0);
+  band_pack(0, out.cu, 0);
+  out.cvw.assign(static_cast<size_t>(Ls::ctot(1) + Ls::ctot(2)), 0.0);
+  band_pack(1, out.cvw, 0);
+  band_pack(2, out.cvw, static_cast<size_t>(Ls::ctot(1)));
+  if (cudaMalloc(&out.d_cvw, sizeof(double) * out.cvw.size()) != cudaSuccess) return false;
+  return cudaMemcpy(out.d_cvw, out.cvw.data(), sizeof(double) * out.cvw.size(),
+                    cudaMemcpyHostToDevice) == cudaSuccess;
+}
+
+template <class Ls>
+cudaError_t launch_large_moments(const double* alpha, double* I, int64_t n_units, const LargePack& pk,
+                                 cudaStream_t st) {
+  LMomParams<Ls> p;
+  p.alpha = alpha;
+  p.I = I;
+  p.n_units = n_units;
+  std::memcpy(p.tab, pk.tab.data(), sizeof(double) * Ls::TALL);
+  if (n_units == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(large_moments_kernel<Ls>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ls::MOM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  large_moments_kernel<Ls><<<static_cast<unsigned>(n_units * Ls::S * Ls::NCH), 256, Ls::MOM_SMEM, st>>>(p);
+  return cudaGetLastError();
+}
+
+// contraction of n_units units from I (device) via the X scratch (chunks of xchunk units)
+template <class Ls>
+cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t n_units,
+                                  int64_t xchunk, int64_t ldM, int nc, int P, int Nt,
+                                  const LargePack& pk, cudaStream_t st) {
+  static bool attr = false;
+  constexpr size_t vw_smem = large_vw_smem<Ls>();
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(large_vw_kernel<Ls>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vw_smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  LUParams<Ls> up;
+  up.M = M;
+  up.ldM = ldM;
+  up.mat_stride = static_cast<int64_t>(nc) * Nt * ldM;
+  up.nc = nc;
+  up.P = P;
+  up.Nt = Nt;
+  std::memcpy(up.cu, pk.cu.data(), sizeof(double) * Ls::ctot(0));
+  // X holds two chunk buffers; chunk i uses buffer i % 2
+  const bool ov = pk.overlap && pk.aux != nullptr;
+  cudaError_t e;
+  if (ov) {
+    if ((e = cudaEventRecord(pk.ev_start, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(pk.aux, pk.ev_start, 0)) != cudaSuccess) return e;  // I ready
+  }
+  int64_t i = 0;
+  for (int64_t u0 = 0; u0 < n_units; u0 += xchunk, ++i) {
+    const int64_t cnt = std::min(xchunk, n_units - u0);
+    const int b = static_cast<int>(i % 2);
+    double* Xb = X + (ov ? b : 0) * xchunk * Ls::XPU;
+    LVWParams<Ls> vp;
+    vp.I = I + u0 * Ls::MPP;
+    vp.X = Xb;
+    vp.cvw = pk.d_cvw;
+    vp.n_units = cnt;
+    cudaStream_t vs = ov ? pk.aux : st;
+    if (ov && i >= 2 && (e = cudaStreamWaitEvent(pk.aux, pk.ev_u[b], 0)) != cudaSuccess) return e;
+    large_vw_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), 256, vw_smem, vs>>>(vp);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (ov) {
+      if ((e = cudaEventRecord(pk.ev_vw[b], pk.aux)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(st, pk.ev_vw[b], 0)) != cudaSuccess) return e;
+    }
+    // u stage: absolute units u0 .. u0+cnt-1; Xb holds the chunk
+    up.X = Xb;
+    up.n_units = cnt;
+    large_u_dispatch<Ls>(up, u0, cnt, pk.ps, st);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (ov && (e = cudaEventRecord(pk.ev_u[b], st)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+
+template <class Ls>
+LargeEntry make_large() {
+  LargeEntry r{};
+  for (int d = 0; d < 3; ++d) {
+    r.order[d] = Ls::N(d);
+    r.nq[d] = Ls::Q(d);
+  }
+  r.S = Ls::S;
+  for (int s = 0; s < Ls::S; ++s)
+    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Ls::kind(s, d);
+  r.pack = &pack_large<Ls>;
+  r.moments = &launch_large_moments<Ls>;
+  r.contract = &launch_large_contract<Ls>;
+  r.mpp = Ls::MPP;
+  r.xpu = Ls::XPU;
+  return r;
+}
+
+const std::vector<LargeEntry>& large_registry() {
+  static const std::vector<LargeEntry> reg = {
+      make_large<LShape<16, 16, 16, 36, 36, 36, 8, kPPP, kDDD>>(),   // C5
+      make_large<LShape<5, 4, 3, 8, 8, 6, 4, kPPP, kDDD>>(),         // test shape
+      make_large<LShape<5, 4, 3, 8, 8, 6, 4, kCPPP, kCDDD>>(),       // test shape, conforming
+  };
+  return reg;
+}
+
+}  // namespace reg
+}  // namespace p2s

@@ -1,0 +1,161 @@
+// p2s_reg_v2.cu -- shape-specialised contraction (contract_v2_kernel) and moment (moments_v2_kernel) registries.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "p2s_reg_common.cuh"
+
+namespace p2s {
+namespace reg {
+
+// ------------------------------------------------------------ shape-specialised registry
+
+
+template <class Sh>
+cudaError_t launch_v2(const V2Args& a, const std::vector<double>& packed, cudaStream_t st,
+                      int num_sms) {
+  V2Params<Sh> p;
+  p.I = a.I;
+  p.M = a.M;
+  p.ldM = a.ldM;
+  p.mat_stride = a.n_tot * a.ldM;
+  p.n_units = a.n_elem * a.P;
+  p.nc = a.nc;
+  p.P = a.P;
+  p.Nt = a.Nt;
+  p.mom_per_elem = a.mom_per_elem;
+  p.amma = a.amma;
+  p.vec2 = vec2_ok(a.M, a.ldM);
+  std::memcpy(p.cu, packed.data(), sizeof(double) * Sh::ctot(0));
+  std::memcpy(p.cv, packed.data() + Sh::ctot(0), sizeof(double) * Sh::ctot(1));
+  std::memcpy(p.cw, packed.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));
+  if (p.n_units == 0) return cudaSuccess;
+  static int blocks_per_sm = -1;  // per instantiation (kernel attributes are process-wide)
+  if (blocks_per_sm < 0) {
+    cudaError_t e = cudaFuncSetAttribute(contract_v2_kernel<Sh>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)v2_smem<Sh>());
+    if (e != cudaSuccess) return e;
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, contract_v2_kernel<Sh>, Sh::THREADS,
+                                                      v2_smem<Sh>());
+    if (e != cudaSuccess) return e;
+    if (b < 1) return cudaErrorInvalidConfiguration;
+    blocks_per_sm = b;
+  }
+  const int64_t grid = Sh::PERSIST
+                           ? std::min<int64_t>(p.n_units, static_cast<int64_t>(blocks_per_sm) * num_sms)
+                           : p.n_units;
+  contract_v2_kernel<Sh><<<static_cast<unsigned>(grid), Sh::THREADS, v2_smem<Sh>(), st>>>(p);
+  return cudaGetLastError();
+}
+
+
+template <class Sh>
+V2Entry make_v2() {
+  V2Entry r{};
+  for (int d = 0; d < 3; ++d) r.order[d] = Sh::N(d);
+  r.S = Sh::S;
+  for (int s = 0; s < Sh::S; ++s)
+    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Sh::kind(s, d);
+  r.launch = &launch_v2<Sh>;
+  r.pack = &pack_v2<Sh>;
+  r.mma_pack = &pack_mma<Sh>;
+  r.smem = v2_smem<Sh>();
+  r.desc = stage_c_desc<Sh>();
+  return r;
+}
+
+
+// <N_u, N_v, N_w, n1 tile, p1 tile, threads, min CTAs/SM, A once per unit, fibers per
+//  thread, term kinds...>.  Several variants per shape: the first is the default,
+//  P2S_V2_VARIANT=k selects the k-th match (tuning).
+const std::vector<V2Entry>& v2_registry() {
+  static const std::vector<V2Entry> reg = {
+      // <NU, NV, NW, T, P1T (= NW), PG (= NW), threads, minB,
+      //  flags (1 AALL, 2 ROWLOOP, 4 SYM, 8 PERSIST), FPT, kinds...>
+      make_v2<Shape<4, 4, 4, 4, 4, 4, 256, 2, 4, 1, kPPP>>(),                 // C1
+      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>>(),           // C2
+      make_v2<Shape<6, 6, 6, 1, 6, 6, 224, 2, 4, 1, kPPP, kDDD>>(),
+      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 0, 2, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 1, kPPP, kDDD>>(),           // C3
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 12, 2, kPPP, kDDD>>(),
+      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>>(),          // C4
+      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 4, 1, kPPP, kDDD>>(),
+      make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 1, kPPP, kDDD>>(),
+      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>>(),            // test shapes
+      make_v2<Shape<3, 3, 3, 1, 3, 3, 64, 4, 12, 2, kPPP, kDDD>>(),
+      make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 2, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+      make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 18, 1, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 20, 1, kPPP, kDDD>>(),
+      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 64, 2, kPPP, kDDD>>(),
+      make_v2<Shape<4, 3, 3, 3, 3, 3, 96, 4, 66, 2, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+      // conforming basis
+      make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kCPPP, kCDDD>>(),
+      make_v2<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kCPPP, kCDDD>>(),
+  };
+  return reg;
+}
+
+
+// ------------------------------------------------------------ shape-specialised moments
+
+
+template <class Ms>
+cudaError_t launch_mv2(const double* alpha, double* I, int64_t n_elem, int P, int64_t mom_per_elem,
+                       const std::vector<double>& packed, cudaStream_t st) {
+  MV2Params<Ms> p;
+  p.alpha = alpha;
+  p.I = I;
+  p.P = P;
+  p.n_units = n_elem * P * Ms::S;
+  p.mom_per_elem = mom_per_elem;
+  std::memcpy(p.tab, packed.data(), sizeof(double) * Ms::TALL);
+  if (p.n_units == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(moments_v2_kernel<Ms>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ms::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  moments_v2_kernel<Ms><<<static_cast<unsigned>(p.n_units), Ms::THREADS, Ms::SMEM, st>>>(p);
+  return cudaGetLastError();
+}
+
+
+template <class Ms>
+MV2Entry make_mv2() {
+  MV2Entry r{};
+  for (int d = 0; d < 3; ++d) {
+    r.order[d] = Ms::N(d);
+    r.nq[d] = Ms::Q(d);
+  }
+  r.S = Ms::S;
+  for (int s = 0; s < Ms::S; ++s)
+    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Ms::kind(s, d);
+  r.launch = &launch_mv2<Ms>;
+  r.pack = &pack_mv2<Ms>;
+  return r;
+}
+
+// <N_u, N_v, N_w, nq_u, nq_v, nq_w, threads, term kinds...>
+const std::vector<MV2Entry>& mv2_registry() {
+  static const std::vector<MV2Entry> reg = {
+      make_mv2<MShape<4, 4, 4, 8, 8, 8, 128, kPPP>>(),                    // C1
+      make_mv2<MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),           // C2
+      make_mv2<MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),           // C3
+      make_mv2<MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>>(),          // C4
+      make_mv2<MShape<3, 3, 3, 6, 6, 6, 128, kPPP, kDDD>>(),              // test shapes
+      make_mv2<MShape<4, 3, 3, 9, 5, 7, 128, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
+      make_mv2<MShape<5, 5, 5, 9, 9, 9, 128, kPPP, kDDD>>(),
+  };
+  return reg;
+}
+
+}  // namespace reg
+}  // namespace p2s

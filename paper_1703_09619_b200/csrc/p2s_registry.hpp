@@ -1,0 +1,139 @@
+// p2s_registry.hpp -- the shape registries shared by the C-ABI (p2s_capi.cu)
+// and the translation units that instantiate the kernels (p2s_reg_*.cu, built
+// in parallel): entry structs, launch / pack function types and accessors.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "../../include/p2s_b200.h"
+#include "p2s_kernels.cuh"
+#include "p2s_tables.hpp"
+
+namespace p2s {
+namespace reg {
+
+struct ContractArgs {
+  const double* I;
+  double* M;
+  int64_t ldM, n_tot, n_elem;
+  int nc, P, Nv, Nw, Nt;
+  int S;
+  int Kv[kMaxTerms], Kw[kMaxTerms], kind_v[kMaxTerms], kind_w[kMaxTerms];
+  int64_t mom_per_elem, mom_per_pair, mom_off[kMaxTerms];
+  const double* Cv[kMaxTerms];
+  const double* Cw[kMaxTerms];
+  const double* cu_packed;  // host, Cfg-packed
+};
+
+struct Plan {  // per-context launch geometry of the contraction
+  int G, NG, threads;
+  size_t smem;
+};
+
+using contract_fn = cudaError_t (*)(const ContractArgs&, const Plan&, cudaStream_t);
+
+struct RegEntry {
+  int NU, S;
+  int kinds[kMaxTerms];
+  contract_fn launch;
+  std::vector<double> (*pack)(const std::vector<const std::vector<double>*>&);
+  int ktot;
+};
+
+struct V2Args {
+  const double* I;
+  double* M;
+  int64_t ldM, n_tot, n_elem, mom_per_elem;
+  int nc, P, Nt;
+  const std::vector<double>* dense[kMaxTerms][3];  // [N][N][K] per term, direction
+  const double* amma;                              // device stage-C A (MMA shapes)
+};
+
+using v2_fn = cudaError_t (*)(const V2Args&, const std::vector<double>&, cudaStream_t, int);
+
+using v2_pack_fn = std::vector<double> (*)(const V2Args&);
+
+struct V2Entry {
+  int order[3];
+  int S;
+  int kinds[kMaxTerms][3];
+  v2_fn launch;
+  v2_pack_fn pack;
+  v2_pack_fn mma_pack;
+  size_t smem;
+  const char* desc;
+};
+
+using mv2_fn = cudaError_t (*)(const double*, double*, int64_t, int, int64_t,
+                               const std::vector<double>&, cudaStream_t);
+
+using mv2_pack_fn = std::vector<double> (*)(const std::vector<double> (*)[3]);
+
+struct MV2Entry {
+  int order[3], nq[3], S;
+  int kinds[kMaxTerms][3];
+  mv2_fn launch;
+  mv2_pack_fn pack;
+};
+
+using fused_fn = cudaError_t (*)(const double*, double*, int64_t, int64_t, int64_t, int, int, int,
+                                 const std::vector<double>&, const std::vector<double>&,
+                                 const double*, cudaStream_t, int);
+
+struct FusedEntry {
+  int order[3], nq[3], S;
+  int kinds[kMaxTerms][3];
+  fused_fn launch;
+  fused_fn launch_geo;          // coupling factors from geometry records, per unit
+  fused_fn launch_geo_cluster;  // ... shared per element through a cluster (DSMEM)
+  v2_pack_fn cpack;
+  mv2_pack_fn mpack;
+  v2_pack_fn mma_pack;
+  const char* desc;
+};
+
+struct LargeArgs {
+  const std::vector<double> (*phi)[3];            // [s][d] full tables
+  const std::vector<double>* dense[kMaxTerms][3];  // [s][d] [N][N][K]
+};
+
+struct LargePack {
+  std::vector<double> tab, cu, cvw;
+  double* d_cvw = nullptr;
+  // runtime: parity-split u stage; v/w of chunk i+1 on `aux` overlapping u of
+  // chunk i on the caller's stream (X double-buffered), ordered by events
+  bool ps = true, overlap = true;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_vw[2]{}, ev_u[2]{};
+};
+
+using large_pack_fn = bool (*)(const LargeArgs&, LargePack&);
+
+using large_mom_fn = cudaError_t (*)(const double*, double*, int64_t, const LargePack&, cudaStream_t);
+
+using large_con_fn = cudaError_t (*)(const double*, double*, double*, int64_t, int64_t, int64_t, int,
+                                     int, int, const LargePack&, cudaStream_t);
+
+struct LargeEntry {
+  int order[3], nq[3], S;
+  int kinds[kMaxTerms][3];
+  large_pack_fn pack;
+  large_mom_fn moments;
+  large_con_fn contract;
+  int64_t mpp, xpu;
+};
+
+// accessors (one translation unit each)
+const std::vector<RegEntry>& registry();         // p2s_reg_generic.cu
+const std::vector<V2Entry>& v2_registry();       // p2s_reg_v2.cu
+const std::vector<MV2Entry>& mv2_registry();     // p2s_reg_v2.cu
+const std::vector<FusedEntry>& fused_registry(); // p2s_reg_fused.cu
+const std::vector<LargeEntry>& large_registry(); // p2s_reg_large.cu
+// runtime-shaped moment kernel (p2s_reg_generic.cu)
+cudaError_t launch_moments(int kmax, const MomentParams& p, size_t smem, cudaStream_t st);
+
+}  // namespace reg
+}  // namespace p2s

@@ -1,16 +1,18 @@
-"""Registers / spills per kernel from the ptxas -v log of the build
-(build/csrc/p2s_capi.ptxas.log).  Usage: python tools/ptxas_summary.py [filter]"""
+"""Registers / spills per kernel from the ptxas -v logs of the build
+(build/csrc/*.ptxas.log).  Usage: python tools/ptxas_summary.py [filter]"""
+import glob
 import re
 import subprocess
 import sys
 
-log = open("build/csrc/p2s_capi.ptxas.log").read()
+log = "\n".join(open(f).read() for f in sorted(glob.glob("build/csrc/*.ptxas.log")))
 flt = sys.argv[1] if len(sys.argv) > 1 else ""
 cur = None
 for line in log.splitlines():
     m = re.search(r"Compiling entry function '(\S+)'", line)
     if m:
         cur = subprocess.run(["c++filt", m.group(1)], capture_output=True, text=True).stdout.strip()
+        cur = re.sub(r"\(anonymous namespace\)::", "", cur)
         cur = re.sub(r"\(int\)|p2s::|\(.*\)$", "", cur)
         continue
     if cur and "spill stores" in line:
