@@ -447,7 +447,8 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
   if (prop.major != 10)
     return fail(P2S_CUDA_ERROR, std::string("p2s_create: built for sm_100a, device is ") + prop.name);
 
-  auto c = std::make_unique<p2s_ctx>();
+  // every early return below releases what was allocated so far
+  std::unique_ptr<p2s_ctx, void (*)(p2s_ctx*)> c(new p2s_ctx, &p2s_destroy);
   c->pb = *spec;
   c->device = device;
   c->entry = entry;

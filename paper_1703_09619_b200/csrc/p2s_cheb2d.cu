@@ -256,7 +256,8 @@ p2s_status p2s_cheb2d_create(const p2s_cheb2d_problem* spec, int device, p2s_che
     return p2s_internal_fail(P2S_CUDA_ERROR, "p2s_cheb2d_create: no CUDA device (no CPU fallback)");
   if (device < 0 || device >= ndev) return p2s_internal_fail(P2S_INVALID_ARG, "bad device");
   if (cudaSetDevice(device) != cudaSuccess) return p2s_internal_fail(P2S_CUDA_ERROR, "cudaSetDevice");
-  auto c = std::make_unique<p2s_cheb2d_ctx>();
+  // early returns below free the device tables uploaded so far
+  std::unique_ptr<p2s_cheb2d_ctx, void (*)(p2s_cheb2d_ctx*)> c(new p2s_cheb2d_ctx, &p2s_cheb2d_destroy);
   c->pb = *spec;
   c->device = device;
   std::vector<double> x, w;
