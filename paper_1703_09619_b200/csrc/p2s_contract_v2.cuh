@@ -47,6 +47,7 @@ struct Shape {
   // MMA (bit 4): stage C as FP64 tensor-core GEMMs (p2s_mma.cuh) instead of
   // the banded register form; FPT is unused then.
   static constexpr int MMA = (FLAGS_ >> 4) & 1;
+  static constexpr bool WLAST = false;  // u-last contraction (p2s_contract_wl.cuh: w-last)
   // PAIR (bit 5): a thread's stage-C fibers come in adjacent pairs (f, f+1) of
   // one matrix row, written with one 16-B store (half the store instructions)
   static constexpr int PAIR = (FLAGS_ >> 5) & 1;

@@ -9,6 +9,7 @@
 #include <cooperative_groups.h>
 
 #include "p2s_contract_v2.cuh"
+#include "p2s_contract_wl.cuh"
 #include "p2s_moments_v2.cuh"
 
 namespace p2s {
@@ -149,7 +150,10 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     }
     double* Mbase =
         p.c.M + e * p.c.mat_stride + static_cast<int64_t>(gci * p.c.Nt) * p.c.ldM + gcj * p.c.Nt;
-    v2_unit<Sh>(p.c, Ibuf, Abuf, Bbuf, Mbase, []() {}, mm);
+    if constexpr (Sh::WLAST)
+      wl_unit<Sh>(p.c, Ibuf, Abuf, Bbuf, Mbase);
+    else
+      v2_unit<Sh>(p.c, Ibuf, Abuf, Bbuf, Mbase, []() {}, mm);
   };
   if constexpr (Sh::PERSIST) {
     for (int64_t unit = blockIdx.x; unit < p.c.n_units; unit += gridDim.x) do_unit(unit, gridDim.x);

@@ -56,7 +56,8 @@ inline int vec2_ok(const double* M, int64_t ldM) {
 
 template <class Sh>
 constexpr const char* stage_c_desc() {
-  return Sh::MMA     ? "stage C on DMMA"
+  return Sh::WLAST   ? "w-last contraction"
+         : Sh::MMA  ? "stage C on DMMA"
          : Sh::PSPLIT ? (Sh::PAIR ? "banded stage C, parity split, paired 16-B stores"
                                   : "banded stage C, parity split")
          : Sh::PAIR   ? "banded stage C, paired 16-B stores"

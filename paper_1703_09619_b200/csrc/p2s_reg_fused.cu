@@ -154,6 +154,11 @@ const std::vector<FusedEntry>& fused_registry() {
       // C2 in the conforming basis
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kCPPP, kCDDD>,
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+      // C4 w-last contraction (p2s_contract_wl.cuh): 4 (TM 11), 5 (TM 55 = one tile)
+      make_fused<WShape<10, 6, 4, 11, 192, 2, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
+      make_fused<WShape<10, 6, 4, 19, 256, 2, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>>(),
       // test shapes
       make_fused<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>,
                  MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),
