@@ -142,7 +142,11 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 22, 1, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
-      // C4: 0 parity split (default), 1 banded, 2 paired stores, 3 DMMA
+      // C4: 0 parity split, all six n1 per tile, 2 fibers / thread (default: every
+      // constant-bank coefficient feeds two DFMAs; 1 CTA of 288 threads per SM),
+      // 1 parity split with n1 tiles of 2 (2 CTAs/SM), 2 banded, 3 paired stores, 4 DMMA
+      make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 70, 2, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 70, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
@@ -154,7 +158,7 @@ const std::vector<FusedEntry>& fused_registry() {
       // C2 in the conforming basis
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kCPPP, kCDDD>,
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
-      // C4 w-last contraction (p2s_contract_wl.cuh): 4 (TM 11), 5 (TM 55 = one tile)
+      // C4 w-last contraction (p2s_contract_wl.cuh): 5 (TM 11), 6 (TM 19)
       make_fused<WShape<10, 6, 4, 11, 192, 2, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
       make_fused<WShape<10, 6, 4, 19, 256, 2, kPPP, kDDD>,
