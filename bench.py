@@ -329,7 +329,7 @@ def run_b200(args, cfg):
     fused = stages["n_moments"] == 0 and stages["n_contract"] > 0
     path = ctx.kernel_path
     kname = ("fill_fused_kernel" if fused else
-             "large_vw_kernel + large_u_kernel" if path.startswith("large") else
+             "large_w_kernel + large_v_kernel + large_u_kernel" if path.startswith("large") else
              "contract_v2_kernel" if "contract_v2" in path else "contract_kernel")
     alg_bytes_elem = (counts["bytes_alpha"] + counts["bytes_M"]) if fused else counts["bytes_con"]
     n_con = max(1, stages["n_contract"])

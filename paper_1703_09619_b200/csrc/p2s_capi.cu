@@ -401,7 +401,7 @@ const char* p2s_version(void) { return "p2s_b200 0.1 (sm_100a)"; }
 
 const char* p2s_kernel_path(const p2s_ctx* c) {
   if (!c) return "";
-  if (c->large) return "large-order: large_moments_kernel + large_vw_kernel + large_u_kernel";
+  if (c->large) return "large-order: large_moments_kernel + large_w_kernel + large_v_kernel + large_u_kernel";
   static thread_local std::string path;
   if (c->fused) {
     path = std::string("fused: fill_fused_kernel (moments + contraction; ") + c->fused->desc + ")";
@@ -575,7 +575,7 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     for (int s = 0; s < S; ++s)
       for (int d = 0; d < 3; ++d) la.dense[s][d] = &c->coef[s][d];
     if (!lge->pack(la, c->lpack)) return fail(P2S_CUDA_ERROR, "p2s_create: large-path table upload");
-    // X chunk: ~64 MB of triangle-packed intermediates per buffer (two buffers: the
+    // X chunk: ~64 MB of v/w-contracted intermediates per buffer (two buffers: the
     // v/w stage of the next chunk overlaps the u stage of this one)
     int64_t xmb = 64;
     if (const char* v = std::getenv("P2S_XCHUNK_MB")) xmb = std::max(1, std::atoi(v));
@@ -583,8 +583,20 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     if (const char* v = std::getenv("P2S_LARGE_OVERLAP")) c->lpack.overlap = v[0] != '0';
     c->xchunk = std::max<int64_t>(1, (xmb << 20) / (lge->xpu * 8));
     P2S_CUDA(cudaMalloc(&c->d_X, sizeof(double) * lge->xpu * c->xchunk * 2));
-    P2S_CUDA(cudaStreamCreateWithFlags(&c->lpack.aux, cudaStreamNonBlocking));
+    P2S_CUDA(cudaMalloc(&c->lpack.d_Z, sizeof(double) * lge->zpu * c->xchunk));
+    // P2S_LARGE_PRIO=1 puts the v/w steps on a high-priority stream (the block
+    // scheduler then hands retiring u-stage CTA slots to v/w CTAs first); measured
+    // no gain, so off by default
+    int prio_lo = 0, prio_hi = 0;
+    P2S_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    bool hi = false;
+    if (const char* v = std::getenv("P2S_LARGE_PRIO")) hi = v[0] != '0';
+    P2S_CUDA(cudaStreamCreateWithPriority(&c->lpack.aux, cudaStreamNonBlocking, hi ? prio_hi : prio_lo));
+    P2S_CUDA(cudaStreamCreateWithFlags(&c->lpack.aux_u, cudaStreamNonBlocking));
     P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_start, cudaEventDisableTiming));
+    P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_join, cudaEventDisableTiming));
+    if (const char* v = std::getenv("P2S_LARGE_USTREAMS")) c->lpack.two_u = v[0] != '1';
+    if (const char* v = std::getenv("P2S_LARGE_FIB")) c->lpack.ufib = std::atoi(v) == 2 ? 2 : 1;
     for (int b = 0; b < 2; ++b) {
       P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_vw[b], cudaEventDisableTiming));
       P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_u[b], cudaEventDisableTiming));
@@ -612,9 +624,11 @@ void p2s_destroy(p2s_ctx* c) {
     if (c->d_x[d]) cudaFree(c->d_x[d]);
   if (c->d_scratch) cudaFree(c->d_scratch);
   if (c->d_X) cudaFree(c->d_X);
-  if (c->lpack.d_cvw) cudaFree(c->lpack.d_cvw);
+  if (c->lpack.d_Z) cudaFree(c->lpack.d_Z);
   if (c->lpack.aux) cudaStreamDestroy(c->lpack.aux);
+  if (c->lpack.aux_u) cudaStreamDestroy(c->lpack.aux_u);
   if (c->lpack.ev_start) cudaEventDestroy(c->lpack.ev_start);
+  if (c->lpack.ev_join) cudaEventDestroy(c->lpack.ev_join);
   for (int b = 0; b < 2; ++b) {
     if (c->lpack.ev_vw[b]) cudaEventDestroy(c->lpack.ev_vw[b]);
     if (c->lpack.ev_u[b]) cudaEventDestroy(c->lpack.ev_u[b]);

@@ -56,6 +56,18 @@ struct Shape {
   // one after the other; a class reads only the k1 of one parity, so the
   // register-resident fiber halves
   static constexpr int PSPLIT = (FLAGS_ >> 6) & 1;
+  // USYM: every term's u-kind is symmetric in (m1, m2) (PP / DD, either basis),
+  // so Cu[m1][m2] = Cu[m2][m1] and M[m1 n1 p1][m2 n2 p2] = M[m2 n1 p1][m1 n2 p2]:
+  // stage C forms m2 >= m1 only and stores each value at both (m1, m2) and
+  // (m2, m1) -- (N_u + 1) / (2 N_u) of the DFMAs, same stores.  FLAGS bit 7
+  // (NOUSYM) turns it off for A/B measurements.
+  static constexpr bool u_symmetric() {
+    constexpr int k[] = {TK...};
+    for (int s = 0; s < static_cast<int>(sizeof...(TK)); ++s)
+      if (base_kind(k[s] & 7) != PP && base_kind(k[s] & 7) != DD) return false;
+    return true;
+  }
+  static constexpr bool USYM = u_symmetric() && !((FLAGS_ >> 7) & 1);
   static constexpr int AALL = (FLAGS_ & 1) | SYM, ROWLOOP = (FLAGS_ >> 1) & 1;
   static constexpr int NQV = NV_ * (NV_ + 1) / 2, NQW = NW_ * (NW_ + 1) / 2;
   static constexpr int tri(int a, int b, int n) { return a * n - a * (a - 1) / 2 + (b - a); }
@@ -467,9 +479,10 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
         }
         auto row = [&](auto m1c) {
           constexpr int m1 = decltype(m1c)::value;
-          static_for<0, NU>([&](auto m2c) {
+          static_for<(Sh::USYM ? m1 : 0), NU>([&](auto m2c) {
             constexpr int m2 = decltype(m2c)::value;
             if constexpr (PAR < 0 || (m1 + m2) % 2 == PAR) {
+            constexpr bool mirror = Sh::USYM && m2 != m1;  // also store at (m2, m1)
             double v[FPT];
 #pragma unroll
             for (int q = 0; q < FPT; ++q) v[q] = 0.0;
@@ -493,17 +506,28 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
 #pragma unroll
               for (int q = 0; q < FPT; q += 2) {
                 double* d = out[q] + m1 * rowstep + m2 * (NV * NW);
+                double* dm = out[q] + m2 * rowstep + m1 * (NV * NW);
                 if (p.vec2) {
-                  if (live[q]) st_cs2(d, v[q], v[q + 1]);
+                  if (live[q]) {
+                    st_cs2(d, v[q], v[q + 1]);
+                    if constexpr (mirror) st_cs2(dm, v[q], v[q + 1]);
+                  }
                 } else {
                   if (live[q]) st_cs(d, v[q]);
                   if (live[q + 1]) st_cs(d + 1, v[q + 1]);
+                  if constexpr (mirror) {
+                    if (live[q]) st_cs(dm, v[q]);
+                    if (live[q + 1]) st_cs(dm + 1, v[q + 1]);
+                  }
                 }
               }
             } else {
 #pragma unroll
               for (int q = 0; q < FPT; ++q)
-                if (live[q]) st_cs(out[q] + m1 * rowstep + m2 * (NV * NW), v[q]);
+                if (live[q]) {
+                  st_cs(out[q] + m1 * rowstep + m2 * (NV * NW), v[q]);
+                  if constexpr (mirror) st_cs(out[q] + m2 * rowstep + m1 * (NV * NW), v[q]);
+                }
             }
             }  // parity class
           });

@@ -1,14 +1,15 @@
 // p2s_large.cuh -- large-order path (C5: N = 16, K = 31 / 29, 36^3 points),
 // where one element's moment block (433 KB) and intermediates do not fit a
-// CTA's shared memory.  Three kernels per chunk of elements:
+// CTA's shared memory.  Kernels per chunk of elements:
 //   large_moments_kernel  I_s[k1][k2][k3], one CTA per (unit, term, k1 chunk)
 //                         (three even/odd-folded 1-D passes as in
 //                         p2s_moments_v2.cuh, pass u restricted to the chunk)
-//   large_vw_kernel       X_s[k1][tri(n1,n2)][tri(p1,p2)] =
-//                         sum_k2 Cv[n1 n2 k2] sum_k3 Cw[p1 p2 k3] I_s[k1][k2][k3]
-//                         one CTA per (unit, term, k1); symmetric v/w kinds, so
-//                         only the (n1<=n2, p1<=p2) triangles are formed; the
-//                         chunk's X stays L2-resident (8.9 MB per C5 element)
+//   large_w_kernel,       X_s[k1][tri(n1,n2)][p1][p2] =
+//   large_v_kernel        sum_k2 Cv[n1 n2 k2] sum_k3 Cw[p1 p2 k3] I_s[k1][k2][k3]
+//                         (w step into Z, then v step; symmetric v kinds, so
+//                         only the n1 <= n2 triangle is formed; full (p1, p2)
+//                         rows for coalesced u-stage loads); the chunk's X stays
+//                         L2-resident (16.7 MB per C5 element)
 //   large_u_kernel        M[m1 n1 p1][m2 n2 p2] = sum_s sum_k1 Cu[m1 m2 k1] X_s[..]
 //                         one CTA per (unit, n1, p1), thread = fiber (n2, p2):
 //                         every warp store is 256 contiguous bytes
@@ -45,13 +46,24 @@ struct LShape {
     return o;
   }
   static constexpr int MPP = (moff(S) + 3) & ~3;
-  // X block of one unit: terms back to back, [K_u][NQV][NQW]
+  // X block of one unit: terms back to back, [K_u][NQV][N_w][N_w] (v triangle,
+  // full (p1, p2): the u stage's lanes read contiguous p2 runs)
   static constexpr int64_t xoff(int s) {
     int64_t o = 0;
-    for (int i = 0; i < s; ++i) o += static_cast<int64_t>(K(i, 0)) * NQV * NQW;
+    for (int i = 0; i < s; ++i) o += static_cast<int64_t>(K(i, 0)) * NQV * NW * NW;
     return o;
   }
   static constexpr int64_t XPU = xoff(S);
+  // Z block of one unit (w-contracted moments): terms back to back,
+  // [K_u][N_w][N_w][K2P], k2 fastest and padded to 32 (one lane per k2)
+  static constexpr int K2P = 32;
+  static constexpr int64_t zoff(int s) {
+    int64_t o = 0;
+    for (int i = 0; i < s; ++i) o += static_cast<int64_t>(K(i, 0)) * NW * NW * K2P;
+    return o;
+  }
+  static constexpr int64_t ZPU = zoff(S);
+  static constexpr int NGRP = (NW + 1) / 2;  // w-step p1 groups {g, N_w-1-g}
   static constexpr int KUTOT() {
     int o = 0;
     for (int s = 0; s < S; ++s) o += K(s, 0);
@@ -111,6 +123,18 @@ struct LShape {
     return true;
   }
   static_assert(sym_ok(), "large path needs symmetric v/w kinds (PP / DD)");
+  // symmetric u-kinds: the u stage forms m2 >= m1 and stores (m1, m2) and (m2, m1)
+  // (as Shape::USYM); -DP2S_LARGE_NOUSYM turns it off for A/B measurements
+  static constexpr bool u_symmetric() {
+    for (int s = 0; s < S; ++s)
+      if (base_kind(kind(s, 0)) != PP && base_kind(kind(s, 0)) != DD) return false;
+    return true;
+  }
+#ifdef P2S_LARGE_NOUSYM
+  static constexpr bool USYM = false;
+#else
+  static constexpr bool USYM = u_symmetric();
+#endif
 };
 
 // ------------------------------------------------------------------ moments
@@ -202,101 +226,132 @@ __global__ void __launch_bounds__(256) large_moments_kernel(const __grid_constan
 }
 
 // ------------------------------------------------------------------ v/w stage
+// Two steps, both "fiber in registers, compile-time bands, constant-bank
+// coefficients, coalesced stores" kernels:
+//   w step  Z_s[k1][p1][p2][k2] = sum_k3 Cw[p1 p2 k3] I_s[k1][k2][k3]
+//           warp = (unit, term, k1, p1 group {g, N_w-1-g}), lane = k2 with the
+//           I row (K_w values) in registers; lanes store consecutive k2
+//   v step  X_s[k1][tri(n1,n2)][p1][p2] = sum_k2 Cv[n1 n2 k2] Z_s[k1][p1][p2][k2]
+//           CTA = (unit, term, k1), thread = (p1, p2) with its Z fiber (K_v
+//           values) in registers; every warp store is 256 contiguous bytes
+// (w first: its fibers are the K_v rows of I, the v step's the N_w^2 rows of Z,
+// so the wide n1 <= n2 triangle is produced by the step with the most threads.)
 
 template <class Ls>
-struct LVWParams {
+struct LWParams {
   const double* I;      // [units][MPP]
-  double* X;            // [units][XPU]
-  const double* cvw;    // global band-packed Cv then Cw (copied to smem per CTA)
+  double* Z;            // [units][ZPU]
   int64_t n_units;
+  double cw[Ls::ctot(2)];
 };
 
 template <class Ls>
-constexpr size_t large_vw_smem() {
-  return sizeof(double) * (size_t)(Ls::KMAX(1) * Ls::KMAX(2) + Ls::NQV * Ls::KMAX(2) +
-                                   Ls::ctot(1) + Ls::ctot(2) + 2);
-}
+struct LVParams {
+  const double* Z;
+  double* X;            // [units][XPU]
+  int64_t n_units;
+  double cv[Ls::ctot(1)];
+};
 
 template <class Ls, int s>
-__device__ __forceinline__ void large_vw_term(const LVWParams<Ls>& p, int64_t unit, int k1, double* sm) {
-  constexpr int NV = Ls::NV, NW = Ls::NW, NQV = Ls::NQV, NQW = Ls::NQW;
-  constexpr int KV = Ls::K(s, 1), KW = Ls::K(s, 2);
-  constexpr int kv = Ls::kind(s, 1), kw = Ls::kind(s, 2);
-  constexpr int NT = 256;
-  double* Is = sm;                                   // [KV][KW]
-  double* Y = Is + Ls::KMAX(1) * Ls::KMAX(2);        // [NQV][KW]
-  const double* cv = Y + NQV * Ls::KMAX(2);          // band-packed Cv (smem copy)
-  const double* cw = cv + Ls::ctot(1);
-  const double* src = p.I + unit * Ls::MPP + Ls::moff(s) + k1 * KV * KW;
-  for (int i = threadIdx.x; i < KV * KW; i += NT) Is[i] = src[i];
-  __syncthreads();
-  // stage A: Y[tri(n1,n2)][k3], thread = (n1, k3), outputs n2 >= n1 (runtime n1,
-  // compile-time n2 via dispatch on n1)
-  // runtime loops here (coefficients come from smem, nothing to hoist); unrolled
-  // rounds would multiply the 136-output dispatch code and thrash the I-cache
-  for (int r = threadIdx.x; r < NV * KW; r += NT) {
-    const int n1 = r / KW, k3 = r - (r / KW) * KW;
-    double x[KV];
+__device__ __forceinline__ void large_w_row(const LWParams<Ls>& p, const double* cw, int64_t unit, int k1,
+                                            int g, int lane) {
+  constexpr int NW = Ls::NW, K2P = Ls::K2P;
+  constexpr int KV = Ls::K(s, 1), KW = Ls::K(s, 2), kw = Ls::kind(s, 2);
+  static_assert(KV <= K2P, "w step maps k2 to lanes");
+  if (lane >= KV) return;
+  const double* src = p.I + unit * Ls::MPP + Ls::moff(s) + (k1 * KV + lane) * KW;
+  double y[KW];
 #pragma unroll
-    for (int k2 = 0; k2 < KV; ++k2) x[k2] = Is[k2 * KW + k3];
-    static_for<0, NV>([&](auto n1c) {
-      constexpr int a = decltype(n1c)::value;
-      if (n1 == a) {
-        static_for<a, NV>([&](auto n2c) {
-          constexpr int b = decltype(n2c)::value;
-          constexpr int lo = band_lo(kv, a, b), cnt = band_count(kv, a, b);
-          constexpr int co = Ls::coff(1, s, a, b) - Ls::coff(1, 0, 0, 0);
-          double v = 0.0;
-          static_for<0, cnt>([&](auto jc) {
-            constexpr int j = decltype(jc)::value;
-            v = fma(cv[co + j], x[lo + band_step(kv, a, b) * j], v);
-          });
-          Y[Ls::tri(a, b, NV) * KW + k3] = v;
-        });
-      }
+  for (int k3 = 0; k3 < KW; ++k3) y[k3] = src[k3];
+  double* Zk = p.Z + unit * Ls::ZPU + Ls::zoff(s) + static_cast<int64_t>(k1) * NW * NW * K2P + lane;
+  auto prow = [&](auto p1c) {
+    constexpr int a = decltype(p1c)::value;
+    static_for<0, NW>([&](auto p2c) {
+      constexpr int b = decltype(p2c)::value;
+      constexpr int lo = band_lo(kw, a, b), cnt = band_count(kw, a, b);
+      constexpr int co = Ls::coff(2, s, a, b);
+      double v = 0.0;
+      static_for<0, cnt>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        v = fma(cw[co + j], y[lo + band_step(kw, a, b) * j], v);
+      });
+      Zk[(a * NW + b) * K2P] = v;
     });
-  }
+  };
+  // rows g and N_w-1-g (one each per group: balanced band work)
+  static_for<0, Ls::NGRP>([&](auto gc) {
+    constexpr int gg = decltype(gc)::value;
+    if (g == gg) {
+      prow(std::integral_constant<int, gg>{});
+      if constexpr (NW - 1 - gg != gg) prow(std::integral_constant<int, NW - 1 - gg>{});
+    }
+  });
+}
+
+// w step: coefficients staged in shared memory (one copy per CTA, uniform-address
+// broadcast reads): its warps work on different p1 rows at once, and as
+// constant-bank operands the N = 16 table (26 KB) missed the constant cache
+// (LDCU short-scoreboard / MIO-throttle stalls, 4 % issue; 30 -> 24 us per
+// 4-element chunk).  The v and u steps walk their rows in lockstep and keep
+// constant-bank operands (staging them in shared memory measured 1.5-1.9x slower).
+template <class Ls, class Cf>
+__device__ __forceinline__ void stage_coefficients(const Cf (&c), double* sm) {
+  constexpr int n = static_cast<int>(sizeof(Cf) / sizeof(double));
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = c[i];
   __syncthreads();
-  // stage B: X[qv][tri(p1,p2)], thread = (qv, p1)
-  double* Xo = p.X + unit * Ls::XPU + Ls::xoff(s) + static_cast<int64_t>(k1) * NQV * NQW;
-  for (int r = threadIdx.x; r < NQV * NW; r += NT) {
-    const int p1 = r / NQV, qv = r - (r / NQV) * NQV;   // p1 warp-uniform (dispatch below)
-    double y[KW];
-#pragma unroll
-    for (int k3 = 0; k3 < KW; ++k3) y[k3] = Y[qv * KW + k3];
-    double* o = Xo + static_cast<int64_t>(qv) * NQW;
-    static_for<0, NW>([&](auto p1c) {
-      constexpr int a = decltype(p1c)::value;
-      if (p1 == a) {
-        static_for<a, NW>([&](auto p2c) {
-          constexpr int b = decltype(p2c)::value;
-          constexpr int lo = band_lo(kw, a, b), cnt = band_count(kw, a, b);
-          constexpr int co = Ls::coff(2, s, a, b) - Ls::coff(2, 0, 0, 0);
-          double v = 0.0;
-          static_for<0, cnt>([&](auto jc) {
-            constexpr int j = decltype(jc)::value;
-            v = fma(cw[co + j], y[lo + band_step(kw, a, b) * j], v);
-          });
-          o[Ls::tri(a, b, NW)] = v;
-        });
-      }
-    });
-  }
 }
 
 template <class Ls>
-__global__ void __launch_bounds__(256) large_vw_kernel(const __grid_constant__ LVWParams<Ls> p) {
-  extern __shared__ __align__(16) double sm[];
-  const int64_t b = blockIdx.x;
-  const int row = static_cast<int>(b % Ls::KUTOT());
-  const int64_t unit = b / Ls::KUTOT();
-  // coefficient copy to smem (after the I slab and Y)
-  double* cvs = sm + Ls::KMAX(1) * Ls::KMAX(2) + Ls::NQV * Ls::KMAX(2);
-  for (int i = threadIdx.x; i < Ls::ctot(1) + Ls::ctot(2); i += 256) cvs[i] = __ldg(p.cvw + i);
+__global__ void __launch_bounds__(32 * Ls::NGRP) large_w_kernel(const __grid_constant__ LWParams<Ls> p) {
+  extern __shared__ __align__(16) double csm[];
+  stage_coefficients<Ls>(p.cw, csm);
+  const int lane = threadIdx.x & 31, g = threadIdx.x / 32;
+  const int row = static_cast<int>(blockIdx.x % Ls::KUTOT());
+  const int64_t unit = blockIdx.x / Ls::KUTOT();
   static_for<0, Ls::S>([&](auto sc) {
     constexpr int s = decltype(sc)::value;
     if (row >= Ls::kuoff(s) && row < Ls::kuoff(s) + Ls::K(s, 0))
-      large_vw_term<Ls, s>(p, unit, row - Ls::kuoff(s), sm);
+      large_w_row<Ls, s>(p, csm, unit, row - Ls::kuoff(s), g, lane);
+  });
+}
+
+template <class Ls>
+__global__ void __launch_bounds__(Ls::NW * Ls::NW) large_v_kernel(const __grid_constant__ LVParams<Ls> p) {
+  constexpr int NV = Ls::NV, NW = Ls::NW, NQV = Ls::NQV, K2P = Ls::K2P;
+  const int64_t b = blockIdx.x;
+  const int row = static_cast<int>(b % Ls::KUTOT());
+  const int64_t unit = b / Ls::KUTOT();
+  const int t = threadIdx.x;  // p1 * N_w + p2
+  static_for<0, Ls::S>([&](auto sc) {
+    constexpr int s = decltype(sc)::value;
+    constexpr int KV = Ls::K(s, 1), kv = Ls::kind(s, 1);
+    if (row < Ls::kuoff(s) || row >= Ls::kuoff(s) + Ls::K(s, 0)) return;
+    const int k1 = row - Ls::kuoff(s);
+    const double2* src = reinterpret_cast<const double2*>(
+        p.Z + unit * Ls::ZPU + Ls::zoff(s) + (static_cast<int64_t>(k1) * NW * NW + t) * K2P);
+    double z[(KV + 1) & ~1];
+#pragma unroll
+    for (int q = 0; q < (KV + 1) / 2; ++q) {
+      const double2 v = src[q];
+      z[2 * q] = v.x;
+      z[2 * q + 1] = v.y;
+    }
+    double* Xk = p.X + unit * Ls::XPU + Ls::xoff(s) + static_cast<int64_t>(k1) * NQV * NW * NW + t;
+    static_for<0, NV>([&](auto n1c) {
+      constexpr int a = decltype(n1c)::value;
+      static_for<a, NV>([&](auto n2c) {
+        constexpr int c = decltype(n2c)::value;
+        constexpr int lo = band_lo(kv, a, c), cnt = band_count(kv, a, c);
+        constexpr int co = Ls::coff(1, s, a, c);
+        double v = 0.0;
+        static_for<0, cnt>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          v = fma(p.cv[co + j], z[lo + band_step(kv, a, c) * j], v);
+        });
+        Xk[Ls::tri(a, c, NV) * NW * NW] = v;
+      });
+    });
   });
 }
 
@@ -312,47 +367,61 @@ struct LUParams {
 };
 
 // PS: the (m1, m2) classes of even and odd m1+m2 run one after the other, each
-// holding only the x_s[k1] of its parity (half the registers: 2 CTAs per SM)
-template <class Ls, bool PS>
-__global__ void __launch_bounds__(Ls::NV * Ls::NW, PS ? 2 : 1)
+// holding only the x_s[k1] of its parity (half the registers).
+// FIB fibers per thread: thread (n2, p2) of a CTA of N_v N_w / FIB threads also
+// owns the fibers n2 + i N_v / FIB; every constant-bank coefficient feeds FIB
+// DFMAs (half the LDCU per DFMA at FIB = 2, 3 CTAs of 128 threads per SM).
+template <class Ls, bool PS, int FIB>
+__global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? 2 : 3) : 1)
     large_u_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0) {
-  constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S, NQV = Ls::NQV, NQW = Ls::NQW;
+  constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S, NQV = Ls::NQV;
+  static_assert(NV % FIB == 0, "fibers per thread must divide N_v");
   const int64_t b = blockIdx.x;
   const int np = static_cast<int>(b % (NV * NW));
   const int64_t unit = unit0 + b / (NV * NW);
   const int n1 = np / NW, p1 = np - (np / NW) * NW;
-  const int n2 = threadIdx.x / NW, p2 = threadIdx.x - (threadIdx.x / NW) * NW;
+  const int n2b = threadIdx.x / NW, p2 = threadIdx.x - (threadIdx.x / NW) * NW;
   const int64_t e = unit / p.P;
   const int pair = static_cast<int>(unit - e * p.P);
   const int gci = pair / p.nc, gcj = pair - gci * p.nc;
-  const int qv = n1 <= n2 ? Ls::tri(n1, n2, NV) : Ls::tri(n2, n1, NV);
-  const int qw = p1 <= p2 ? Ls::tri(p1, p2, NW) : Ls::tri(p2, p1, NW);
-  const double* Xu = p.X + (unit - unit0) * Ls::XPU + static_cast<int64_t>(qv) * NQW + qw;
+  const double* Xu[FIB];
+#pragma unroll
+  for (int f = 0; f < FIB; ++f) {
+    const int n2 = n2b + f * (NV / FIB);
+    const int qv = n1 <= n2 ? Ls::tri(n1, n2, NV) : Ls::tri(n2, n1, NV);
+    Xu[f] = p.X + (unit - unit0) * Ls::XPU + (static_cast<int64_t>(qv) * NW + p1) * NW + p2;
+  }
   double* out = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt + n1 * NW + p1) * p.ldM +
-                gcj * p.Nt + n2 * NW + p2;
+                gcj * p.Nt + n2b * NW + p2;
+  constexpr int FSTEP = (NV / FIB) * NW;  // column offset between a thread's fibers
   const int64_t rowstep = static_cast<int64_t>(NV * NW) * p.ldM;
   auto run = [&](auto parc) {
     constexpr int PAR = decltype(parc)::value;  // -1: every (m1, m2)
-    double x[Ls::KX(PAR)];
+    double x[FIB][Ls::KX(PAR)];
     static_for<0, S>([&](auto sc) {
       constexpr int s = decltype(sc)::value;
-      if constexpr (PAR < 0) {
 #pragma unroll
-        for (int k1 = 0; k1 < Ls::K(s, 0); ++k1)
-          x[Ls::kuoff(s) + k1] = __ldg(Xu + Ls::xoff(s) + static_cast<int64_t>(k1) * NQV * NQW);
-      } else {
+      for (int f = 0; f < FIB; ++f) {
+        if constexpr (PAR < 0) {
 #pragma unroll
-        for (int j = 0; j < Ls::ucnt(s, PAR); ++j)
-          x[Ls::kpo(s, PAR) + j] = __ldg(
-              Xu + Ls::xoff(s) + static_cast<int64_t>(Ls::uk0(s, PAR) + 2 * j) * NQV * NQW);
+          for (int k1 = 0; k1 < Ls::K(s, 0); ++k1)
+            x[f][Ls::kuoff(s) + k1] = __ldg(Xu[f] + Ls::xoff(s) + static_cast<int64_t>(k1) * NQV * NW * NW);
+        } else {
+#pragma unroll
+          for (int j = 0; j < Ls::ucnt(s, PAR); ++j)
+            x[f][Ls::kpo(s, PAR) + j] = __ldg(
+                Xu[f] + Ls::xoff(s) + static_cast<int64_t>(Ls::uk0(s, PAR) + 2 * j) * NQV * NW * NW);
+        }
       }
     });
     auto row = [&](auto m1c) {
       constexpr int m1 = decltype(m1c)::value;
-      static_for<0, NU>([&](auto m2c) {
+      static_for<(Ls::USYM ? m1 : 0), NU>([&](auto m2c) {
         constexpr int m2 = decltype(m2c)::value;
         if constexpr (PAR < 0 || (m1 + m2) % 2 == PAR) {
-          double v = 0.0;
+          double v[FIB];
+#pragma unroll
+          for (int f = 0; f < FIB; ++f) v[f] = 0.0;
           static_for<0, S>([&](auto sc) {
             constexpr int s = decltype(sc)::value;
             constexpr int ku = Ls::kind(s, 0);
@@ -362,10 +431,16 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, PS ? 2 : 1)
               constexpr int j = decltype(jc)::value;
               constexpr int xi = PAR < 0 ? Ls::kuoff(s) + lo + band_step(ku, m1, m2) * j
                                          : Ls::kpo(s, PAR) + (lo - Ls::uk0(s, PAR)) / 2 + j;
-              v = fma(p.cu[co + j], x[xi], v);
+              const double c = p.cu[co + j];
+#pragma unroll
+              for (int f = 0; f < FIB; ++f) v[f] = fma(c, x[f][xi], v[f]);
             });
           });
-          st_cs(out + m1 * rowstep + m2 * (NV * NW), v);
+#pragma unroll
+          for (int f = 0; f < FIB; ++f) {
+            st_cs(out + m1 * rowstep + m2 * (NV * NW) + f * FSTEP, v[f]);
+            if constexpr (Ls::USYM && m2 != m1) st_cs(out + m2 * rowstep + m1 * (NV * NW) + f * FSTEP, v[f]);
+          }
         }
       });
     };
@@ -384,12 +459,15 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, PS ? 2 : 1)
 }
 
 template <class Ls>
-void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps, cudaStream_t st) {
+void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps, int fib, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(cnt * Ls::NV * Ls::NW);
-  if (ps)
-    large_u_kernel<Ls, true><<<grid, Ls::NV * Ls::NW, 0, st>>>(p, unit0);
+  constexpr int T = Ls::NV * Ls::NW;
+  if (ps && fib == 2 && Ls::NV % 2 == 0)
+    large_u_kernel<Ls, true, (Ls::NV % 2 == 0 ? 2 : 1)><<<grid, T / (Ls::NV % 2 == 0 ? 2 : 1), 0, st>>>(p, unit0);
+  else if (ps)
+    large_u_kernel<Ls, true, 1><<<grid, T, 0, st>>>(p, unit0);
   else
-    large_u_kernel<Ls, false><<<grid, Ls::NV * Ls::NW, 0, st>>>(p, unit0);
+    large_u_kernel<Ls, false, 1><<<grid, T, 0, st>>>(p, unit0);
 }
 
 }  // namespace p2s

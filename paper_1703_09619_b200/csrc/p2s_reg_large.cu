@@ -1,4 +1,5 @@
-// p2s_reg_large.cu -- large-order registry (C5: large_moments_kernel, large_vw_kernel, large_u_kernel).
+// p2s_reg_large.cu -- large-order registry (C5: large_moments_kernel, large_w_kernel, large_v_kernel,
+// large_u_kernel).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -49,9 +50,7 @@ bool pack_large(const LargeArgs& a, LargePack& out) {
   out.cvw.assign(static_cast<size_t>(Ls::ctot(1) + Ls::ctot(2)), 0.0);
   band_pack(1, out.cvw, 0);
   band_pack(2, out.cvw, static_cast<size_t>(Ls::ctot(1)));
-  if (cudaMalloc(&out.d_cvw, sizeof(double) * out.cvw.size()) != cudaSuccess) return false;
-  return cudaMemcpy(out.d_cvw, out.cvw.data(), sizeof(double) * out.cvw.size(),
-                    cudaMemcpyHostToDevice) == cudaSuccess;
+  return true;
 }
 
 template <class Ls>
@@ -79,14 +78,6 @@ template <class Ls>
 cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t n_units,
                                   int64_t xchunk, int64_t ldM, int nc, int P, int Nt,
                                   const LargePack& pk, cudaStream_t st) {
-  static bool attr = false;
-  constexpr size_t vw_smem = large_vw_smem<Ls>();
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(large_vw_kernel<Ls>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vw_smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
   LUParams<Ls> up;
   up.M = M;
   up.ldM = ldM;
@@ -95,37 +86,52 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
   up.P = P;
   up.Nt = Nt;
   std::memcpy(up.cu, pk.cu.data(), sizeof(double) * Ls::ctot(0));
+  LWParams<Ls> wp;
+  wp.Z = pk.d_Z;
+  std::memcpy(wp.cw, pk.cvw.data() + Ls::ctot(1), sizeof(double) * Ls::ctot(2));
+  LVParams<Ls> vp;
+  vp.Z = pk.d_Z;
+  std::memcpy(vp.cv, pk.cvw.data(), sizeof(double) * Ls::ctot(1));
   // X holds two chunk buffers; chunk i uses buffer i % 2
   const bool ov = pk.overlap && pk.aux != nullptr;
+  const bool two = ov && pk.two_u && pk.aux_u != nullptr && n_units > xchunk;
   cudaError_t e;
   if (ov) {
     if ((e = cudaEventRecord(pk.ev_start, st)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(pk.aux, pk.ev_start, 0)) != cudaSuccess) return e;  // I ready
+    if (two && (e = cudaStreamWaitEvent(pk.aux_u, pk.ev_start, 0)) != cudaSuccess) return e;
   }
   int64_t i = 0;
   for (int64_t u0 = 0; u0 < n_units; u0 += xchunk, ++i) {
     const int64_t cnt = std::min(xchunk, n_units - u0);
     const int b = static_cast<int>(i % 2);
     double* Xb = X + (ov ? b : 0) * xchunk * Ls::XPU;
-    LVWParams<Ls> vp;
-    vp.I = I + u0 * Ls::MPP;
+    wp.I = I + u0 * Ls::MPP;
+    wp.n_units = vp.n_units = cnt;
     vp.X = Xb;
-    vp.cvw = pk.d_cvw;
-    vp.n_units = cnt;
     cudaStream_t vs = ov ? pk.aux : st;
     if (ov && i >= 2 && (e = cudaStreamWaitEvent(pk.aux, pk.ev_u[b], 0)) != cudaSuccess) return e;
-    large_vw_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), 256, vw_smem, vs>>>(vp);
+    // w step then v step (Z single-buffered: both on the same stream)
+    large_w_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), 32 * Ls::NGRP,
+                         sizeof(double) * Ls::ctot(2), vs>>>(wp);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    large_v_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), Ls::NW * Ls::NW, 0, vs>>>(vp);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    cudaStream_t us = (two && b == 1) ? pk.aux_u : st;
     if (ov) {
       if ((e = cudaEventRecord(pk.ev_vw[b], pk.aux)) != cudaSuccess) return e;
-      if ((e = cudaStreamWaitEvent(st, pk.ev_vw[b], 0)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(us, pk.ev_vw[b], 0)) != cudaSuccess) return e;
     }
     // u stage: absolute units u0 .. u0+cnt-1; Xb holds the chunk
     up.X = Xb;
     up.n_units = cnt;
-    large_u_dispatch<Ls>(up, u0, cnt, pk.ps, st);
+    large_u_dispatch<Ls>(up, u0, cnt, pk.ps, pk.ufib, us);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (ov && (e = cudaEventRecord(pk.ev_u[b], st)) != cudaSuccess) return e;
+    if (ov && (e = cudaEventRecord(pk.ev_u[b], us)) != cudaSuccess) return e;
+  }
+  if (two) {  // join: the caller's stream sees every u stage
+    if ((e = cudaEventRecord(pk.ev_join, pk.aux_u)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st, pk.ev_join, 0)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
@@ -146,6 +152,7 @@ LargeEntry make_large() {
   r.contract = &launch_large_contract<Ls>;
   r.mpp = Ls::MPP;
   r.xpu = Ls::XPU;
+  r.zpu = Ls::ZPU;
   return r;
 }
 

@@ -101,13 +101,16 @@ struct LargeArgs {
 };
 
 struct LargePack {
-  std::vector<double> tab, cu, cvw;
-  double* d_cvw = nullptr;
+  std::vector<double> tab, cu, cvw;  // cvw: band-packed Cv then Cw (kernel parameters)
+  double* d_Z = nullptr;             // w-step output of one chunk (ZPU x xchunk doubles)
   // runtime: parity-split u stage; v/w of chunk i+1 on `aux` overlapping u of
-  // chunk i on the caller's stream (X double-buffered), ordered by events
-  bool ps = true, overlap = true;
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_vw[2]{}, ev_u[2]{};
+  // chunk i (X double-buffered), ordered by events; two_u: the u stages of
+  // consecutive chunks alternate between the caller's stream and `aux_u`, so the
+  // tail wave of one overlaps the start of the next
+  bool ps = true, overlap = true, two_u = true;
+  int ufib = 1;  // u-stage fibers per thread (P2S_LARGE_FIB; 2 measured 18 % slower)
+  cudaStream_t aux = nullptr, aux_u = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_join = nullptr, ev_vw[2]{}, ev_u[2]{};
 };
 
 using large_pack_fn = bool (*)(const LargeArgs&, LargePack&);
@@ -123,7 +126,7 @@ struct LargeEntry {
   large_pack_fn pack;
   large_mom_fn moments;
   large_con_fn contract;
-  int64_t mpp, xpu;
+  int64_t mpp, xpu, zpu;
 };
 
 // accessors (one translation unit each)

@@ -210,6 +210,24 @@ def test_large_order_path_small_shape(n_comp):
                 O.ALPHA_JACOBIAN if n_comp == 3 else O.ALPHA_SINE, 0.5, 3.0, n_elem=5)
 
 
+@pytest.mark.parametrize("env", [
+    {"P2S_XCHUNK_MB": "1"},                                 # many chunks, two u streams
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_USTREAMS": "1"},      # many chunks, one u stream
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_OVERLAP": "0"},       # serial v/w and u stages
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_PS": "0"},            # u stage without parity split
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_FIB": "2"},           # two u fibers per thread
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_PRIO": "1"},          # high-priority v/w stream
+])
+def test_large_order_path_chunk_schedules(env, monkeypatch):
+    # the chunked v/w -> u pipeline over many X chunks (double buffer reuse,
+    # alternating u streams) gives the oracle's matrices
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    ctx = capi.Context(3, (5, 4, 3), [PP, DD], (8, 8, 6))
+    assert ctx.kernel_path.startswith("large-order")
+    _check_case(3, (5, 4, 3), [PP, DD], (8, 8, 6), O.ALPHA_JACOBIAN, 0.5, 3.0, n_elem=40)
+
+
 def test_c5_matches_oracle():
     # BASELINE config 5 (order 16, 36^3 points): 134 MB per element matrix
     cfg = CONFIGS["c5"]
