@@ -577,7 +577,7 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     if (!lge->pack(la, c->lpack)) return fail(P2S_CUDA_ERROR, "p2s_create: large-path table upload");
     // X chunk: ~64 MB of v/w-contracted intermediates per buffer (two buffers: the
     // v/w stage of the next chunk overlaps the u stage of this one)
-    int64_t xmb = 64;
+    int64_t xmb = 96;
     if (const char* v = std::getenv("P2S_XCHUNK_MB")) xmb = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("P2S_LARGE_PS")) c->lpack.ps = v[0] != '0';
     if (const char* v = std::getenv("P2S_LARGE_OVERLAP")) c->lpack.overlap = v[0] != '0';

@@ -289,30 +289,25 @@ __device__ __forceinline__ void large_w_row(const LWParams<Ls>& p, const double*
   });
 }
 
-// w step: coefficients staged in shared memory (one copy per CTA, uniform-address
-// broadcast reads): its warps work on different p1 rows at once, and as
-// constant-bank operands the N = 16 table (26 KB) missed the constant cache
-// (LDCU short-scoreboard / MIO-throttle stalls, 4 % issue; 30 -> 24 us per
-// 4-element chunk).  The v and u steps walk their rows in lockstep and keep
-// constant-bank operands (staging them in shared memory measured 1.5-1.9x slower).
-template <class Ls, class Cf>
-__device__ __forceinline__ void stage_coefficients(const Cf (&c), double* sm) {
-  constexpr int n = static_cast<int>(sizeof(Cf) / sizeof(double));
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = c[i];
-  __syncthreads();
-}
+// w step: CTA = 8 warps on 8 consecutive (unit, row) items, all in the same p1
+// group, so the CTA's warps read one small coefficient set (the two p1 rows of
+// the group) in lockstep -- constant-cache hits.  (Mapping the groups to the
+// warps of one row instead put 8 different coefficient regions of the N = 16
+// table (26 KB) on an SM at once: LDCU misses, 4 % issue.)
+constexpr int kLargeWWarps = 8;
 
 template <class Ls>
-__global__ void __launch_bounds__(32 * Ls::NGRP) large_w_kernel(const __grid_constant__ LWParams<Ls> p) {
-  extern __shared__ __align__(16) double csm[];
-  stage_coefficients<Ls>(p.cw, csm);
-  const int lane = threadIdx.x & 31, g = threadIdx.x / 32;
-  const int row = static_cast<int>(blockIdx.x % Ls::KUTOT());
-  const int64_t unit = blockIdx.x / Ls::KUTOT();
+__global__ void __launch_bounds__(32 * kLargeWWarps) large_w_kernel(const __grid_constant__ LWParams<Ls> p) {
+  const int lane = threadIdx.x & 31;
+  const int g = static_cast<int>(blockIdx.x % Ls::NGRP);
+  const int64_t item = static_cast<int64_t>(blockIdx.x / Ls::NGRP) * kLargeWWarps + threadIdx.x / 32;
+  const int row = static_cast<int>(item % Ls::KUTOT());
+  const int64_t unit = item / Ls::KUTOT();
+  if (unit >= p.n_units) return;
   static_for<0, Ls::S>([&](auto sc) {
     constexpr int s = decltype(sc)::value;
     if (row >= Ls::kuoff(s) && row < Ls::kuoff(s) + Ls::K(s, 0))
-      large_w_row<Ls, s>(p, csm, unit, row - Ls::kuoff(s), g, lane);
+      large_w_row<Ls, s>(p, p.cw, unit, row - Ls::kuoff(s), g, lane);
   });
 }
 
@@ -451,6 +446,15 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? 2 : 3)
       });
   };
   if constexpr (PS && !Ls::u_conforming()) {
+    // the odd class's x lines go to L1 while the even class computes
+#pragma unroll
+    for (int f = 0; f < FIB; ++f)
+      static_for<0, S>([&](auto sc) {
+        constexpr int s = decltype(sc)::value;
+#pragma unroll
+        for (int j = 0; j < Ls::ucnt(s, 1); ++j)
+          prefetch_l1(Xu[f] + Ls::xoff(s) + static_cast<int64_t>(Ls::uk0(s, 1) + 2 * j) * NQV * NW * NW);
+      });
     run(std::integral_constant<int, 0>{});
     run(std::integral_constant<int, 1>{});
   } else {

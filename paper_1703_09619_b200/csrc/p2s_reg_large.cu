@@ -112,8 +112,8 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
     cudaStream_t vs = ov ? pk.aux : st;
     if (ov && i >= 2 && (e = cudaStreamWaitEvent(pk.aux, pk.ev_u[b], 0)) != cudaSuccess) return e;
     // w step then v step (Z single-buffered: both on the same stream)
-    large_w_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), 32 * Ls::NGRP,
-                         sizeof(double) * Ls::ctot(2), vs>>>(wp);
+    const int64_t wblocks = (cnt * Ls::KUTOT() + kLargeWWarps - 1) / kLargeWWarps * Ls::NGRP;
+    large_w_kernel<Ls><<<static_cast<unsigned>(wblocks), 32 * kLargeWWarps, 0, vs>>>(wp);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     large_v_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), Ls::NW * Ls::NW, 0, vs>>>(vp);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
