@@ -596,6 +596,9 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_start, cudaEventDisableTiming));
     P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_join, cudaEventDisableTiming));
     if (const char* v = std::getenv("P2S_LARGE_USTREAMS")) c->lpack.two_u = v[0] != '1';
+    c->lpack.u_ctas = 2 * static_cast<int64_t>(c->num_sms);  // persistent u stage, 2 CTAs per SM
+    if (const char* v = std::getenv("P2S_LARGE_UPERSIST"))
+      c->lpack.u_ctas = static_cast<int64_t>(std::max(0, std::atoi(v))) * c->num_sms;
     if (const char* v = std::getenv("P2S_LARGE_FIB")) c->lpack.ufib = std::atoi(v) == 2 ? 2 : 1;
     for (int b = 0; b < 2; ++b) {
       P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_vw[b], cudaEventDisableTiming));

@@ -367,11 +367,9 @@ struct LUParams {
 // owns the fibers n2 + i N_v / FIB; every constant-bank coefficient feeds FIB
 // DFMAs (half the LDCU per DFMA at FIB = 2, 3 CTAs of 128 threads per SM).
 template <class Ls, bool PS, int FIB>
-__global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? 2 : 3) : 1)
-    large_u_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0) {
+__device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, int64_t unit0, int64_t b) {
   constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S, NQV = Ls::NQV;
   static_assert(NV % FIB == 0, "fibers per thread must divide N_v");
-  const int64_t b = blockIdx.x;
   const int np = static_cast<int>(b % (NV * NW));
   const int64_t unit = unit0 + b / (NV * NW);
   const int n1 = np / NW, p1 = np - (np / NW) * NW;
@@ -462,16 +460,28 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? 2 : 3)
   }
 }
 
+template <class Ls, bool PS, int FIB>
+__global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? 2 : 3) : 1)
+    large_u_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
+  // one (unit, n1, p1) tile per CTA, or a grid-stride loop over the tiles when the
+  // grid is smaller (persistent CTAs: P2S_LARGE_UPERSIST CTAs per SM)
+#pragma unroll 1
+  for (int64_t b = blockIdx.x; b < ntiles; b += gridDim.x) large_u_tile<Ls, PS, FIB>(p, unit0, b);
+}
+
 template <class Ls>
-void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps, int fib, cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>(cnt * Ls::NV * Ls::NW);
+void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps, int fib, int64_t max_ctas,
+                      cudaStream_t st) {
+  const int64_t ntiles = cnt * Ls::NV * Ls::NW;
+  const unsigned grid = static_cast<unsigned>(max_ctas > 0 && max_ctas < ntiles ? max_ctas : ntiles);
   constexpr int T = Ls::NV * Ls::NW;
-  if (ps && fib == 2 && Ls::NV % 2 == 0)
-    large_u_kernel<Ls, true, (Ls::NV % 2 == 0 ? 2 : 1)><<<grid, T / (Ls::NV % 2 == 0 ? 2 : 1), 0, st>>>(p, unit0);
+  constexpr int F2 = Ls::NV % 2 == 0 ? 2 : 1;
+  if (ps && fib == 2)
+    large_u_kernel<Ls, true, F2><<<grid, T / F2, 0, st>>>(p, unit0, ntiles);
   else if (ps)
-    large_u_kernel<Ls, true, 1><<<grid, T, 0, st>>>(p, unit0);
+    large_u_kernel<Ls, true, 1><<<grid, T, 0, st>>>(p, unit0, ntiles);
   else
-    large_u_kernel<Ls, false, 1><<<grid, T, 0, st>>>(p, unit0);
+    large_u_kernel<Ls, false, 1><<<grid, T, 0, st>>>(p, unit0, ntiles);
 }
 
 }  // namespace p2s

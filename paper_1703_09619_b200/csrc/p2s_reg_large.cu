@@ -125,7 +125,7 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
     // u stage: absolute units u0 .. u0+cnt-1; Xb holds the chunk
     up.X = Xb;
     up.n_units = cnt;
-    large_u_dispatch<Ls>(up, u0, cnt, pk.ps, pk.ufib, us);
+    large_u_dispatch<Ls>(up, u0, cnt, pk.ps, pk.ufib, pk.u_ctas, us);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ov && (e = cudaEventRecord(pk.ev_u[b], us)) != cudaSuccess) return e;
   }

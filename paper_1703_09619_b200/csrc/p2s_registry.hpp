@@ -108,6 +108,7 @@ struct LargePack {
   // consecutive chunks alternate between the caller's stream and `aux_u`, so the
   // tail wave of one overlaps the start of the next
   bool ps = true, overlap = true, two_u = true;
+  int64_t u_ctas = 0;  // u-stage grid cap (persistent CTAs; 0: one CTA per tile)
   int ufib = 1;  // u-stage fibers per thread (P2S_LARGE_FIB; 2 measured 18 % slower)
   cudaStream_t aux = nullptr, aux_u = nullptr;
   cudaEvent_t ev_start = nullptr, ev_join = nullptr, ev_vw[2]{}, ev_u[2]{};

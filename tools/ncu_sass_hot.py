@@ -25,6 +25,17 @@ for r in recs:
     o = o.split(".")[0]
     op[o] = op.get(o, 0) + int(r["Warp Stall Sampling (All Samples)"])
 print("samples by opcode:", ", ".join(f"{k} {v / tot:.2f}" for k, v in sorted(op.items(), key=lambda x: -x[1])[:12]))
+ex = {}
+for r in recs:
+    toks = r["Source"].split()
+    o = toks[1] if toks and toks[0].startswith("@") and len(toks) > 1 else (toks[0] if toks else "?")
+    try:
+        ex[o] = ex.get(o, 0) + int(r["Instructions Executed"].replace(",", ""))
+    except ValueError:
+        pass
+etot = sum(ex.values()) or 1
+print("executed warp-instructions", etot)
+print("executed by opcode:", ", ".join(f"{k} {v / etot:.3f}" for k, v in sorted(ex.items(), key=lambda x: -x[1])[:16]))
 recs.sort(key=lambda r: -int(r["Warp Stall Sampling (All Samples)"]))
 for r in recs[:top]:
     s = int(r["Warp Stall Sampling (All Samples)"])
