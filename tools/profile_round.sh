@@ -16,6 +16,11 @@ for c in c2 c3 c4; do
       --steps 1 --warmup 3 --n-elem 2048 --no-cpu-baseline --no-e2e --no-ablation \
       > gpurun_out/${R}_ncu_${c}_fused_raw.csv 2> /dev/null
 done
-ncu --set full --clock-control none -k regex:large_u_kernel -s 2 -c 1 --csv --page raw python bench.py --config c5 \
-    --steps 1 --warmup 1 --n-elem 32 --no-cpu-baseline --no-e2e --no-ablation > gpurun_out/${R}_ncu_c5_u_raw.csv 2> /dev/null
+ncu --set full --clock-control none -k regex:large_ -s 4 -c 4 --csv --page raw python bench.py --config c5 \
+    --steps 1 --warmup 1 --n-elem 32 --no-cpu-baseline --no-e2e --no-ablation > gpurun_out/${R}_ncu_c5_raw.csv 2> /dev/null
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 \
+    --csv --log-file gpurun_out/${R}_launches_c5.csv python bench.py --config c5 --steps 1 --warmup 3 --n-elem 48 \
+    --no-cpu-baseline --no-e2e --no-ablation > gpurun_out/${R}_launches_c5.log 2>&1
+for c in c3 c4 c5; do python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --no-ablation \
+    > gpurun_out/${R}_bench_$c.json 2> /dev/null; done
 ls -la gpurun_out/${R}_*
