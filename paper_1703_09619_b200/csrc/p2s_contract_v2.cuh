@@ -68,6 +68,12 @@ struct Shape {
     return true;
   }
   static constexpr bool USYM = u_symmetric() && !((FLAGS_ >> 7) & 1);
+  // QUAD (bit 8): a thread's stage-C fibers come in groups of 4 adjacent columns
+  // of one row, written with one 32-B store (st.global.v4.f64, sm_100)
+  static constexpr int QUAD = (FLAGS_ >> 8) & 1;
+  static_assert(!QUAD || (FPT_ % 4 == 0 && (NV_ * NW_) % 4 == 0 && !PAIR),
+                "QUAD needs FPT and rows divisible by 4 (and excludes PAIR)");
+  static constexpr int VW = QUAD ? 4 : PAIR ? 2 : 1;  // adjacent fibers per vector store
   static constexpr int AALL = (FLAGS_ & 1) | SYM, ROWLOOP = (FLAGS_ >> 1) & 1;
   static constexpr int NQV = NV_ * (NV_ + 1) / 2, NQW = NW_ * (NW_ + 1) / 2;
   static constexpr int tri(int a, int b, int n) { return a * n - a * (a - 1) / 2 + (b - a); }
@@ -199,7 +205,7 @@ struct V2Params {
   int nc, P, Nt;
   int64_t mom_per_elem;
   const double* amma;  // fragment-ordered stage-C A (MMA shapes), else null
-  int vec2;            // M rows 16-B aligned (even ldM, aligned base): paired stores
+  int vec2;            // widest aligned vector store of M rows: 4 (32 B), 2 (16 B) or 1
   double cu[Sh::ctot(0)];
   double cv[Sh::ctot(1)];
   double cw[Sh::ctot(2)];
@@ -434,7 +440,8 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
       // ---- stage C
       constexpr int NF = T * Sh::P1T * NV * NW;  // fibers of the sub-tile
       // thread items: FPT single fibers, or FPT/2 adjacent pairs (PAIR)
-      constexpr int NFT = Sh::PAIR ? (NF / 2 + FPT / 2 - 1) / (FPT / 2) : (NF + FPT - 1) / FPT;
+      constexpr int VW = Sh::VW;
+      constexpr int NFT = (NF / VW + FPT / VW - 1) / (FPT / VW);
       const int64_t rowstep = static_cast<int64_t>(NV * NW) * p.ldM;
       if constexpr (Sh::MMA) {
         stage_c_mma<Sh>(
@@ -467,7 +474,7 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
 #pragma unroll
         for (int q = 0; q < FPT; ++q) {
           // f = ((i*P1T + p1l)*NV + n2)*NW + p2
-          const int f = Sh::PAIR ? 2 * (f0 + (q / 2) * NFT) + (q % 2) : f0 + q * NFT;
+          const int f = VW * (f0 + (q / VW) * NFT) + (q % VW);
           live[q] = f < NF;
           const int fs = live[q] ? f : 0;
           const int r = fs % (NV * NW);
@@ -502,7 +509,17 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
                 for (int q = 0; q < FPT; ++q) v[q] = fma(c, b[q][bi], v[q]);
               });
             });
-            if constexpr (Sh::PAIR) {
+            if constexpr (Sh::QUAD) {
+#pragma unroll
+              for (int q = 0; q < FPT; q += 4) {
+                double* d = out[q] + m1 * rowstep + m2 * (NV * NW);
+                double* dm = out[q] + m2 * rowstep + m1 * (NV * NW);
+                if (live[q]) {  // NF % 4 == 0: a group is live as a whole
+                  st_cs_n(d, &v[q], p.vec2);
+                  if constexpr (mirror) st_cs_n(dm, &v[q], p.vec2);
+                }
+              }
+            } else if constexpr (Sh::PAIR) {
 #pragma unroll
               for (int q = 0; q < FPT; q += 2) {
                 double* d = out[q] + m1 * rowstep + m2 * (NV * NW);

@@ -94,4 +94,24 @@ __device__ __forceinline__ void st_cs2(double* p, double a, double b) {
   __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
 }
 
+// 32-B streaming store of four adjacent doubles (p 32-B aligned; sm_100 STG.256)
+__device__ __forceinline__ void st_cs4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+// four adjacent doubles with the widest store the alignment allows (w = 4, 2 or 1)
+__device__ __forceinline__ void st_cs_n(double* p, const double* v, int w) {
+  if (w >= 4) {
+    st_cs4(p, v[0], v[1], v[2], v[3]);
+  } else if (w == 2) {
+    st_cs2(p, v[0], v[1]);
+    st_cs2(p + 2, v[2], v[3]);
+  } else {
+    st_cs(p, v[0]);
+    st_cs(p + 1, v[1]);
+    st_cs(p + 2, v[2]);
+    st_cs(p + 3, v[3]);
+  }
+}
+
 }  // namespace p2s

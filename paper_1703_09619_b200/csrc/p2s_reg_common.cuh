@@ -50,14 +50,19 @@ std::vector<double> pack_mma(const V2Args& a) {
   }
 }
 
+// widest vector store the M rows allow: 4 (32-B aligned rows), 2 (16-B), else 0
 inline int vec2_ok(const double* M, int64_t ldM) {
-  return (ldM % 2 == 0 && reinterpret_cast<uintptr_t>(M) % 16 == 0) ? 1 : 0;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(M);
+  if (ldM % 4 == 0 && a % 32 == 0) return 4;
+  return (ldM % 2 == 0 && a % 16 == 0) ? 2 : 0;
 }
 
 template <class Sh>
 constexpr const char* stage_c_desc() {
   return Sh::WLAST   ? "w-last contraction"
          : Sh::MMA  ? "stage C on DMMA"
+         : Sh::QUAD   ? (Sh::PSPLIT ? "banded stage C, parity split, 32-B stores"
+                                    : "banded stage C, 32-B stores")
          : Sh::PSPLIT ? (Sh::PAIR ? "banded stage C, parity split, paired 16-B stores"
                                   : "banded stage C, parity split")
          : Sh::PAIR   ? "banded stage C, paired 16-B stores"

@@ -111,7 +111,7 @@ FusedEntry make_fused() {
 
 // <Shape: N_u, N_v, N_w, n1 tile, p1 tile, p1 group, threads, min CTAs/SM, flags, FPT, kinds>
 // flags: 1 AALL, 2 ROWLOOP, 4 SYM, 8 PERSIST, 16 MMA (stage C on DMMA), 32 PAIR (16-B
-// stores), 64 PSPLIT (parity-split stage C).  The first match of a problem is the
+// stores), 64 PSPLIT (parity-split stage C), 128 NOUSYM, 256 QUAD (32-B stores).  The first match of a problem is the
 // default; P2S_FUSED_VARIANT=k selects the k-th (tuning / A-B measurements, see
 // profiles/README.md for the numbers behind each default).
 const std::vector<FusedEntry>& fused_registry() {
@@ -163,6 +163,18 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
       make_fused<WShape<10, 6, 4, 19, 256, 2, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>>(),
+      // 32-B stores (QUAD, flag 256: st.global.v4.f64): C2 variant 6 (FPT 4, spills),
+      // C3 variants 4 (FPT 4; 1.75 M vs 2.21 M default) and 5 (+ parity split; 2.01 M),
+      // C4 variant 7 (parity split, FPT 4; 0.97 M vs 1.11 M): the 4 fibers per thread
+      // cost more (registers) than the halved store count gains
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 260, 4, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 262, 4, kPPP, kDDD>,
+                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 326, 4, kPPP, kDDD>,
+                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
+      make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 326, 4, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
       // test shapes
       make_fused<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>,
                  MShape<3, 3, 3, 6, 6, 6, 96, kPPP, kDDD>>(),

@@ -263,6 +263,10 @@ VARIANT_CASES = [
     ("c3", False, "parity split, paired", 3),
     ("c4", False, "parity split", 3),
     ("c4", False, "w-last", 3),
+    ("c2", False, "32-B stores", 6),
+    ("c3", False, "32-B stores", 3),
+    ("c3", False, "parity split, 32-B stores", 3),
+    ("c4", False, "parity split, 32-B stores", 3),
     ((3, (3, 3, 3), [PP, DD], (6, 6, 6)), True, "parity split", 4),
     ((1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7)), True, "parity split", 4),
     ((3, (3, 3, 3), [PP, DD], (6, 6, 6)), True, "DMMA", 4),
