@@ -18,6 +18,10 @@
 #include "p2s_kernels.cuh"
 #include "p2s_moments_v2.cuh"  // fold_contract
 
+#ifndef P2S_LARGE_FIB2_MINB
+#define P2S_LARGE_FIB2_MINB 2  // CTAs per SM of the two-fiber u stage (3: 170-register cap, spills)
+#endif
+
 namespace p2s {
 
 template <int NU_, int NV_, int NW_, int QU_, int QV_, int QW_, int KC_, int... TK>
@@ -461,7 +465,7 @@ __device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, int64_t unit
 }
 
 template <class Ls, bool PS, int FIB>
-__global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? 2 : 3) : 1)
+__global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? 2 : P2S_LARGE_FIB2_MINB) : 1)
     large_u_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
   // one (unit, n1, p1) tile per CTA, or a grid-stride loop over the tiles when the
   // grid is smaller (persistent CTAs: P2S_LARGE_UPERSIST CTAs per SM)

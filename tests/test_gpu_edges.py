@@ -128,3 +128,39 @@ def test_unsupported_orders_report_unsupported_shape():
     assert not capi.shape_supported(1, (11, 3, 3), [PP], (12, 4, 4))
     with pytest.raises(capi.UnsupportedShape):
         capi.Context(1, (11, 3, 3), [PP], (12, 4, 4))
+
+
+GUARD = 8192  # doubles of canary on each side of the output matrices
+
+
+@pytest.mark.parametrize("problem,env", [
+    ((3, (6, 6, 6), [PP, DD], (14, 14, 14)), {}),                                    # C2 fused
+    ((3, (6, 6, 6), [PP, DD], (14, 14, 14)), {"P2S_FUSED_VARIANT": "1"}),          # paired stores
+    ((1, (8, 8, 8), [PP, DD], (20, 20, 20)), {}),                                   # C3 fused
+    ((3, (10, 6, 4), [PP, DD], (16, 16, 16)), {}),                                  # C4 fused
+    ((3, (5, 4, 3), [PP, DD], (8, 8, 6)), {"P2S_XCHUNK_MB": "1"}),                 # large path
+    ((1, (2, 3, 4), [PP], (5, 6, 7)), {}),                                          # generic kernels
+])
+@pytest.mark.parametrize("odd_ld", [False, True])
+def test_writes_stay_inside_the_output(problem, env, odd_ld, monkeypatch):
+    """Canary zones around M (and the padding columns of ld_M > n_tot) are left
+    untouched by every kernel path; compute-sanitizer is unavailable on the pool,
+    so out-of-bounds stores are caught by value here."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    ctx = capi.Context(*problem)
+    n = 7
+    ld = ctx.n_tot + (1 if odd_ld else 0)
+    o = oracle_for(*problem)
+    alpha = torch.from_numpy(o.alpha(O.ALPHA_SINE, 0.5, 3.0, 3, 0, n)).cuda()
+    canary = -1.2345e300
+    buf = torch.full((GUARD + n * ctx.n_tot * ld + GUARD,), canary, dtype=torch.float64, device="cuda")
+    M = buf[GUARD:GUARD + n * ctx.n_tot * ld].view(n, ctx.n_tot, ld)
+    ctx.fill(alpha, M, ld, n, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    b = buf.cpu().numpy()
+    assert (b[:GUARD] == canary).all() and (b[-GUARD:] == canary).all()
+    Mh = M.cpu().numpy()
+    assert np.isfinite(Mh[:, :, :ctx.n_tot]).all() and not (Mh[:, :, :ctx.n_tot] == canary).any()
+    if odd_ld:
+        assert (Mh[:, :, ctx.n_tot:] == canary).all()
