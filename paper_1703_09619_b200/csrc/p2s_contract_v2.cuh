@@ -74,6 +74,14 @@ struct Shape {
   static_assert(!QUAD || (FPT_ % 4 == 0 && (NV_ * NW_) % 4 == 0 && !PAIR),
                 "QUAD needs FPT and rows divisible by 4 (and excludes PAIR)");
   static constexpr int VW = QUAD ? 4 : PAIR ? 2 : 1;  // adjacent fibers per vector store
+  // NSYM (bit 9, needs SYM): B is symmetric in (n1, n2), so the stage-C fibers
+  // (n1, p1, n2, p2) and (n2, p1, n1, p2) hold the same values and give the same
+  // outputs: stage C enumerates only n2 >= n1 (compactly, so whole warps retire
+  // early) and also stores each value at row (n2, p1), column (n1, p2); stage B
+  // skips n2 < n1.  Together with USYM one computed value lands in up to 4 places.
+  static constexpr int NSYM = (FLAGS_ >> 9) & 1;
+  static_assert(!NSYM || (SYM && !MMA && !QUAD), "NSYM needs SYM (and the banded stage C)");
+  static_assert(!NSYM || !PAIR || NW_ % 2 == 0, "NSYM pairs need an even N_w");
   static constexpr int AALL = (FLAGS_ & 1) | SYM, ROWLOOP = (FLAGS_ >> 1) & 1;
   static constexpr int NQV = NV_ * (NV_ + 1) / 2, NQW = NW_ * (NW_ + 1) / 2;
   static constexpr int tri(int a, int b, int n) { return a * n - a * (a - 1) / 2 + (b - a); }
@@ -352,6 +360,7 @@ __device__ __forceinline__ void v2_stage_b_sym(const V2Params<Sh>& p, const doub
         const int ik = g - n2 * (T * Ku);
         const int i = ik / Ku, k1 = ik - i * Ku;
         const int n1 = n1base + i;
+        if (Sh::NSYM && n2 < n1) return;  // stage C reads only n2 >= n1
         const int a = n1 < n2 ? n1 : n2, b = n1 < n2 ? n2 : n1;
         const double* src = Abuf + Sh::aoff(s) + k1 * Sh::aks(s) + Sh::tri(a, b, NV) * Kw;
         double y[Kw];
@@ -465,24 +474,57 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
               return Mbase + static_cast<int64_t>(n1 * NW + p1) * p.ldM + r;
             });
       } else {
+      // NSYM: the tile's canonical (n2 >= n1) fibers, i-major blocks of
+      // P1T * (NV - n1) * NW; nf / nft are this tile's fiber / thread-item counts
+      int nf = NF;
+      if constexpr (Sh::NSYM) {
+        nf = 0;
+#pragma unroll
+        for (int i = 0; i < T; ++i) nf += Sh::P1T * (NV - (t * T + i)) * NW;
+      }
+      const int nft = Sh::NSYM ? (nf / VW + FPT / VW - 1) / (FPT / VW) : NFT;
       auto stage_c = [&](auto parc) {
       constexpr int PAR = decltype(parc)::value;  // -1: all (m1, m2) at once
       for_items<NFT, Sh::THREADS>([&](int f0) {
+        if (Sh::NSYM && f0 >= nft) return;
         double b[FPT][Sh::KTOT_PAR(PAR)];
         double* out[FPT];
+        double* outn[FPT];  // NSYM mirror (row n2, column n1); nullptr when n2 == n1
         bool live[FPT];
 #pragma unroll
         for (int q = 0; q < FPT; ++q) {
-          // f = ((i*P1T + p1l)*NV + n2)*NW + p2
-          const int f = VW * (f0 + (q / VW) * NFT) + (q % VW);
-          live[q] = f < NF;
+          // f = ((i*P1T + p1l)*NV + n2)*NW + p2  (NSYM: compact canonical index)
+          const int f = VW * (f0 + (q / VW) * nft) + (q % VW);
+          live[q] = f < nf;
           const int fs = live[q] ? f : 0;
-          const int r = fs % (NV * NW);
-          const int ip = fs / (NV * NW);
-          const int p1l = ip % Sh::P1T, i = ip / Sh::P1T;
+          int r, p1l, i;
+          if constexpr (Sh::NSYM) {
+            int rem = fs;
+            i = 0;
+#pragma unroll
+            for (int ii = 0; ii < T - 1; ++ii) {
+              const int c = Sh::P1T * (NV - (t * T + ii)) * NW;
+              if (i == ii && rem >= c) {
+                rem -= c;
+                i = ii + 1;
+              }
+            }
+            const int w = (NV - (t * T + i)) * NW;
+            p1l = rem / w;
+            r = (t * T + i) * NW + (rem - p1l * w);  // n2 * NW + p2 with n2 >= n1
+          } else {
+            r = fs % (NV * NW);
+            const int ip = fs / (NV * NW);
+            p1l = ip % Sh::P1T;
+            i = ip / Sh::P1T;
+          }
           const int n1 = t * T + i, p1 = pt * Sh::P1T + p1l;
           v2_load_fiber<Sh, PAR>(Bbuf, i, p1l, r, b[q]);
           out[q] = Mbase + static_cast<int64_t>(n1 * NW + p1) * p.ldM + r;
+          if constexpr (Sh::NSYM) {
+            const int n2 = r / NW, p2 = r - n2 * NW;
+            outn[q] = n2 > n1 ? Mbase + static_cast<int64_t>(n2 * NW + p1) * p.ldM + n1 * NW + p2 : nullptr;
+          }
         }
         auto row = [&](auto m1c) {
           constexpr int m1 = decltype(m1c)::value;
@@ -522,19 +564,25 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
             } else if constexpr (Sh::PAIR) {
 #pragma unroll
               for (int q = 0; q < FPT; q += 2) {
-                double* d = out[q] + m1 * rowstep + m2 * (NV * NW);
-                double* dm = out[q] + m2 * rowstep + m1 * (NV * NW);
-                if (p.vec2) {
-                  if (live[q]) {
-                    st_cs2(d, v[q], v[q + 1]);
-                    if constexpr (mirror) st_cs2(dm, v[q], v[q + 1]);
-                  }
-                } else {
-                  if (live[q]) st_cs(d, v[q]);
-                  if (live[q + 1]) st_cs(d + 1, v[q + 1]);
-                  if constexpr (mirror) {
-                    if (live[q]) st_cs(dm, v[q]);
-                    if (live[q + 1]) st_cs(dm + 1, v[q + 1]);
+                // the pair shares n2 (even N_w, pairs start at even p2): one mirror row
+                double* bases[2] = {out[q], Sh::NSYM ? outn[q] : nullptr};
+#pragma unroll
+                for (int h = 0; h < (Sh::NSYM ? 2 : 1); ++h) {
+                  if (bases[h] == nullptr) continue;
+                  double* d = bases[h] + m1 * rowstep + m2 * (NV * NW);
+                  double* dm = bases[h] + m2 * rowstep + m1 * (NV * NW);
+                  if (p.vec2) {
+                    if (live[q]) {
+                      st_cs2(d, v[q], v[q + 1]);
+                      if constexpr (mirror) st_cs2(dm, v[q], v[q + 1]);
+                    }
+                  } else {
+                    if (live[q]) st_cs(d, v[q]);
+                    if (live[q + 1]) st_cs(d + 1, v[q + 1]);
+                    if constexpr (mirror) {
+                      if (live[q]) st_cs(dm, v[q]);
+                      if (live[q + 1]) st_cs(dm + 1, v[q + 1]);
+                    }
                   }
                 }
               }
@@ -544,6 +592,12 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
                 if (live[q]) {
                   st_cs(out[q] + m1 * rowstep + m2 * (NV * NW), v[q]);
                   if constexpr (mirror) st_cs(out[q] + m2 * rowstep + m1 * (NV * NW), v[q]);
+                  if constexpr (Sh::NSYM) {
+                    if (outn[q] != nullptr) {
+                      st_cs(outn[q] + m1 * rowstep + m2 * (NV * NW), v[q]);
+                      if constexpr (mirror) st_cs(outn[q] + m2 * rowstep + m1 * (NV * NW), v[q]);
+                    }
+                  }
                 }
             }
             }  // parity class

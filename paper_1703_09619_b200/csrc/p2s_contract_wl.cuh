@@ -23,7 +23,7 @@ template <int NU_, int NV_, int NW_, int TM_, int THREADS_, int MINB_, int... TK
 struct WShape {
   static constexpr int NU = NU_, NV = NV_, NW = NW_, TM = TM_, THREADS = THREADS_, MINB = MINB_;
   static constexpr int S = sizeof...(TK);
-  static constexpr int MMA = 0, PAIR = 0, PSPLIT = 0, QUAD = 0, SYM = 1, PERSIST = 0;  // registry interface
+  static constexpr int MMA = 0, PAIR = 0, PSPLIT = 0, QUAD = 0, NSYM = 0, SYM = 1, PERSIST = 0;  // registry interface
   static constexpr int N(int d) { return d == 0 ? NU : d == 1 ? NV : NW; }
   static constexpr int kind(int s, int d) {
     const int k[] = {TK...};

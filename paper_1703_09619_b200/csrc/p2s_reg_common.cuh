@@ -59,6 +59,10 @@ inline int vec2_ok(const double* M, int64_t ldM) {
 
 template <class Sh>
 constexpr const char* stage_c_desc() {
+  if constexpr (!Sh::WLAST && Sh::NSYM)
+    return Sh::PSPLIT ? "banded stage C, parity split, (n1, n2)-symmetric"
+           : Sh::PAIR ? "banded stage C, paired 16-B stores, (n1, n2)-symmetric"
+                      : "banded stage C, (n1, n2)-symmetric";
   return Sh::WLAST   ? "w-last contraction"
          : Sh::MMA  ? "stage C on DMMA"
          : Sh::QUAD   ? (Sh::PSPLIT ? "banded stage C, parity split, 32-B stores"

@@ -111,7 +111,8 @@ FusedEntry make_fused() {
 
 // <Shape: N_u, N_v, N_w, n1 tile, p1 tile, p1 group, threads, min CTAs/SM, flags, FPT, kinds>
 // flags: 1 AALL, 2 ROWLOOP, 4 SYM, 8 PERSIST, 16 MMA (stage C on DMMA), 32 PAIR (16-B
-// stores), 64 PSPLIT (parity-split stage C), 128 NOUSYM, 256 QUAD (32-B stores).  The first match of a problem is the
+// stores), 64 PSPLIT (parity-split stage C), 128 NOUSYM, 256 QUAD (32-B stores),
+// 512 NSYM ((n1, n2)-symmetric stage C).  The first match of a problem is the
 // default; P2S_FUSED_VARIANT=k selects the k-th (tuning / A-B measurements, see
 // profiles/README.md for the numbers behind each default).
 const std::vector<FusedEntry>& fused_registry() {
@@ -174,6 +175,16 @@ const std::vector<FusedEntry>& fused_registry() {
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 326, 4, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 326, 4, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
+      // (n1, n2)-symmetric stage C (NSYM, flag 512): C2 variant 7 (1.26 M vs 1.69 M),
+      // C3 variant 6 (1.87 M vs 2.19 M), C4 variant 8 (1.04 M vs 1.11 M): 42 % fewer
+      // stage-C DFMAs, but the mirrored stores (row n2, N_w-double runs) are poorly
+      // coalesced and the later n1 tiles leave threads idle
+      make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 516, 2, kPPP, kDDD>,
+                 MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 550, 2, kPPP, kDDD>,
+                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
+      make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 582, 2, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
       // test shapes
       make_fused<Shape<3, 3, 3, 3, 3, 3, 96, 4, 0, 1, kPPP, kDDD>,

@@ -267,6 +267,9 @@ VARIANT_CASES = [
     ("c3", False, "32-B stores", 3),
     ("c3", False, "parity split, 32-B stores", 3),
     ("c4", False, "parity split, 32-B stores", 3),
+    ("c2", False, "(n1, n2)-symmetric", 6),
+    ("c3", False, "paired 16-B stores, (n1, n2)-symmetric", 3),
+    ("c4", False, "parity split, (n1, n2)-symmetric", 3),
     ((3, (3, 3, 3), [PP, DD], (6, 6, 6)), True, "parity split", 4),
     ((1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7)), True, "parity split", 4),
     ((3, (3, 3, 3), [PP, DD], (6, 6, 6)), True, "DMMA", 4),
