@@ -94,6 +94,13 @@ __device__ __forceinline__ void st_cs2(double* p, double a, double b) {
   __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
 }
 
+// 32-B read-only load of four adjacent doubles (p 32-B aligned; sm_100 LDG.256)
+__device__ __forceinline__ void ld_nc4(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
+
 // 32-B streaming store of four adjacent doubles (p 32-B aligned; sm_100 STG.256)
 __device__ __forceinline__ void st_cs4(double* p, double a, double b, double c, double d) {
   asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)

@@ -327,15 +327,11 @@ __global__ void __launch_bounds__(Ls::NW * Ls::NW) large_v_kernel(const __grid_c
     constexpr int KV = Ls::K(s, 1), kv = Ls::kind(s, 1);
     if (row < Ls::kuoff(s) || row >= Ls::kuoff(s) + Ls::K(s, 0)) return;
     const int k1 = row - Ls::kuoff(s);
-    const double2* src = reinterpret_cast<const double2*>(
-        p.Z + unit * Ls::ZPU + Ls::zoff(s) + (static_cast<int64_t>(k1) * NW * NW + t) * K2P);
-    double z[(KV + 1) & ~1];
+    // the thread's Z fiber: K2P contiguous doubles (32-B aligned), 32-B loads
+    const double* src = p.Z + unit * Ls::ZPU + Ls::zoff(s) + (static_cast<int64_t>(k1) * NW * NW + t) * K2P;
+    double z[(KV + 3) & ~3];
 #pragma unroll
-    for (int q = 0; q < (KV + 1) / 2; ++q) {
-      const double2 v = src[q];
-      z[2 * q] = v.x;
-      z[2 * q + 1] = v.y;
-    }
+    for (int q = 0; q < (KV + 3) / 4; ++q) ld_nc4(src + 4 * q, z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
     double* Xk = p.X + unit * Ls::XPU + Ls::xoff(s) + static_cast<int64_t>(k1) * NQV * NW * NW + t;
     static_for<0, NV>([&](auto n1c) {
       constexpr int a = decltype(n1c)::value;
