@@ -421,7 +421,6 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
                                         double* Bbuf, double* Mbase, AfterA&& after_a,
                                         MmaSmem mm = MmaSmem{nullptr, nullptr}) {
   constexpr int S = Sh::S, NU = Sh::NU, NV = Sh::NV, NW = Sh::NW, T = Sh::T, FPT = Sh::FPT;
-  const int tid = threadIdx.x;
   if constexpr (Sh::SYM) {
     v2_stage_a_sym<Sh>(p, Ibuf, Abuf);
     __syncthreads();
@@ -489,7 +488,8 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
         if (Sh::NSYM && f0 >= nft) return;
         double b[FPT][Sh::KTOT_PAR(PAR)];
         double* out[FPT];
-        double* outn[FPT];  // NSYM mirror (row n2, column n1); nullptr when n2 == n1
+        double* outn[Sh::NSYM ? FPT : 1];  // NSYM mirror (row n2, column n1); nullptr when n2 == n1
+        (void)outn;
         bool live[FPT];
 #pragma unroll
         for (int q = 0; q < FPT; ++q) {
@@ -565,7 +565,8 @@ __device__ __forceinline__ void v2_unit(const V2Params<Sh>& p, const double* Ibu
 #pragma unroll
               for (int q = 0; q < FPT; q += 2) {
                 // the pair shares n2 (even N_w, pairs start at even p2): one mirror row
-                double* bases[2] = {out[q], Sh::NSYM ? outn[q] : nullptr};
+                double* bases[2] = {out[q], nullptr};
+                if constexpr (Sh::NSYM) bases[1] = outn[q];
 #pragma unroll
                 for (int h = 0; h < (Sh::NSYM ? 2 : 1); ++h) {
                   if (bases[h] == nullptr) continue;

@@ -108,8 +108,7 @@ struct WShape {
 template <class Ws>
 __device__ __forceinline__ void wl_unit(const V2Params<Ws>& p, const double* Ibuf, double* Abuf,
                                         double* Bbuf, double* Mbase) {
-  constexpr int S = Ws::S, NU = Ws::NU, NV = Ws::NV, NW = Ws::NW, TM = Ws::TM, NQU = Ws::NQU,
-                NQV = Ws::NQV;
+  constexpr int S = Ws::S, NU = Ws::NU, NV = Ws::NV, NW = Ws::NW, TM = Ws::TM, NQU = Ws::NQU;
   constexpr int NT = Ws::THREADS;
   const int64_t rowstep_m = static_cast<int64_t>(NV * NW) * p.ldM;  // row of m1
 #pragma unroll 1

@@ -88,11 +88,18 @@ __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
 
 // Streaming (evict-first) 8-byte store: element matrices are written once and
 // never re-read by the fill.
+#ifdef P2S_STORE_WB
+__device__ __forceinline__ void st_cs(double* p, double v) { *p = v; }
+__device__ __forceinline__ void st_cs2(double* p, double a, double b) {
+  *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+#else
 __device__ __forceinline__ void st_cs(double* p, double v) { __stcs(p, v); }
 // 16-B streaming store of two adjacent doubles (p 16-B aligned)
 __device__ __forceinline__ void st_cs2(double* p, double a, double b) {
   __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
 }
+#endif
 
 // 32-B read-only load of four adjacent doubles (p 32-B aligned; sm_100 LDG.256)
 __device__ __forceinline__ void ld_nc4(const double* p, double& a, double& b, double& c, double& d) {
