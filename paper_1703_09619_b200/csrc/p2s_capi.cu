@@ -96,7 +96,8 @@ const FusedEntry* find_fused(const p2s_problem& pb) {
   if (const char* v = std::getenv("P2S_NO_FUSED"))
     if (v[0] == '1') return nullptr;
   int want = 0, seen = 0;
-  if (const char* v = std::getenv("P2S_FUSED_VARIANT")) want = std::atoi(v);
+  const char* var = std::getenv("P2S_FUSED_VARIANT");
+  if (var) want = std::atoi(var);
   const FusedEntry* first = nullptr;
   for (const FusedEntry& r : fused_registry()) {
     bool ok = r.S == pb.n_terms;
@@ -104,7 +105,10 @@ const FusedEntry* find_fused(const p2s_problem& pb) {
     for (int s = 0; ok && s < r.S; ++s)
       for (int d = 0; d < 3; ++d) ok = ok && r.kinds[s][d] == pb.kind[s][d];
     if (!ok) continue;
-    if (!first) first = &r;
+    if (!first) {
+      if (r.prefer_two_stage && !var) return nullptr;
+      first = &r;
+    }
     if (seen++ == want) return &r;
   }
   return first;
@@ -164,6 +168,9 @@ struct p2s_ctx {
   // host pipeline
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
   int64_t host_chunk = 0;
+  // two-stage fill: moments of the next chunk on s_mom (double-buffered scratch)
+  cudaStream_t s_mom = nullptr;
+  cudaEvent_t ev_fill_start = nullptr, ev_mom_done[2]{}, ev_con_done[2]{};
   double* d_ring_alpha[2]{};
   double* d_ring_M[2]{};
   cudaEvent_t ev_h2d[2]{}, ev_comp[2]{}, ev_d2h[2]{};
@@ -374,12 +381,34 @@ p2s_status run_fill(p2s_ctx* c, const double* alpha, double* M, int64_t ldM, int
   }
   const int64_t ape = c->sz.alpha_per_elem;
   const int64_t mstride = static_cast<int64_t>(c->sz.n_tot) * ldM;
-  for (int64_t e0 = 0; e0 < n; e0 += c->chunk) {
+  if (c->large || !c->s_mom) {  // serial (the large path overlaps inside its contraction)
+    for (int64_t e0 = 0; e0 < n; e0 += c->chunk) {
+      const int64_t cnt = std::min(c->chunk, n - e0);
+      p2s_status s1 = run_moments(c, alpha + e0 * ape, c->d_scratch, cnt, st);
+      if (s1 != P2S_OK) return s1;
+      p2s_status s2 = run_contract(c, c->d_scratch, M + e0 * mstride, ldM, cnt, st);
+      if (s2 != P2S_OK) return s2;
+    }
+    return P2S_OK;
+  }
+  // two-stage path, double-buffered moment scratch: the moments of chunk i+1 run
+  // on s_mom while the (store-bound) contraction of chunk i runs on the caller's
+  // stream; chunk i+2's moments wait for chunk i's contraction (buffer reuse)
+  P2S_CUDA(cudaEventRecord(c->ev_fill_start, st));
+  P2S_CUDA(cudaStreamWaitEvent(c->s_mom, c->ev_fill_start, 0));
+  int64_t i = 0;
+  for (int64_t e0 = 0; e0 < n; e0 += c->chunk, ++i) {
     const int64_t cnt = std::min(c->chunk, n - e0);
-    p2s_status s1 = run_moments(c, alpha + e0 * ape, c->d_scratch, cnt, st);
+    const int b = static_cast<int>(i & 1);
+    double* I = c->d_scratch + b * c->sz.moments_per_elem * c->chunk;
+    if (i >= 2) P2S_CUDA(cudaStreamWaitEvent(c->s_mom, c->ev_con_done[b], 0));
+    p2s_status s1 = run_moments(c, alpha + e0 * ape, I, cnt, c->s_mom);
     if (s1 != P2S_OK) return s1;
-    p2s_status s2 = run_contract(c, c->d_scratch, M + e0 * mstride, ldM, cnt, st);
+    P2S_CUDA(cudaEventRecord(c->ev_mom_done[b], c->s_mom));
+    P2S_CUDA(cudaStreamWaitEvent(st, c->ev_mom_done[b], 0));
+    p2s_status s2 = run_contract(c, I, M + e0 * mstride, ldM, cnt, st);
     if (s2 != P2S_OK) return s2;
+    P2S_CUDA(cudaEventRecord(c->ev_con_done[b], st));
   }
   return P2S_OK;
 }
@@ -606,10 +635,26 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     }
   }
 
-  // scheduler chunk: moment scratch of ~32 MB stays in L2 between the stages
+  // scheduler chunk: ~256 MB of moment scratch per buffer, double-buffered in the
+  // two-stage path (P2S_TWO_STAGE_OVERLAP=0: serial).  Measured on C3 (elem/s):
+  // 32 MB (L2-resident I, short launches with tails) 2.07 M, 128 MB 2.26 M,
+  // 256 MB 2.29 M, 1 GB 2.31 M -- the I round trip through HBM (2 % of the bytes)
+  // costs less than the launch tails of small chunks
   const int64_t per = c->sz.moments_per_elem * 8;
-  c->chunk = std::max<int64_t>(1, (int64_t(32) << 20) / per);
-  P2S_CUDA(cudaMalloc(&c->d_scratch, sizeof(double) * c->sz.moments_per_elem * c->chunk));
+  int64_t cmb = 256;
+  if (const char* v = std::getenv("P2S_CHUNK_MB")) cmb = std::max(1, std::atoi(v));
+  c->chunk = std::max<int64_t>(1, (cmb << 20) / per);
+  bool overlap = !c->large && !c->fused;
+  if (const char* v = std::getenv("P2S_TWO_STAGE_OVERLAP")) overlap = overlap && v[0] != '0';
+  P2S_CUDA(cudaMalloc(&c->d_scratch, sizeof(double) * c->sz.moments_per_elem * c->chunk * (overlap ? 2 : 1)));
+  if (overlap) {
+    P2S_CUDA(cudaStreamCreateWithFlags(&c->s_mom, cudaStreamNonBlocking));
+    P2S_CUDA(cudaEventCreateWithFlags(&c->ev_fill_start, cudaEventDisableTiming));
+    for (int b = 0; b < 2; ++b) {
+      P2S_CUDA(cudaEventCreateWithFlags(&c->ev_mom_done[b], cudaEventDisableTiming));
+      P2S_CUDA(cudaEventCreateWithFlags(&c->ev_con_done[b], cudaEventDisableTiming));
+    }
+  }
   *out = c.release();
   return P2S_OK;
 }
@@ -626,6 +671,12 @@ void p2s_destroy(p2s_ctx* c) {
   for (int d = 0; d < 3; ++d)
     if (c->d_x[d]) cudaFree(c->d_x[d]);
   if (c->d_scratch) cudaFree(c->d_scratch);
+  if (c->s_mom) cudaStreamDestroy(c->s_mom);
+  if (c->ev_fill_start) cudaEventDestroy(c->ev_fill_start);
+  for (int b = 0; b < 2; ++b) {
+    if (c->ev_mom_done[b]) cudaEventDestroy(c->ev_mom_done[b]);
+    if (c->ev_con_done[b]) cudaEventDestroy(c->ev_con_done[b]);
+  }
   if (c->d_X) cudaFree(c->d_X);
   if (c->lpack.d_Z) cudaFree(c->lpack.d_Z);
   if (c->lpack.aux) cudaStreamDestroy(c->lpack.aux);

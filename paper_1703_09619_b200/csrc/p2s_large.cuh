@@ -168,14 +168,8 @@ __device__ __forceinline__ void large_moments_term(const LMomParams<Ls>& p, cons
     constexpr int Hf = QU / 2, H = (QU + 1) / 2;
     const int q3 = r / QV, q2 = r - (r / QV) * QV;
     double x[QU];
-    const double2* row = reinterpret_cast<const double2*>(a + static_cast<int64_t>(r) * QU);
     static_assert(QU % 2 == 0, "large path expects an even rule along u");
-#pragma unroll
-    for (int q = 0; q < QU / 2; ++q) {
-      const double2 v = __ldg(row + q);
-      x[2 * q] = v.x;
-      x[2 * q + 1] = v.y;
-    }
+    load_row<QU>(a + static_cast<int64_t>(r) * QU, x);
     double ev[Hf], od[Hf];
 #pragma unroll
     for (int h = 0; h < Hf; ++h) {

@@ -108,6 +108,28 @@ struct MV2Params {
                          // per-direction tables [KMAX][H]
 };
 
+// One alpha row (QU contiguous doubles) into registers with the widest loads the
+// row length allows: 32-B (LDG.256, sm_100) when QU % 4 == 0 -- every sector is
+// touched by exactly one load -- else 16-B.  Rows start at multiples of QU
+// doubles from a 32-B aligned slab.
+template <int QU>
+__device__ __forceinline__ void load_row(const double* __restrict__ row, double (&x)[QU]) {
+  if constexpr (QU % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < QU / 4; ++q) ld_nc4(row + 4 * q, x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+  } else if constexpr (QU % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < QU / 2; ++q) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(row) + q);
+      x[2 * q] = v.x;
+      x[2 * q + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < QU; ++q) x[q] = __ldg(row + q);
+  }
+}
+
 // Even/odd folded contraction of one register fiber a[Q] against the half
 // table tb[K][H]; out(k, value) receives each result.
 template <int Q, int K, class Out>
@@ -153,18 +175,7 @@ __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const
   for_items<QW * QV, NTHR>([&](int r) {
     const int q3 = r / QV, q2 = r - (r / QV) * QV;
     double x[QU];
-    if constexpr ((QU & 1) == 0) {
-      const double2* row = reinterpret_cast<const double2*>(a + static_cast<int64_t>(r) * QU);
-#pragma unroll
-      for (int q = 0; q < QU / 2; ++q) {
-        const double2 v = __ldg(row + q);
-        x[2 * q] = v.x;
-        x[2 * q + 1] = v.y;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < QU; ++q) x[q] = __ldg(a + static_cast<int64_t>(r) * QU + q);
-    }
+    load_row<QU>(a + static_cast<int64_t>(r) * QU, x);
     fold_contract<QU, KU>(x, tu, [&](int k, double v) { T1[(k * QW + q3) * S2 + q2] = v; });
   });
   __syncthreads();
@@ -177,13 +188,18 @@ __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const
     fold_contract<QV, KV>(x, tv, [&](int k, double v) { T2[(k1 * KV + k) * S3 + q3] = v; });
   });
   __syncthreads();
+  // pass w: the thread's KW outputs are one contiguous run of I; they go to shared
+  // memory first (T1 is free after pass v) and leave in one coalesced sweep
+  static_assert(KU * KV * KW <= KU * QW * S2, "I tile must fit the T1 scratch");
   for_items<KU * KV, NTHR>([&](int r) {
     const double* src = T2 + r * S3;
     double x[QW];
 #pragma unroll
     for (int q = 0; q < QW; ++q) x[q] = src[q];
-    fold_contract<QW, KW>(x, tw, [&](int k, double v) { Iout[r * KW + k] = v; });
+    fold_contract<QW, KW>(x, tw, [&](int k, double v) { T1[r * KW + k] = v; });
   });
+  __syncthreads();
+  for (int i = threadIdx.x; i < KU * KV * KW; i += NTHR) Iout[i] = T1[i];
   __syncthreads();
 }
 
@@ -320,17 +336,20 @@ __device__ __forceinline__ void moments_all_terms(const double* __restrict__ a, 
       constexpr int s = decltype(sc)::value;
       double x[QU];
       const double* row = a + s * slab + static_cast<int64_t>(r) * QU;
-      if constexpr ((QU & 1) == 0) {
+      if constexpr (SRC == 2) {  // alpha in shared memory (cluster mode)
+        if constexpr ((QU & 1) == 0) {
 #pragma unroll
-        for (int q = 0; q < QU / 2; ++q) {
-          const double2 v = SRC == 2 ? reinterpret_cast<const double2*>(row)[q]
-                                     : __ldg(reinterpret_cast<const double2*>(row) + q);
-          x[2 * q] = v.x;
-          x[2 * q + 1] = v.y;
+          for (int q = 0; q < QU / 2; ++q) {
+            const double2 v = reinterpret_cast<const double2*>(row)[q];
+            x[2 * q] = v.x;
+            x[2 * q + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < QU; ++q) x[q] = row[q];
         }
       } else {
-#pragma unroll
-        for (int q = 0; q < QU; ++q) x[q] = SRC == 2 ? row[q] : __ldg(row + q);
+        load_row<QU>(row, x);
       }
 #pragma unroll
       for (int h = 0; h < Hf; ++h) {

@@ -86,7 +86,7 @@ cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_
 }
 
 
-template <class Sh, class Ms, bool WITH_GEO = false>
+template <class Sh, class Ms, bool WITH_GEO = false, bool PREFER_TWO_STAGE = false>
 FusedEntry make_fused() {
   FusedEntry r{};
   for (int d = 0; d < 3; ++d) {
@@ -106,6 +106,7 @@ FusedEntry make_fused() {
   r.mpack = &pack_mv2<Ms>;
   r.mma_pack = &pack_mma<Sh>;
   r.desc = stage_c_desc<Sh>();
+  r.prefer_two_stage = PREFER_TWO_STAGE;
   return r;
 }
 
@@ -134,9 +135,13 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 100, 4, kPPP, kDDD>,
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),
-      // C3: 0 paired stores (default), 1 banded, 2 parity split + paired, 3 DMMA
+      // C3: p2s_fill runs the two-stage path by default (moments_v2 + contract_v2 over
+      // 256 MB chunks, the next chunk's moments overlapping this chunk's contraction:
+      // 2.29-2.31 M elem/s vs 2.26 M fused -- the fused kernel fits one 223 KB CTA per
+      // SM, so its moment phase never overlaps another CTA's stores); fused variants (via
+      // P2S_FUSED_VARIANT): 0 paired stores, 1 banded, 2 parity split + paired, 3 DMMA
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 38, 2, kPPP, kDDD>,
-                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
+                 MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>, false, true>(),
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 6, 2, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 102, 2, kPPP, kDDD>,

@@ -93,6 +93,9 @@ struct FusedEntry {
   mv2_pack_fn mpack;
   v2_pack_fn mma_pack;
   const char* desc;
+  // p2s_fill runs the two-stage path (moments_v2 + contract_v2) for this shape
+  // unless P2S_FUSED_VARIANT asks for a fused kernel: measured faster (C3)
+  bool prefer_two_stage;
 };
 
 struct LargeArgs {

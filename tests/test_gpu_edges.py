@@ -164,3 +164,30 @@ def test_writes_stay_inside_the_output(problem, env, odd_ld, monkeypatch):
     assert np.isfinite(Mh[:, :, :ctx.n_tot]).all() and not (Mh[:, :, :ctx.n_tot] == canary).any()
     if odd_ld:
         assert (Mh[:, :, ctx.n_tot:] == canary).all()
+
+
+@pytest.mark.parametrize("env", [
+    {"P2S_CHUNK_MB": "1"},                                   # C3 default: two-stage, overlapped
+    {"P2S_CHUNK_MB": "1", "P2S_TWO_STAGE_OVERLAP": "0"},     # serial chunks
+    {"P2S_CHUNK_MB": "1", "P2S_NO_FUSED": "1"},
+])
+def test_two_stage_chunk_pipeline_matches_oracle(env, monkeypatch):
+    """The two-stage fill over many scheduler chunks (double-buffered moment
+    scratch, the next chunk's moments on a side stream) gives the oracle's
+    matrices; C3 runs this path by default."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = CONFIGS["c3"]
+    ctx = capi.Context(**cfg.problem())
+    assert ctx.kernel_path.startswith("two-stage"), ctx.kernel_path
+    n = 61  # 23 elements per 1 MB chunk: three chunks, the last one ragged
+    o = oracle_for(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
+    alpha = o.alpha(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 17, 0, n)
+    M = _nan(n, ctx.n_tot, ctx.n_tot)
+    ctx.fill(torch.from_numpy(alpha).cuda(), M, ctx.n_tot, n, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    Mo = o.fill(alpha, threads=16)
+    Mg = M.cpu().numpy()
+    for e in range(n):
+        ok, msg, _ = blocks_close(Mg[e], Mo[e], 1, ctx.n_tot)
+        assert ok, (e, msg)

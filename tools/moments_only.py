@@ -1,0 +1,13 @@
+import sys, torch
+sys.path.insert(0, '.')
+from paper_1703_09619_b200 import capi
+from paper_1703_09619_b200.configs import CONFIGS
+cfg = CONFIGS[sys.argv[1]]
+ctx = capi.Context(**cfg.problem())
+E = int(sys.argv[2])
+st = torch.cuda.current_stream().cuda_stream
+a = torch.empty((E, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")
+ctx.alpha_generate(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 7, 0, E, a, st)
+I = torch.empty((E, ctx.moments_per_elem), dtype=torch.float64, device="cuda")
+for _ in range(3): ctx.moments(a, I, E, st)
+torch.cuda.synchronize()
