@@ -207,7 +207,7 @@ __device__ __forceinline__ void large_moments_term(const LMomParams<Ls>& p, cons
 }
 
 template <class Ls>
-__global__ void __launch_bounds__(256) large_moments_kernel(const __grid_constant__ LMomParams<Ls> p) {
+__global__ void __launch_bounds__(256, Ls::MOM_SMEM <= 110 * 1024 ? 2 : 1) large_moments_kernel(const __grid_constant__ LMomParams<Ls> p) {
   extern __shared__ __align__(16) double sm[];
   const int64_t b = blockIdx.x;
   const int chunk = static_cast<int>(b % Ls::NCH);
