@@ -81,14 +81,19 @@ const V2Entry* find_v2(const p2s_problem& pb) {
 
 
 const MV2Entry* find_mv2(const p2s_problem& pb) {
+  int want = 0, seen = 0;
+  if (const char* v = std::getenv("P2S_MV2_VARIANT")) want = std::atoi(v);
+  const MV2Entry* first = nullptr;
   for (const MV2Entry& r : mv2_registry()) {
     bool ok = r.S == pb.n_terms;
     for (int d = 0; d < 3; ++d) ok = ok && r.order[d] == pb.order[d] && r.nq[d] == pb.nq[d];
     for (int s = 0; ok && s < r.S; ++s)
       for (int d = 0; d < 3; ++d) ok = ok && r.kinds[s][d] == base_kind(pb.kind[s][d]);
-    if (ok) return &r;  // moments do not depend on the basis
+    if (!ok) continue;  // moments do not depend on the basis
+    if (!first) first = &r;
+    if (seen++ == want) return &r;
   }
-  return nullptr;
+  return first;
 }
 
 

@@ -148,11 +148,23 @@ const std::vector<MV2Entry>& mv2_registry() {
   static const std::vector<MV2Entry> reg = {
       make_mv2<MShape<4, 4, 4, 8, 8, 8, 128, kPPP>>(),                    // C1
       make_mv2<MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),           // C2
-      make_mv2<MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),           // C3
+      make_mv2<MShape<8, 8, 8, 20, 20, 20, 512, kPPP, kDDD>>(),           // C3 (512 threads)
       make_mv2<MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>>(),          // C4
       make_mv2<MShape<3, 3, 3, 6, 6, 6, 128, kPPP, kDDD>>(),              // test shapes
       make_mv2<MShape<4, 3, 3, 9, 5, 7, 128, enc_kind(DP, PD, PP), enc_kind(PD, DP, DD)>>(),
       make_mv2<MShape<5, 5, 5, 9, 9, 9, 128, kPPP, kDDD>>(),
+      // thread-count variants (P2S_MV2_VARIANT), FP64 TF/s of the C3 moments kernel:
+      // C3 0 = 512 (25.8, default), 1 = 200 (18.9), 2 = 320 (21.2), 3 = 400 (25.6),
+      // 4 = 256 (19.8); C4 1 = 192, 2 = 384 and C2 1 = 128, 2 = 196 (all within 2 % of
+      // their 256-thread defaults)
+      make_mv2<MShape<8, 8, 8, 20, 20, 20, 200, kPPP, kDDD>>(),
+      make_mv2<MShape<8, 8, 8, 20, 20, 20, 320, kPPP, kDDD>>(),
+      make_mv2<MShape<8, 8, 8, 20, 20, 20, 400, kPPP, kDDD>>(),
+      make_mv2<MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
+      make_mv2<MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
+      make_mv2<MShape<10, 6, 4, 16, 16, 16, 384, kPPP, kDDD>>(),
+      make_mv2<MShape<6, 6, 6, 14, 14, 14, 128, kPPP, kDDD>>(),
+      make_mv2<MShape<6, 6, 6, 14, 14, 14, 196, kPPP, kDDD>>(),
   };
   return reg;
 }
