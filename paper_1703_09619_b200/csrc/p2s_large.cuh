@@ -18,6 +18,13 @@
 #include "p2s_kernels.cuh"
 #include "p2s_moments_v2.cuh"  // fold_contract
 
+#ifndef P2S_LARGE_MOM_THREADS
+#define P2S_LARGE_MOM_THREADS 256  // threads of large_moments_kernel
+#endif
+#ifndef P2S_LARGE_MOM_MINB
+#define P2S_LARGE_MOM_MINB 2
+#endif
+
 #ifndef P2S_LARGE_FIB2_MINB
 #define P2S_LARGE_FIB2_MINB 2  // CTAs per SM of the two-fiber u stage (3: 170-register cap, spills)
 #endif
@@ -157,7 +164,7 @@ __device__ __forceinline__ void large_moments_term(const LMomParams<Ls>& p, cons
   constexpr int QU = Ls::Q(0), QV = Ls::Q(1), QW = Ls::Q(2);
   constexpr int KU = Ls::K(s, 0), KV = Ls::K(s, 1), KW = Ls::K(s, 2), KC = Ls::KC;
   constexpr int S2 = Ls::S2, S3 = Ls::S3;
-  constexpr int NT = 256;
+  constexpr int NT = P2S_LARGE_MOM_THREADS;
   const int k0 = chunk * KC;
   if (k0 >= KU) return;
   double* T1 = sm;                         // [KC][QW][S2]
@@ -207,7 +214,7 @@ __device__ __forceinline__ void large_moments_term(const LMomParams<Ls>& p, cons
 }
 
 template <class Ls>
-__global__ void __launch_bounds__(256, Ls::MOM_SMEM <= 110 * 1024 ? 2 : 1) large_moments_kernel(const __grid_constant__ LMomParams<Ls> p) {
+__global__ void __launch_bounds__(P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM <= 110 * 1024 ? P2S_LARGE_MOM_MINB : 1) large_moments_kernel(const __grid_constant__ LMomParams<Ls> p) {
   extern __shared__ __align__(16) double sm[];
   const int64_t b = blockIdx.x;
   const int chunk = static_cast<int>(b % Ls::NCH);

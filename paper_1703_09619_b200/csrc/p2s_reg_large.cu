@@ -69,7 +69,8 @@ cudaError_t launch_large_moments(const double* alpha, double* I, int64_t n_units
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  large_moments_kernel<Ls><<<static_cast<unsigned>(n_units * Ls::S * Ls::NCH), 256, Ls::MOM_SMEM, st>>>(p);
+  large_moments_kernel<Ls><<<static_cast<unsigned>(n_units * Ls::S * Ls::NCH), P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM,
+                             st>>>(p);
   return cudaGetLastError();
 }
 
