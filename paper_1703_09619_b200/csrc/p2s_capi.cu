@@ -767,8 +767,12 @@ p2s_status p2s_fill_host(p2s_ctx* c, const double* h_alpha, double* h_M, int64_t
       P2S_CUDA(cudaEventCreateWithFlags(&c->ev_comp[i], cudaEventDisableTiming));
       P2S_CUDA(cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming));
     }
-    // ~256 MB of matrices per slot
-    c->host_chunk = std::max<int64_t>(1, (int64_t(256) << 20) / (mel * 8));
+    // ~64 MB of matrices per slot (P2S_HOST_CHUNK_MB); C2 e2e measured 32 MB 15.31 k,
+    // 64 MB 15.38 k, 256 MB 15.26 k, 1 GB 15.02 k elem/s: the D2H copy (51.7 GB/s of a
+    // 56.4 GB/s PCIe peak) is the bound
+    int64_t hmb = 64;
+    if (const char* v = std::getenv("P2S_HOST_CHUNK_MB")) hmb = std::max(1, std::atoi(v));
+    c->host_chunk = std::max<int64_t>(1, (hmb << 20) / (mel * 8));
     for (int i = 0; i < 2; ++i) {
       P2S_CUDA(cudaMalloc(&c->d_ring_alpha[i], sizeof(double) * ape * c->host_chunk));
       P2S_CUDA(cudaMalloc(&c->d_ring_M[i], sizeof(double) * mel * c->host_chunk));
