@@ -65,8 +65,9 @@ def test_ragged_batches_match_oracle(n, path_env, monkeypatch):
 
 
 def test_host_path_across_ring_chunks():
-    """p2s_fill_host pipelines 256 MB chunks through a 2-slot ring: 80 C2 elements
-    straddle a chunk boundary (76 per chunk)."""
+    """p2s_fill_host pipelines 64 MB chunks through a 2-slot ring: 80 C2 elements
+    span five chunks (19 per chunk; elements 75 | 76 straddle a boundary) and
+    reuse both slots twice."""
     cfg = CONFIGS["c2"]
     ctx = capi.Context(**cfg.problem())
     n = 80
