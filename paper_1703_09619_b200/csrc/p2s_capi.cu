@@ -633,6 +633,7 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     c->lpack.u_ctas = 2 * static_cast<int64_t>(c->num_sms);  // persistent u stage, 2 CTAs per SM
     if (const char* v = std::getenv("P2S_LARGE_UPERSIST"))
       c->lpack.u_ctas = static_cast<int64_t>(std::max(0, std::atoi(v))) * c->num_sms;
+    if (const char* v = std::getenv("P2S_LARGE_USMEM")) c->lpack.u_smemc = v[0] == '1';
     if (const char* v = std::getenv("P2S_LARGE_FIB")) c->lpack.ufib = std::atoi(v) == 2 ? 2 : 1;
     for (int b = 0; b < 2; ++b) {
       P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_vw[b], cudaEventDisableTiming));
@@ -684,6 +685,7 @@ void p2s_destroy(p2s_ctx* c) {
   }
   if (c->d_X) cudaFree(c->d_X);
   if (c->lpack.d_Z) cudaFree(c->lpack.d_Z);
+  if (c->lpack.d_cu) cudaFree(c->lpack.d_cu);
   if (c->lpack.aux) cudaStreamDestroy(c->lpack.aux);
   if (c->lpack.aux_u) cudaStreamDestroy(c->lpack.aux_u);
   if (c->lpack.ev_start) cudaEventDestroy(c->lpack.ev_start);

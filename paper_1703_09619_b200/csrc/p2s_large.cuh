@@ -357,6 +357,7 @@ template <class Ls>
 struct LUParams {
   const double* X;
   double* M;
+  const double* cu_g;   // device copy of cu (SMEMC: staged into shared memory per CTA)
   int64_t ldM, mat_stride, n_units;
   int nc, P, Nt;
   double cu[Ls::ctot(0)];
@@ -367,8 +368,9 @@ struct LUParams {
 // FIB fibers per thread: thread (n2, p2) of a CTA of N_v N_w / FIB threads also
 // owns the fibers n2 + i N_v / FIB; every constant-bank coefficient feeds FIB
 // DFMAs (half the LDCU per DFMA at FIB = 2, 3 CTAs of 128 threads per SM).
-template <class Ls, bool PS, int FIB>
-__device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, int64_t unit0, int64_t b) {
+template <class Ls, bool PS, int FIB, bool SMEMC>
+__device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, const double* cus, int64_t unit0,
+                                             int64_t b) {
   constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S, NQV = Ls::NQV;
   static_assert(NV % FIB == 0, "fibers per thread must divide N_v");
   const int np = static_cast<int>(b % (NV * NW));
@@ -425,7 +427,7 @@ __device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, int64_t unit
               constexpr int j = decltype(jc)::value;
               constexpr int xi = PAR < 0 ? Ls::kuoff(s) + lo + band_step(ku, m1, m2) * j
                                          : Ls::kpo(s, PAR) + (lo - Ls::uk0(s, PAR)) / 2 + j;
-              const double c = p.cu[co + j];
+              const double c = SMEMC ? cus[co + j] : p.cu[co + j];
 #pragma unroll
               for (int f = 0; f < FIB; ++f) v[f] = fma(c, x[f][xi], v[f]);
             });
@@ -461,23 +463,34 @@ __device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, int64_t unit
   }
 }
 
-template <class Ls, bool PS, int FIB>
+// SMEMC: the coefficients are copied once per (persistent) CTA from global memory
+// into shared memory (coalesced) and read as uniform-address LDS; else they are
+// constant-bank operands (LDCU).
+template <class Ls, bool PS, int FIB, bool SMEMC = false>
 __global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? 2 : P2S_LARGE_FIB2_MINB) : 1)
     large_u_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
+  extern __shared__ __align__(16) double cus[];
+  if constexpr (SMEMC) {
+    for (int i = threadIdx.x; i < Ls::ctot(0); i += blockDim.x) cus[i] = __ldg(p.cu_g + i);
+    __syncthreads();
+  }
   // one (unit, n1, p1) tile per CTA, or a grid-stride loop over the tiles when the
   // grid is smaller (persistent CTAs: P2S_LARGE_UPERSIST CTAs per SM)
 #pragma unroll 1
-  for (int64_t b = blockIdx.x; b < ntiles; b += gridDim.x) large_u_tile<Ls, PS, FIB>(p, unit0, b);
+  for (int64_t b = blockIdx.x; b < ntiles; b += gridDim.x) large_u_tile<Ls, PS, FIB, SMEMC>(p, cus, unit0, b);
 }
 
 template <class Ls>
 void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps, int fib, int64_t max_ctas,
-                      cudaStream_t st) {
+                      bool smemc, cudaStream_t st) {
   const int64_t ntiles = cnt * Ls::NV * Ls::NW;
   const unsigned grid = static_cast<unsigned>(max_ctas > 0 && max_ctas < ntiles ? max_ctas : ntiles);
   constexpr int T = Ls::NV * Ls::NW;
   constexpr int F2 = Ls::NV % 2 == 0 ? 2 : 1;
-  if (ps && fib == 2)
+  constexpr size_t cs = sizeof(double) * Ls::ctot(0);
+  if (ps && smemc && p.cu_g)
+    large_u_kernel<Ls, true, 1, true><<<grid, T, cs, st>>>(p, unit0, ntiles);
+  else if (ps && fib == 2)
     large_u_kernel<Ls, true, F2><<<grid, T / F2, 0, st>>>(p, unit0, ntiles);
   else if (ps)
     large_u_kernel<Ls, true, 1><<<grid, T, 0, st>>>(p, unit0, ntiles);

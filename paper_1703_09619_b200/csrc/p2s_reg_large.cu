@@ -47,6 +47,10 @@ bool pack_large(const LargeArgs& a, LargePack& out) {
   };
   out.cu.assign(static_cast<size_t>(Ls::ctot(0)), 0.0);
   band_pack(0, out.cu, 0);
+  if (cudaMalloc(&out.d_cu, sizeof(double) * out.cu.size()) != cudaSuccess) return false;
+  if (cudaMemcpy(out.d_cu, out.cu.data(), sizeof(double) * out.cu.size(), cudaMemcpyHostToDevice) !=
+      cudaSuccess)
+    return false;
   out.cvw.assign(static_cast<size_t>(Ls::ctot(1) + Ls::ctot(2)), 0.0);
   band_pack(1, out.cvw, 0);
   band_pack(2, out.cvw, static_cast<size_t>(Ls::ctot(1)));
@@ -87,6 +91,7 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
   up.P = P;
   up.Nt = Nt;
   std::memcpy(up.cu, pk.cu.data(), sizeof(double) * Ls::ctot(0));
+  up.cu_g = pk.d_cu;
   LWParams<Ls> wp;
   wp.Z = pk.d_Z;
   std::memcpy(wp.cw, pk.cvw.data() + Ls::ctot(1), sizeof(double) * Ls::ctot(2));
@@ -126,7 +131,7 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
     // u stage: absolute units u0 .. u0+cnt-1; Xb holds the chunk
     up.X = Xb;
     up.n_units = cnt;
-    large_u_dispatch<Ls>(up, u0, cnt, pk.ps, pk.ufib, pk.u_ctas, us);
+    large_u_dispatch<Ls>(up, u0, cnt, pk.ps, pk.ufib, pk.u_ctas, pk.u_smemc, us);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ov && (e = cudaEventRecord(pk.ev_u[b], us)) != cudaSuccess) return e;
   }

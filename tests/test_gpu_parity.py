@@ -219,6 +219,7 @@ def test_large_order_path_small_shape(n_comp):
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_PRIO": "1"},          # high-priority v/w stream
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_UPERSIST": "1"},      # persistent u stage, 1 CTA / SM
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_UPERSIST": "0"},      # one u-stage CTA per tile
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_USMEM": "1"},         # u coefficients in shared memory
 ])
 def test_large_order_path_chunk_schedules(env, monkeypatch):
     # the chunked v/w -> u pipeline over many X chunks (double buffer reuse,
