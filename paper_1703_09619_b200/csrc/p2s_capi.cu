@@ -609,7 +609,7 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     for (int s = 0; s < S; ++s)
       for (int d = 0; d < 3; ++d) la.dense[s][d] = &c->coef[s][d];
     if (!lge->pack(la, c->lpack)) return fail(P2S_CUDA_ERROR, "p2s_create: large-path table upload");
-    // X chunk: ~64 MB of v/w-contracted intermediates per buffer (two buffers: the
+    // X chunk: ~96 MB of v/w-contracted intermediates per buffer (two buffers: the
     // v/w stage of the next chunk overlaps the u stage of this one)
     int64_t xmb = 96;
     if (const char* v = std::getenv("P2S_XCHUNK_MB")) xmb = std::max(1, std::atoi(v));

@@ -148,13 +148,14 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 22, 1, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
-      // C4: 0 parity split, all six n1 per tile, 2 fibers / thread (default: every
-      // constant-bank coefficient feeds two DFMAs; 1 CTA of 288 threads per SM),
-      // 1 parity split with n1 tiles of 2 (2 CTAs/SM), 2 banded, 3 paired stores, 4 DMMA
-      make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 70, 2, kPPP, kDDD>,
-                 MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
+      // C4: 0 parity split with n1 tiles of 2 (default: 2 CTAs of 192 threads per SM;
+      // 1.126 M elem/s vs 1.104 M for variant 1 since the 32-B alpha loads), 1 parity
+      // split, all six n1 per tile, 2 fibers / thread (1 CTA of 288 threads per SM),
+      // 2 banded, 3 paired stores, 4 DMMA
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 70, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
+      make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 70, 2, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 38, 2, kPPP, kDDD>,
