@@ -14,6 +14,9 @@
 // which rounds like the host): values agree with it to ~1e-15 relative.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include <cstdint>
 
 namespace p2s {
@@ -112,7 +115,14 @@ cudaError_t launch_alpha_geometry_fast(double* alpha, const double* geom, const 
                                        cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
   if (nq[0] > 64 || nq[1] > 64 || nq[2] > 64) return cudaErrorInvalidValue;
-  const unsigned slabs = static_cast<unsigned>((nq[0] * nq[1] * nq[2] + 255) / 256);
+  // points per thread (P2S_GEO_PPT, default 4): the per-CTA prologue (record ->
+  // polynomial map, nodes) is amortised over several points per thread
+  static int ppt = -1;
+  if (ppt < 0) {
+    ppt = 4;
+    if (const char* v = std::getenv("P2S_GEO_PPT")) ppt = std::max(1, std::atoi(v));
+  }
+  const unsigned slabs = static_cast<unsigned>((nq[0] * nq[1] * nq[2] + 256 * ppt - 1) / (256 * ppt));
   const dim3 grid(static_cast<unsigned>(n), slabs);
 #define P2S_GEO_CASE(NC_, S_)                                                                         \
   if (nc == NC_ && S == S_) {                                                                       \
