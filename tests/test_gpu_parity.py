@@ -102,6 +102,30 @@ def test_moments_match_oracle():
                 assert ok, (e, pr, s, i, j, g[i, j], r[i, j])
 
 
+@pytest.mark.parametrize("name,variant", [("c3", v) for v in range(5)] + [("c4", v) for v in range(3)]
+                         + [("c2", v) for v in range(3)] + [("c5", 0)])
+def test_moment_kernel_variants_match_oracle(name, variant, monkeypatch):
+    # every registered moments_v2 thread-count variant (P2S_MV2_VARIANT) and the
+    # large-order moment kernel reproduce the oracle's moment integrals
+    monkeypatch.setenv("P2S_MV2_VARIANT", str(variant))
+    cfg = CONFIGS[name]
+    o = oracle_for(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
+    ctx = capi.Context(**cfg.problem())
+    n = 1 if name == "c5" else 2
+    alpha = o.alpha(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 23, 0, n)
+    Ig = _gpu_moments(ctx, alpha)
+    Io = o.moments(alpha, threads=16)
+    for e in range(n):
+        for pr in range(ctx.n_pairs):
+            for s in range(len(cfg.kinds)):
+                K = [ctx.K(s, d) for d in range(3)]
+                m = K[0] * K[1] * K[2]
+                g = Ig[e, ctx.moment_offset(pr, s):ctx.moment_offset(pr, s) + m].reshape(K[0], -1)
+                r = Io[e, o.moment_offset(pr, s):o.moment_offset(pr, s) + m].reshape(K[0], -1)
+                ok, (i, j) = O.block_close(g, r, RTOL)
+                assert ok, (e, pr, s, i, j, g[i, j], r[i, j])
+
+
 def test_tables_match_oracle():
     for kinds, order, nq in [([PP, DD], (6, 8, 10), (14, 9, 20)), ([DP, PD], (4, 5, 3), (7, 8, 9))]:
         o = oracle_for(1, order, kinds, nq)
