@@ -15,6 +15,8 @@
 //                         every warp store is 256 contiguous bytes
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "p2s_kernels.cuh"
 #include "p2s_moments_v2.cuh"  // fold_contract
 
@@ -158,7 +160,11 @@ struct LMomParams {
   double tab[Ls::TALL];
 };
 
-template <class Ls, int s>
+// CL (cluster mode): the NCH chunk CTAs of one (unit, term) form a thread-block
+// cluster; each loads and folds 1/NCH of the alpha rows once, computes every k1
+// of them and stores each value into the T1 of the CTA owning that k1 through
+// distributed shared memory -- alpha is read and folded once instead of NCH times.
+template <class Ls, int s, bool CL>
 __device__ __forceinline__ void large_moments_term(const LMomParams<Ls>& p, const double* a, double* Iout,
                                                    int chunk, double* sm) {
   constexpr int QU = Ls::Q(0), QV = Ls::Q(1), QW = Ls::Q(2);
@@ -166,9 +172,41 @@ __device__ __forceinline__ void large_moments_term(const LMomParams<Ls>& p, cons
   constexpr int S2 = Ls::S2, S3 = Ls::S3;
   constexpr int NT = P2S_LARGE_MOM_THREADS;
   const int k0 = chunk * KC;
-  if (k0 >= KU) return;
   double* T1 = sm;                         // [KC][QW][S2]
   double* T2 = sm + KC * QW * S2;          // [KC*KV][S3]
+  if constexpr (CL) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    constexpr int NCH = Ls::NCH, H = (QU + 1) / 2, Hf = QU / 2;
+    constexpr int RPC = (QW * QV + NCH - 1) / NCH;  // alpha rows per CTA
+    double* peer[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) peer[c] = cl.map_shared_rank(T1, c);
+    const double* tu = p.tab + Ls::ttoff(0);
+    for_items<RPC, NT>([&](int i) {
+      const int r = chunk * RPC + i;
+      if (r >= QW * QV) return;
+      const int q3 = r / QV, q2 = r - (r / QV) * QV;
+      double x[QU];
+      load_row<QU>(a + static_cast<int64_t>(r) * QU, x);
+      double ev[Hf], od[Hf];
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) {
+        ev[h] = x[h] + x[QU - 1 - h];
+        od[h] = x[h] - x[QU - 1 - h];
+      }
+#pragma unroll
+      for (int k1 = 0; k1 < KU; ++k1) {
+        double v = 0.0;
+#pragma unroll
+        for (int h = 0; h < Hf; ++h) v = fma(tu[k1 * H + h], (k1 & 1) ? od[h] : ev[h], v);
+        peer[k1 / KC][((k1 % KC) * QW + q3) * S2 + q2] = v;
+      }
+    });
+    cl.sync();  // every T1 complete (and no remote access after this point)
+    if (k0 >= KU) return;
+  } else {
+  if (k0 >= KU) return;
   const double* tu = p.tab + Ls::ttoff(0) + k0 * Ls::H(0);
   // pass u (rows of alpha), outputs k1 = k0 .. k0+KC-1
   for_items<QW * QV, NT>([&](int r) {
@@ -192,6 +230,7 @@ __device__ __forceinline__ void large_moments_term(const LMomParams<Ls>& p, cons
     }
   });
   __syncthreads();
+  }
   const double* tv = p.tab + Ls::ttoff(1);
   for_items<KC * QW, NT>([&](int r) {
     const int j = r / QW, q3 = r - (r / QW) * QW;
@@ -213,7 +252,7 @@ __device__ __forceinline__ void large_moments_term(const LMomParams<Ls>& p, cons
   });
 }
 
-template <class Ls>
+template <class Ls, bool CL = false>
 __global__ void __launch_bounds__(P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM <= 110 * 1024 ? P2S_LARGE_MOM_MINB : 1) large_moments_kernel(const __grid_constant__ LMomParams<Ls> p) {
   extern __shared__ __align__(16) double sm[];
   const int64_t b = blockIdx.x;
@@ -226,7 +265,7 @@ __global__ void __launch_bounds__(P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM <= 110 * 1
   double* Ib = p.I + unit * Ls::MPP;
   static_for<0, Ls::S>([&](auto sc) {
     constexpr int ss = decltype(sc)::value;
-    if (s == ss) large_moments_term<Ls, ss>(p, a, Ib + Ls::moff(ss), chunk, sm);
+    if (s == ss) large_moments_term<Ls, ss, CL>(p, a, Ib + Ls::moff(ss), chunk, sm);
   });
 }
 

@@ -71,10 +71,29 @@ cudaError_t launch_large_moments(const double* alpha, double* I, int64_t n_units
     cudaError_t e = cudaFuncSetAttribute(large_moments_kernel<Ls>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ls::MOM_SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(large_moments_kernel<Ls, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Ls::MOM_SMEM);
+    if (e != cudaSuccess) return e;
     attr = true;
   }
-  large_moments_kernel<Ls><<<static_cast<unsigned>(n_units * Ls::S * Ls::NCH), P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM,
-                             st>>>(p);
+  const unsigned grid = static_cast<unsigned>(n_units * Ls::S * Ls::NCH);
+  if (pk.mom_cluster && Ls::NCH <= 8) {
+    // one cluster of NCH chunk CTAs per (unit, term)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(P2S_LARGE_MOM_THREADS);
+    cfg.dynamicSmemBytes = Ls::MOM_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = static_cast<unsigned>(Ls::NCH);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, large_moments_kernel<Ls, true>, p);
+  }
+  large_moments_kernel<Ls><<<grid, P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -103,11 +103,14 @@ def test_moments_match_oracle():
 
 
 @pytest.mark.parametrize("name,variant", [("c3", v) for v in range(5)] + [("c4", v) for v in range(3)]
-                         + [("c2", v) for v in range(3)] + [("c5", 0)])
+                         + [("c2", v) for v in range(3)] + [("c5", 0), ("c5", "cluster")])
 def test_moment_kernel_variants_match_oracle(name, variant, monkeypatch):
     # every registered moments_v2 thread-count variant (P2S_MV2_VARIANT) and the
-    # large-order moment kernel reproduce the oracle's moment integrals
-    monkeypatch.setenv("P2S_MV2_VARIANT", str(variant))
+    # large-order moment kernel (both modes) reproduce the oracle's moment integrals
+    if variant == "cluster":
+        monkeypatch.setenv("P2S_LARGE_MOMCL", "1")
+    else:
+        monkeypatch.setenv("P2S_MV2_VARIANT", str(variant))
     cfg = CONFIGS[name]
     o = oracle_for(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
     ctx = capi.Context(**cfg.problem())
@@ -244,6 +247,7 @@ def test_large_order_path_small_shape(n_comp):
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_UPERSIST": "1"},      # persistent u stage, 1 CTA / SM
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_UPERSIST": "0"},      # one u-stage CTA per tile
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_USMEM": "1"},         # u coefficients in shared memory
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_MOMCL": "1"},         # cluster moments (DSMEM)
 ])
 def test_large_order_path_chunk_schedules(env, monkeypatch):
     # the chunked v/w -> u pipeline over many X chunks (double buffer reuse,
