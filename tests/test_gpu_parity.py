@@ -129,6 +129,31 @@ def test_moment_kernel_variants_match_oracle(name, variant, monkeypatch):
                 assert ok, (e, pr, s, i, j, g[i, j], r[i, j])
 
 
+@pytest.mark.parametrize("name,variant", [(c, v) for c in ("c2", "c3", "c4") for v in range(3)])
+def test_two_stage_contraction_variants_match_oracle(name, variant, monkeypatch):
+    # every registered contract_v2 variant of the benchmark shapes (P2S_V2_VARIANT,
+    # two-stage path) gives the oracle's matrices
+    monkeypatch.setenv("P2S_NO_FUSED", "1")
+    monkeypatch.setenv("P2S_V2_VARIANT", str(variant))
+    cfg = CONFIGS[name]
+    ctx = capi.Context(**cfg.problem())
+    assert ctx.kernel_path.startswith("two-stage"), ctx.kernel_path
+    _check_case(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq, cfg.alpha_kind, cfg.alpha_lo,
+                cfg.alpha_hi, n_elem=3, seed=29, threads=16)
+
+
+@pytest.mark.parametrize("name,variant", [(c, v) for c in ("c2", "c3", "c4") for v in range(10)])
+def test_every_fused_variant_matches_oracle(name, variant, monkeypatch):
+    # every registered fill_fused_kernel variant of the benchmark shapes
+    # (P2S_FUSED_VARIANT; indices past the last fall back to the first)
+    monkeypatch.setenv("P2S_FUSED_VARIANT", str(variant))
+    cfg = CONFIGS[name]
+    ctx = capi.Context(**cfg.problem())
+    assert ctx.kernel_path.startswith("fused"), ctx.kernel_path
+    _check_case(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq, cfg.alpha_kind, cfg.alpha_lo,
+                cfg.alpha_hi, n_elem=2, seed=31, threads=16)
+
+
 def test_tables_match_oracle():
     for kinds, order, nq in [([PP, DD], (6, 8, 10), (14, 9, 20)), ([DP, PD], (4, 5, 3), (7, 8, 9))]:
         o = oracle_for(1, order, kinds, nq)
