@@ -148,10 +148,13 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
       make_fused<Shape<8, 8, 8, 1, 8, 8, 256, 1, 22, 1, kPPP, kDDD>,
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
-      // C4: 0 parity split with n1 tiles of 2 (default: 2 CTAs of 192 threads per SM;
-      // 1.126 M elem/s vs 1.104 M for variant 1 since the 32-B alpha loads), 1 parity
-      // split, all six n1 per tile, 2 fibers / thread (1 CTA of 288 threads per SM),
-      // 2 banded, 3 paired stores, 4 DMMA
+      // C4: 0 parity split with n1 tiles of 2, 2 CTAs of 256 threads per SM (default:
+      // 1.174 M elem/s; 192 threads 1.133 M, n1 tiles of 3 1.009 M, 2 fibers/thread
+      // 1.105 M), 1 the same at 192 threads, then parity split with all six n1 per tile
+      // and 2 fibers / thread (1 CTA of 288 threads per SM, 1.104 M), banded, paired
+      // stores, DMMA
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 256, 2, 70, 1, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 70, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 70, 2, kPPP, kDDD>,
