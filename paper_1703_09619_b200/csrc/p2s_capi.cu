@@ -655,7 +655,13 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
   if (const char* v = std::getenv("P2S_TWO_STAGE_OVERLAP")) overlap = overlap && v[0] != '0';
   P2S_CUDA(cudaMalloc(&c->d_scratch, sizeof(double) * c->sz.moments_per_elem * c->chunk * (overlap ? 2 : 1)));
   if (overlap) {
-    P2S_CUDA(cudaStreamCreateWithFlags(&c->s_mom, cudaStreamNonBlocking));
+    // P2S_MOM_PRIO=1: the moments stream at the highest priority (its CTAs are
+    // dispatched first whenever a contraction CTA retires); C3: 2.30 M either way
+    int plo = 0, phi = 0;
+    P2S_CUDA(cudaDeviceGetStreamPriorityRange(&plo, &phi));
+    bool mhi = false;
+    if (const char* v = std::getenv("P2S_MOM_PRIO")) mhi = v[0] == '1';
+    P2S_CUDA(cudaStreamCreateWithPriority(&c->s_mom, cudaStreamNonBlocking, mhi ? phi : plo));
     P2S_CUDA(cudaEventCreateWithFlags(&c->ev_fill_start, cudaEventDisableTiming));
     for (int b = 0; b < 2; ++b) {
       P2S_CUDA(cudaEventCreateWithFlags(&c->ev_mom_done[b], cudaEventDisableTiming));
