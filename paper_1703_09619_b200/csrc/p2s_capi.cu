@@ -633,6 +633,7 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     c->lpack.u_ctas = 2 * static_cast<int64_t>(c->num_sms);  // persistent u stage, 2 CTAs per SM
     if (const char* v = std::getenv("P2S_LARGE_UPERSIST"))
       c->lpack.u_ctas = static_cast<int64_t>(std::max(0, std::atoi(v))) * c->num_sms;
+    if (const char* v = std::getenv("P2S_LARGE_XS")) c->lpack.u_xs = v[0] != '0';
     if (const char* v = std::getenv("P2S_LARGE_MOMCL")) c->lpack.mom_cluster = v[0] == '1';
     if (const char* v = std::getenv("P2S_LARGE_USMEM")) c->lpack.u_smemc = v[0] == '1';
     if (const char* v = std::getenv("P2S_LARGE_FIB")) c->lpack.ufib = std::atoi(v) == 2 ? 2 : 1;

@@ -397,6 +397,7 @@ struct LUParams {
   const double* X;
   double* M;
   const double* cu_g;   // device copy of cu (SMEMC: staged into shared memory per CTA)
+  int xs;               // XS mode: x classes staged in shared memory by the TMA engine
   int64_t ldM, mat_stride, n_units;
   int nc, P, Nt;
   double cu[Ls::ctot(0)];
@@ -519,6 +520,121 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? 2 : P2
   for (int64_t b = blockIdx.x; b < ntiles; b += gridDim.x) large_u_tile<Ls, PS, FIB, SMEMC>(p, cus, unit0, b);
 }
 
+// XS mode (persistent, parity split, one fiber per thread): each thread's x
+// values of the next parity class (of this tile or of the CTA's next tile) are
+// copied into its shared-memory slots with cp.async while the current class
+// computes, so a class starts with 30 shared-memory loads instead of 30 L2 loads.
+// (A first version with one 128-byte TMA bulk copy per (k1, n2) row issued by one
+// warp ran at 21.4 k elem/s vs 28.5 k: the TMA engine is slow on tiny copies.)
+template <class Ls>
+struct LUXs {
+  static constexpr int NV = Ls::NV, NW = Ls::NW;
+  static constexpr int KXM = Ls::KX(0) > Ls::KX(1) ? Ls::KX(0) : Ls::KX(1);
+  static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(KXM) * NV * NW + 16;
+};
+
+// Per-thread asynchronous copy (cp.async, 8 bytes) of the thread's own x values
+// of one parity class of tile b into its shared-memory slots xbuf[j][tid].
+template <class Ls>
+__device__ __forceinline__ void large_u_xs_issue(const LUParams<Ls>& p, int64_t unit0, int64_t b, int cls,
+                                                 double* xbuf) {
+  constexpr int NV = Ls::NV, NW = Ls::NW, NQV = Ls::NQV, S = Ls::S;
+  const int tid = threadIdx.x;
+  const int np = static_cast<int>(b % (NV * NW));
+  const int64_t unit = unit0 + b / (NV * NW);
+  const int n1 = np / NW, p1 = np - (np / NW) * NW;
+  const int n2 = tid / NW, p2 = tid - (tid / NW) * NW;
+  const int qv = n1 <= n2 ? Ls::tri(n1, n2, NV) : Ls::tri(n2, n1, NV);
+  const double* Xu = p.X + (unit - unit0) * Ls::XPU + (static_cast<int64_t>(qv) * NW + p1) * NW + p2;
+  auto go = [&](auto parc) {
+    constexpr int PAR = decltype(parc)::value;
+    static_for<0, S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+#pragma unroll
+      for (int j = 0; j < Ls::ucnt(s, PAR); ++j) {
+        const double* src =
+            Xu + Ls::xoff(s) + static_cast<int64_t>(Ls::uk0(s, PAR) + 2 * j) * NQV * NW * NW;
+        double* dst = xbuf + (Ls::kpo(s, PAR) + j) * NV * NW + tid;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+      }
+    });
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (cls == 0)
+    go(std::integral_constant<int, 0>{});
+  else
+    go(std::integral_constant<int, 1>{});
+}
+
+template <class Ls>
+__global__ void __launch_bounds__(Ls::NV * Ls::NW, 2)
+    large_u_xs_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
+  constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S;
+  static_assert(NW % 2 == 0, "bulk-copy rows must be 16-byte multiples");
+  extern __shared__ __align__(128) double xbuf[];
+  const int tid = threadIdx.x;
+  int64_t b = blockIdx.x;
+  if (b >= ntiles) return;
+  large_u_xs_issue<Ls>(p, unit0, b, 0, xbuf);
+  const int n2 = tid / NW, p2 = tid - (tid / NW) * NW;
+#pragma unroll 1
+  for (; b < ntiles; b += gridDim.x) {
+    const int np = static_cast<int>(b % (NV * NW));
+    const int64_t unit = unit0 + b / (NV * NW);
+    const int n1 = np / NW, p1 = np - (np / NW) * NW;
+    const int64_t e = unit / p.P;
+    const int pair = static_cast<int>(unit - e * p.P);
+    const int gci = pair / p.nc, gcj = pair - gci * p.nc;
+    double* out = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt + n1 * NW + p1) * p.ldM +
+                  gcj * p.Nt + n2 * NW + p2;
+    const int64_t rowstep = static_cast<int64_t>(NV * NW) * p.ldM;
+    auto run = [&](auto parc) {
+      constexpr int PAR = decltype(parc)::value;
+      constexpr int KX = Ls::KX(PAR);
+      double x[KX];
+      asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < KX; ++j) x[j] = xbuf[j * NV * NW + tid];
+      // bar.sync completes the shared-memory loads above before the next class's
+      // copies are issued into the same slots
+      __syncthreads();
+      if (PAR == 0)
+        large_u_xs_issue<Ls>(p, unit0, b, 1, xbuf);
+      else if (b + gridDim.x < ntiles)
+        large_u_xs_issue<Ls>(p, unit0, b + gridDim.x, 0, xbuf);
+      auto row = [&](auto m1c) {
+        constexpr int m1 = decltype(m1c)::value;
+        static_for<(Ls::USYM ? m1 : 0), NU>([&](auto m2c) {
+          constexpr int m2 = decltype(m2c)::value;
+          if constexpr ((m1 + m2) % 2 == PAR) {
+            double v = 0.0;
+            static_for<0, S>([&](auto sc) {
+              constexpr int s = decltype(sc)::value;
+              constexpr int ku = Ls::kind(s, 0);
+              constexpr int lo = band_lo(ku, m1, m2), cnt = band_count(ku, m1, m2);
+              constexpr int co = Ls::coff(0, s, m1, m2);
+              static_for<0, cnt>([&](auto jc) {
+                constexpr int j = decltype(jc)::value;
+                constexpr int xi = Ls::kpo(s, PAR) + (lo - Ls::uk0(s, PAR)) / 2 + j;
+                v = fma(p.cu[co + j], x[xi], v);
+              });
+            });
+            st_cs(out + m1 * rowstep + m2 * (NV * NW), v);
+            if constexpr (Ls::USYM && m2 != m1) st_cs(out + m2 * rowstep + m1 * (NV * NW), v);
+          }
+        });
+      };
+#pragma unroll 1
+      for (int m1 = 0; m1 < NU; ++m1)
+        static_for<0, NU>([&](auto m1c) {
+          if (m1 == decltype(m1c)::value) row(m1c);
+        });
+    };
+    run(std::integral_constant<int, 0>{});
+    run(std::integral_constant<int, 1>{});
+  }
+}
+
 template <class Ls>
 void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps, int fib, int64_t max_ctas,
                       bool smemc, cudaStream_t st) {
@@ -527,6 +643,18 @@ void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps
   constexpr int T = Ls::NV * Ls::NW;
   constexpr int F2 = Ls::NV % 2 == 0 ? 2 : 1;
   constexpr size_t cs = sizeof(double) * Ls::ctot(0);
+  if constexpr (!Ls::u_conforming() && Ls::NW % 2 == 0) {
+    if (ps && fib == 1 && p.xs) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(large_u_xs_kernel<Ls>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)LUXs<Ls>::SMEM);
+        attr = true;
+      }
+      large_u_xs_kernel<Ls><<<grid, T, LUXs<Ls>::SMEM, st>>>(p, unit0, ntiles);
+      return;
+    }
+  }
   if (ps && smemc && p.cu_g)
     large_u_kernel<Ls, true, 1, true><<<grid, T, cs, st>>>(p, unit0, ntiles);
   else if (ps && fib == 2)

@@ -111,6 +111,7 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
   up.Nt = Nt;
   std::memcpy(up.cu, pk.cu.data(), sizeof(double) * Ls::ctot(0));
   up.cu_g = pk.d_cu;
+  up.xs = pk.u_xs ? 1 : 0;
   LWParams<Ls> wp;
   wp.Z = pk.d_Z;
   std::memcpy(wp.cw, pk.cvw.data() + Ls::ctot(1), sizeof(double) * Ls::ctot(2));

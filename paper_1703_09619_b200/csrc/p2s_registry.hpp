@@ -107,6 +107,7 @@ struct LargePack {
   std::vector<double> tab, cu, cvw;  // cvw: band-packed Cv then Cw (kernel parameters)
   double* d_Z = nullptr;             // w-step output of one chunk (ZPU x xchunk doubles)
   double* d_cu = nullptr;            // device copy of cu (u stage with shared-memory coefficients)
+  bool u_xs = true;                  // P2S_LARGE_XS: next class staged by cp.async (C5 29.4 k vs 28.4 k)
   bool mom_cluster = false;          // P2S_LARGE_MOMCL: one cluster per (unit, term), alpha read once (0.77 vs 0.71 ms: slower)
   bool u_smemc = false;              // P2S_LARGE_USMEM (measured 28.1 k vs 28.4 k elem/s constant-bank)
   // runtime: parity-split u stage; v/w of chunk i+1 on `aux` overlapping u of

@@ -284,6 +284,20 @@ def test_large_order_path_chunk_schedules(env, monkeypatch):
     _check_case(3, (5, 4, 3), [PP, DD], (8, 8, 6), O.ALPHA_JACOBIAN, 0.5, 3.0, n_elem=40)
 
 
+@pytest.mark.parametrize("env", [{"P2S_LARGE_XS": "0"}, {"P2S_LARGE_XS": "1", "P2S_XCHUNK_MB": "20"},
+                                 {"P2S_LARGE_XS": "1", "P2S_LARGE_UPERSIST": "0"}])
+def test_c5_u_stage_schedules_match_oracle(env, monkeypatch):
+    # C5 with the u stage's next parity class staged in shared memory by cp.async
+    # (default; across tiles of the persistent CTAs and across X chunks) and with
+    # direct L2 loads
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = CONFIGS["c5"]
+    worst = _check_case(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq, cfg.alpha_kind,
+                        cfg.alpha_lo, cfg.alpha_hi, n_elem=3, seed=7, threads=16)
+    assert worst < 1e-12
+
+
 def test_c5_matches_oracle():
     # BASELINE config 5 (order 16, 36^3 points): 134 MB per element matrix
     cfg = CONFIGS["c5"]
