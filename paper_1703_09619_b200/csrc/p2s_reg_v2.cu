@@ -81,8 +81,9 @@ const std::vector<V2Entry>& v2_registry() {
       make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kPPP, kDDD>>(),           // C2
       make_v2<Shape<6, 6, 6, 1, 6, 6, 224, 2, 4, 1, kPPP, kDDD>>(),
       make_v2<Shape<6, 6, 6, 2, 6, 6, 256, 2, 0, 2, kPPP, kDDD>>(),
-      // C3 (a persistent SYM variant <..., 256, 1, 12, 2> was dropped: it faulted with an
-      // illegal address at 255 registers + 128 B of stack; unused, never a default)
+      // C3 (persistent SYM variants <..., 256, 1, 12, 1|2> were dropped: both fault with an
+      // illegal address at 255 registers + 100-140 B of stack even for one element,
+      // where they execute the non-persistent code path; unused, never a default)
       make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 1, kPPP, kDDD>>(),           // C3
       make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>>(),
       // (C3 at 384 / 512 threads: 168 / 128 registers with 284 / 256 B of spills,
