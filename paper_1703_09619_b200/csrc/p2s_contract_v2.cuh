@@ -214,6 +214,7 @@ struct V2Params {
   int64_t mom_per_elem;
   const double* amma;  // fragment-ordered stage-C A (MMA shapes), else null
   int vec2;            // widest aligned vector store of M rows: 4 (32 B), 2 (16 B) or 1
+  int64_t prefetch_stride;  // non-persistent launch: resident CTAs (next unit on this SM slot)
   double cu[Sh::ctot(0)];
   double cv[Sh::ctot(1)];
   double cw[Sh::ctot(2)];
@@ -683,7 +684,16 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
         }
       });
   } else {
-    if (unit < p.n_units) do_unit([]() {});
+    if (unit < p.n_units) {
+      // warm L2 with the moments of the unit that takes this SM slot next
+      const int64_t nxt = unit + p.prefetch_stride;
+      if (tid == 0 && p.prefetch_stride > 0 && nxt < p.n_units) {
+        const int64_t e2 = nxt / p.P;
+        const int pair2 = static_cast<int>(nxt - e2 * p.P);
+        prefetch_l2(p.I + e2 * p.mom_per_elem + pair2 * Sh::MPP, kIBytes);
+      }
+      do_unit([]() {});
+    }
   }
 }
 

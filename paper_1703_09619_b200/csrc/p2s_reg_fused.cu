@@ -38,6 +38,7 @@ cudaError_t launch_fused(const double* alpha, double* M, int64_t ldM, int64_t n_
   p.c.mom_per_elem = 0;
   p.c.amma = amma;
   p.c.vec2 = vec2_ok(M, ldM);
+  p.c.prefetch_stride = 0;  // (contract_v2 only)
   std::memcpy(p.c.cu, cpack.data(), sizeof(double) * Sh::ctot(0));
   std::memcpy(p.c.cv, cpack.data() + Sh::ctot(0), sizeof(double) * Sh::ctot(1));
   std::memcpy(p.c.cw, cpack.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));

@@ -49,6 +49,9 @@ cudaError_t launch_v2(const V2Args& a, const std::vector<double>& packed, cudaSt
   const int64_t grid = Sh::PERSIST
                            ? std::min<int64_t>(p.n_units, static_cast<int64_t>(blocks_per_sm) * num_sms)
                            : p.n_units;
+  p.prefetch_stride = static_cast<int64_t>(blocks_per_sm) * num_sms;
+  if (const char* v = std::getenv("P2S_V2_NOPREFETCH"))
+    if (v[0] == '1') p.prefetch_stride = 0;
   contract_v2_kernel<Sh><<<static_cast<unsigned>(grid), Sh::THREADS, v2_smem<Sh>(), st>>>(p);
   return cudaGetLastError();
 }
