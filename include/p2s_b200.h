@@ -99,11 +99,38 @@ typedef struct {
 typedef struct p2s_ctx p2s_ctx;
 
 /* Builds and uploads the Gauss-Legendre rules, weighted Legendre kernel tables
- * and product-to-sum coefficient tables once. */
+ * and product-to-sum coefficient tables once.  Every valid problem is accepted
+ * (the reference's fill takes any Orders, kinds and nq: assembly.hpp:52-56,
+ * 82-83): shapes without an ahead-of-time kernel get a generated module --
+ * the planned kernel family instantiated for exactly this shape, compiled once
+ * for sm_100a with nvcc into the module cache (<dir of libp2s_b200.so>/jit, or
+ * $P2S_JIT_CACHE; compiler $P2S_NVCC, else $CUDA_HOME/bin/nvcc, else nvcc) and
+ * reused by later contexts and processes.  P2S_UNSUPPORTED_SHAPE: no family
+ * holds the shape, or its module is neither cached nor compilable here. */
 p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out);
+
+/* p2s_create with test / tuning hooks: options = "KEY=VALUE" pairs separated by
+ * ';' (NULL or "" = p2s_create).  Keys (unknown keys -> P2S_INVALID_ARG):
+ * P2S_NO_FUSED, P2S_FORCE_GENERIC, P2S_JIT (0: no generated module),
+ * P2S_FORCE_JIT, P2S_FUSED_VARIANT / P2S_V2_VARIANT / P2S_MV2_VARIANT (k-th
+ * registered variant), P2S_CHUNK_MB, P2S_TWO_STAGE_OVERLAP, P2S_MOM_PRIO,
+ * P2S_HOST_CHUNK_MB, P2S_GEO_MODE, P2S_GEO_CHUNK_MB, P2S_XCHUNK_MB and the
+ * large-path switches P2S_LARGE_* (see p2s_capi.cu).  The library never reads
+ * these from the environment. */
+p2s_status p2s_create_ex(const p2s_problem* spec, int device, const char* options, p2s_ctx** out);
+
+/* Plans the problem and builds (or finds) its generated module without touching
+ * a device -- ahead-of-time warm-up of the module cache (build scripts, CI).
+ * desc (may be NULL) receives the plan and the module path. */
+p2s_status p2s_shape_prepare(const p2s_problem* spec, char* desc, int desc_len);
+
+/* Directory of this library's generated modules (root/<kernel-header hash>). */
+const char* p2s_jit_cache_dir(void);
 void p2s_destroy(p2s_ctx* ctx);
 
 p2s_status p2s_get_sizes(const p2s_ctx* ctx, p2s_sizes* out);
+/* The same sizes from the problem alone (no context, no device). */
+p2s_status p2s_problem_sizes(const p2s_problem* spec, p2s_sizes* out);
 
 /* Moment stage:  I_s[k1][k2][k3] = sum_q w_q alpha_s(q) P_k1(u) P_k2(v) P_k3(w). */
 p2s_status p2s_moments(p2s_ctx* ctx, const double* d_alpha, double* d_I, int64_t n_elem,
@@ -152,7 +179,11 @@ p2s_status p2s_alpha_generate(p2s_ctx* ctx, int alpha_kind, double lo, double hi
  *                            on an internal stream while the fill consumes the
  *                            other, so alpha never round-trips through HBM; equal
  *                            bit for bit to p2s_fill(p2s_alpha_from_geometry(...)).
- *                            Not re-entrant on one context (internal buffers). */
+ *                            Not re-entrant on one context (internal buffers).
+ * Both geometry entry points wait for their stream and return P2S_GEOMETRY_ERROR
+ * when the Jacobian determinant is <= 0 at any quadrature point of any element
+ * (the reference's GeometryError, assembly.cpp:95-99); the outputs of such a call
+ * are unspecified. */
 #define P2S_GEOM_DOUBLES 28
 p2s_status p2s_geometry_generate(p2s_ctx* ctx, double lo, double hi, uint64_t seed, int64_t e0,
                                  int64_t n_elem, double* d_geom, void* stream);
@@ -199,7 +230,8 @@ p2s_status p2s_scatter_add(const double* d_elem, int64_t elem_stride, int64_t ld
                            const int32_t* d_dof_free, const double* d_dof_sign, int64_t n_elem,
                            double* d_G, int64_t ld_G, void* stream);
 
-/* 1 if the orders / kinds have a compiled kernel instantiation. */
+/* 1 if p2s_create accepts the problem here: an ahead-of-time kernel, or a
+ * generated module that is cached or can be compiled (nvcc present). */
 int p2s_shape_supported(const p2s_problem* spec);
 
 /* Thread-local description of the last failure on this thread. */

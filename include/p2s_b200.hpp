@@ -64,12 +64,25 @@ struct Orders {
   bool operator==(const Orders& o) const { return Nu == o.Nu && Nv == o.Nv && Nw == o.Nw; }
 };
 
+// Quadrature points per direction when the caller passes nq <= 0: the
+// reference's policy max(M, N) + geometric order + 6 (default_quad_points,
+// assembly.cpp:23-25, applied by assemble_system at :704-706), here over the
+// three orders; geometric order 1 = the trilinear hexahedron.
+inline int default_quad_points(const Orders& o, int geometric_order = 1) {
+  int m = o.Nu > o.Nv ? o.Nu : o.Nv;
+  m = m > o.Nw ? m : o.Nw;
+  return m + geometric_order + 6;
+}
+
 struct Problem {
   int n_comp = 1;
   Orders orders;
   std::vector<Term> terms{Term{}};
-  std::array<int, 3> nq{8, 8, 8};
+  std::array<int, 3> nq{0, 0, 0};  // <= 0: default_quad_points(orders, geometric_order)
+  int geometric_order = 1;
   bool conforming = false;  // conforming basis (reference apply_conforming_transform)
+
+  int resolved_nq(int d) const { return nq[d] > 0 ? nq[d] : default_quad_points(orders, geometric_order); }
 
   p2s_problem c() const {
     p2s_problem p{};
@@ -83,14 +96,16 @@ struct Problem {
       p.kind[s][1] = static_cast<int>(terms[s].v);
       p.kind[s][2] = static_cast<int>(terms[s].w);
     }
-    for (int d = 0; d < 3; ++d) p.nq[d] = nq[d];
+    for (int d = 0; d < 3; ++d) p.nq[d] = resolved_nq(d);
     p.basis = conforming ? P2S_BASIS_CONFORMING : P2S_BASIS_MODAL;
     return p;
   }
   bool same_shape(const Problem& o) const {
-    if (n_comp != o.n_comp || !(orders == o.orders) || nq != o.nq || terms.size() != o.terms.size() ||
+    if (n_comp != o.n_comp || !(orders == o.orders) || terms.size() != o.terms.size() ||
         conforming != o.conforming)
       return false;
+    for (int d = 0; d < 3; ++d)
+      if (resolved_nq(d) != o.resolved_nq(d)) return false;
     for (size_t s = 0; s < terms.size(); ++s)
       if (terms[s].u != o.terms[s].u || terms[s].v != o.terms[s].v || terms[s].w != o.terms[s].w)
         return false;
@@ -160,24 +175,39 @@ class DirectContext {
 };
 
 // Moment integrals of a batch of elements (reference: KernelTable, assembly.hpp:35-40).
+// Counters as the reference's (assembly.cpp:291-310): n_integrals = moment
+// entries computed (one tensor quadrature each), n_mass_uu_integrals = those of
+// the mass term (term 0) of the (0, 0) component pair -- the Kuu table's count.
 struct KernelTable {
   Problem problem;
   int64_t n_elem = 0;
   std::vector<double> I;   // [n_elem][moments_per_elem]
-  long n_integrals = 0;    // moment entries computed (counter of assembly.hpp:38)
+  long n_integrals = 0;
+  long n_mass_uu_integrals = 0;
 };
 
 // Element matrices of a batch (reference: ElementMatrices, assembly.hpp:20-26);
-// matrix e occupies M[e * n_tot * n_tot ...], row-major.
+// matrix e occupies M[e * n_tot * n_tot ...], row-major.  The counters are the
+// kernel tables' (set by fill_elements like fill_one, assembly.cpp:665-666).
 struct ElementMatrices {
   Problem problem;
   int64_t n_elem = 0;
   int n_tot = 0;
   std::vector<double> M;
+  long n_integrals = 0;
+  long n_mass_uu_integrals = 0;
   double operator()(int64_t e, int i, int j) const {
     return M[static_cast<size_t>((e * n_tot + i) * n_tot + j)];
   }
 };
+
+// moment entries per element, all terms and pairs / the mass term of pair (0, 0)
+inline void integral_counts(const p2s_sizes& sz, int n_terms, long* all, long* mass_uu) {
+  long per = 0;
+  for (int s = 0; s < n_terms; ++s) per += static_cast<long>(sz.K[s][0]) * sz.K[s][1] * sz.K[s][2];
+  *all = per * sz.n_pairs;
+  *mass_uu = static_cast<long>(sz.K[0][0]) * sz.K[0][1] * sz.K[0][2];
+}
 
 inline KernelTable compute_kernel_tables(Context& ctx, const std::vector<double>& alpha) {
   if (alpha.size() % static_cast<size_t>(ctx.alpha_per_elem()) != 0)
@@ -187,10 +217,10 @@ inline KernelTable compute_kernel_tables(Context& ctx, const std::vector<double>
   kt.n_elem = static_cast<int64_t>(alpha.size()) / ctx.alpha_per_elem();
   kt.I.assign(static_cast<size_t>(kt.n_elem * ctx.moments_per_elem()), 0.0);
   check(p2s_moments_host(ctx.handle(), alpha.data(), kt.I.data(), kt.n_elem));
-  long per = 0;
-  for (int s = 0; s < static_cast<int>(kt.problem.terms.size()); ++s)
-    per += static_cast<long>(ctx.sizes().K[s][0]) * ctx.sizes().K[s][1] * ctx.sizes().K[s][2];
-  kt.n_integrals = per * ctx.sizes().n_pairs * kt.n_elem;
+  long all = 0, muu = 0;
+  integral_counts(ctx.sizes(), static_cast<int>(kt.problem.terms.size()), &all, &muu);
+  kt.n_integrals = all * kt.n_elem;
+  kt.n_mass_uu_integrals = muu * kt.n_elem;
   return kt;
 }
 
@@ -203,27 +233,41 @@ inline ElementMatrices assemble_p2s_element(Context& ctx, const KernelTable& kt)
   em.n_tot = ctx.n_tot();
   em.M.assign(static_cast<size_t>(em.n_elem) * em.n_tot * em.n_tot, 0.0);
   check(p2s_contract_host(ctx.handle(), kt.I.data(), em.M.data(), em.n_tot, em.n_elem));
+  em.n_integrals = kt.n_integrals;
+  em.n_mass_uu_integrals = kt.n_mass_uu_integrals;
   return em;
 }
 
+// Partition of n elements over g workers: worker w owns [n w / g, n (w+1) / g).
+inline std::pair<int64_t, int64_t> element_range(int64_t n, int w, int g) {
+  return {n * w / g, n * (w + 1) / g};
+}
+
 // Batch fill on `gpus` devices: contiguous element ranges, one host thread
-// per GPU, first exception rethrown after all workers joined; the result is
-// independent of the GPU count (elements are independent).
+// (and one context) per GPU, first exception rethrown after all workers joined;
+// the result is independent of the GPU count (elements are independent).
 inline ElementMatrices fill_elements(const Problem& pb, const std::vector<double>& alpha, int gpus = 1) {
+  if (gpus < 1) throw std::invalid_argument("fill_elements: gpus must be >= 1");
   const p2s_problem cp = pb.c();
-  Context probe(pb, 0);
-  const int64_t ape = probe.alpha_per_elem();
+  p2s_sizes sz{};
+  check(p2s_problem_sizes(&cp, &sz));  // no device, no context
+  const int64_t ape = sz.alpha_per_elem;
   if (alpha.size() % static_cast<size_t>(ape) != 0)
     throw std::invalid_argument("fill_elements: alpha size is not a whole number of elements");
   ElementMatrices em;
   em.problem = pb;
   em.n_elem = static_cast<int64_t>(alpha.size()) / ape;
-  em.n_tot = probe.n_tot();
+  em.n_tot = sz.n_tot;
+  long all = 0, muu = 0;
+  integral_counts(sz, cp.n_terms, &all, &muu);
+  em.n_integrals = all * em.n_elem;
+  em.n_mass_uu_integrals = muu * em.n_elem;
   const int64_t mel = static_cast<int64_t>(em.n_tot) * em.n_tot;
   em.M.assign(static_cast<size_t>(em.n_elem * mel), 0.0);
-  if (gpus < 1) throw std::invalid_argument("fill_elements: gpus must be >= 1");
+  if (em.n_elem == 0) return em;
   if (gpus == 1 || em.n_elem <= 1) {
-    check(p2s_fill_host(probe.handle(), alpha.data(), em.M.data(), em.n_tot, em.n_elem));
+    Context ctx(pb, 0);
+    check(p2s_fill_host(ctx.handle(), alpha.data(), em.M.data(), em.n_tot, em.n_elem));
     return em;
   }
   std::exception_ptr error;
@@ -232,7 +276,8 @@ inline ElementMatrices fill_elements(const Problem& pb, const std::vector<double
   for (int g = 0; g < gpus; ++g) {
     pool.emplace_back([&, g] {
       try {
-        const int64_t e0 = em.n_elem * g / gpus, e1 = em.n_elem * (g + 1) / gpus;
+        const auto r = element_range(em.n_elem, g, gpus);
+        const int64_t e0 = r.first, e1 = r.second;
         if (e1 <= e0) return;
         Context ctx(pb, g);
         check(p2s_fill_host(ctx.handle(), alpha.data() + e0 * ape, em.M.data() + e0 * mel, em.n_tot,
@@ -245,7 +290,6 @@ inline ElementMatrices fill_elements(const Problem& pb, const std::vector<double
   }
   for (std::thread& t : pool) t.join();
   if (error) std::rethrow_exception(error);
-  (void)cp;
   return em;
 }
 

@@ -31,7 +31,8 @@ EXPORTS = ("p2s_create", "p2s_destroy", "p2s_get_sizes", "p2s_moments", "p2s_con
            "p2s_cheb2d_kernel_tables", "p2s_cheb2d_assemble",
            "p2s_direct_create", "p2s_direct_destroy", "p2s_direct_fill",
            "p2s_scatter_add", "p2s_cheb2d_scatter",
-           "p2s_geometry_generate", "p2s_alpha_from_geometry", "p2s_fill_geometry")
+           "p2s_geometry_generate", "p2s_alpha_from_geometry", "p2s_fill_geometry",
+           "p2s_create_ex", "p2s_shape_prepare", "p2s_jit_cache_dir", "p2s_problem_sizes")
 
 
 class P2SError(RuntimeError):
@@ -107,9 +108,13 @@ def lib():
         L = C.CDLL(LIB_PATH)
         vp, i64, dp = C.c_void_p, C.c_int64, C.POINTER(C.c_double)
         L.p2s_create.argtypes = [C.POINTER(Problem), C.c_int, C.POINTER(vp)]
+        L.p2s_create_ex.argtypes = [C.POINTER(Problem), C.c_int, C.c_char_p, C.POINTER(vp)]
+        L.p2s_shape_prepare.argtypes = [C.POINTER(Problem), C.c_char_p, C.c_int]
+        L.p2s_jit_cache_dir.restype = C.c_char_p
         L.p2s_destroy.argtypes = [vp]
         L.p2s_destroy.restype = None
         L.p2s_get_sizes.argtypes = [vp, C.POINTER(Sizes)]
+        L.p2s_problem_sizes.argtypes = [C.POINTER(Problem), C.POINTER(Sizes)]
         L.p2s_moments.argtypes = [vp, vp, vp, i64, vp]
         L.p2s_contract.argtypes = [vp, vp, vp, i64, i64, vp]
         L.p2s_fill.argtypes = [vp, vp, vp, i64, i64, vp]
@@ -144,6 +149,7 @@ def lib():
         L.p2s_cheb2d_scatter.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp]
         for f in EXPORTS:
             if f not in ("p2s_destroy", "p2s_shape_supported", "p2s_last_error", "p2s_version",
+                         "p2s_jit_cache_dir",
                          "p2s_kernel_path", "p2s_cheb2d_destroy", "p2s_direct_destroy"):
                 getattr(L, f).restype = C.c_int
         _lib = L
@@ -185,6 +191,39 @@ def shape_supported_basis(n_comp, order, kinds, nq, basis) -> bool:
     return bool(lib().p2s_shape_supported(C.byref(make_problem(n_comp, order, kinds, nq, basis))))
 
 
+def shape_prepare(n_comp, order, kinds, nq, basis=BASIS_MODAL) -> str:
+    """Build (or find) the generated kernel module of a shape without a device
+    (p2s_shape_prepare); returns the plan and module path."""
+    buf = C.create_string_buffer(1024)
+    _check(lib().p2s_shape_prepare(C.byref(make_problem(n_comp, order, kinds, nq, basis)), buf, 1024))
+    return buf.value.decode()
+
+
+# Test / tuning hooks (p2s_create_ex options) applied to every Context created
+# without explicit options -- the tests set them with monkeypatch.setitem; the
+# library itself never reads the environment.
+DEFAULT_OPTIONS: dict = {}
+
+
+def problem_sizes(n_comp, order, kinds, nq, basis=BASIS_MODAL) -> Sizes:
+    """p2s_problem_sizes: buffer sizes without a context or device."""
+    sz = Sizes()
+    _check(lib().p2s_problem_sizes(C.byref(make_problem(n_comp, order, kinds, nq, basis)), C.byref(sz)))
+    return sz
+
+
+def jit_cache_dir() -> str:
+    """Directory of the generated kernel modules of this library build."""
+    return lib().p2s_jit_cache_dir().decode()
+
+
+def options_string(options) -> bytes | None:
+    """{"P2S_NO_FUSED": "1", ...} -> b"P2S_NO_FUSED=1;..." (p2s_create_ex test/tuning hooks)."""
+    if not options:
+        return None
+    return ";".join(f"{k}={v}" for k, v in options.items()).encode()
+
+
 def _ptr(t) -> int:
     """Raw pointer of a torch tensor / int."""
     if t is None:
@@ -201,7 +240,8 @@ def _ptr(t) -> int:
 class Context:
     """One p2s_ctx (tables uploaded once) on one device."""
 
-    def __init__(self, n_comp, order, kinds, nq, device: int = 0, basis: int = BASIS_MODAL):
+    def __init__(self, n_comp, order, kinds, nq, device: int = 0, basis: int = BASIS_MODAL,
+                 options: dict | None = None):
         self.problem = make_problem(n_comp, order, kinds, nq, basis)
         self.n_comp = n_comp
         self.order = tuple(order)
@@ -209,7 +249,9 @@ class Context:
         self.nq = tuple(nq)
         self.device = device
         h = C.c_void_p()
-        _check(lib().p2s_create(C.byref(self.problem), device, C.byref(h)))
+        opts = dict(DEFAULT_OPTIONS)
+        opts.update(options or {})
+        _check(lib().p2s_create_ex(C.byref(self.problem), device, options_string(opts), C.byref(h)))
         self.h = h
         sz = Sizes()
         _check(lib().p2s_get_sizes(self.h, C.byref(sz)))
@@ -355,7 +397,8 @@ class DirectContext:
     """Direct-quadrature fill (p2s_direct_*): the ablation baseline, reference
     assemble_direct_element (assembly.hpp:50; assembly.cpp:134-274) in 3-D."""
 
-    def __init__(self, n_comp, order, kinds, nq, device: int = 0, basis: int = BASIS_MODAL):
+    def __init__(self, n_comp, order, kinds, nq, device: int = 0, basis: int = BASIS_MODAL,
+                 options: dict | None = None):
         self.problem = make_problem(n_comp, order, kinds, nq, basis)
         self.n_tot = n_comp * order[0] * order[1] * order[2]
         h = C.c_void_p()

@@ -45,6 +45,9 @@ CONFIGS = {
                      "3-component, anisotropic (10,6,4), 16^3 GL"),
     "c5": FillConfig("c5", 1, (16, 16, 16), (PP, DD), (36, 36, 36), 32768, ALPHA_SINE, 0.5, 12.0,
                      "scalar, order 16, frequency up to 12, 36^3 GL"),
+    # drop-in coverage bench line (no ahead-of-time kernel: generated module)
+    "c12": FillConfig("c12", 1, (12, 12, 12), (PP, DD), (18, 18, 18), 8192, ALPHA_SINE, 0.5, 3.0,
+                      "scalar, order 12 (PAPER.md Table I M=N=12), 18^3 GL, generated module"),
 }
 
 

@@ -6,7 +6,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cctype>
 #include <cstdio>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -14,6 +16,8 @@
 #include <vector>
 
 #include "../../include/p2s_b200.h"
+#include "p2s_jit.hpp"
+#include "p2s_launch.cuh"
 #include "p2s_registry.hpp"
 #include "p2s_tables.hpp"
 
@@ -22,7 +26,7 @@ cudaError_t launch_geometry(double* geom, double lo, double hi, uint64_t seed, i
                             cudaStream_t stream);
 cudaError_t launch_alpha_geometry_fast(double* alpha, const double* geom, const double* const x[3],
                                        const int nq[3], int nc, int S, int64_t n, int64_t per_elem,
-                                       cudaStream_t stream);
+                                       int* bad, cudaStream_t stream);
 cudaError_t launch_alpha(double* alpha, const double* const x[3], const int nq[3], int nc, int S,
                          int kind, double lo, double hi, uint64_t seed, int64_t e0, int64_t n,
                          int64_t per_elem, cudaStream_t stream);
@@ -50,6 +54,65 @@ p2s_status cuda_fail(cudaError_t err, const char* where) {
 using namespace p2s;
 using namespace p2s::reg;
 
+// ------------------------------------------------------------ options
+// Test and tuning hooks, passed explicitly to p2s_create_ex as "KEY=VALUE"
+// pairs (';' / ',' / whitespace separated).  The production library never
+// reads them from the environment (a tuning build, -DP2S_TUNING, falls back to
+// environment variables of the same names for the sweep scripts in tools/).
+const char* const kOptionKeys[] = {
+    "P2S_NO_FUSED",         // 1: two-stage path even where a fused kernel exists
+    "P2S_FUSED_VARIANT",    // k: the k-th registered fused variant of the shape
+    "P2S_V2_VARIANT",       // k: the k-th registered contract_v2 variant
+    "P2S_MV2_VARIANT",      // k: the k-th registered moments_v2 variant
+    "P2S_FORCE_GENERIC",    // 1: runtime-shaped generic kernels (where compiled)
+    "P2S_JIT",              // 0: never use a generated module
+    "P2S_FORCE_JIT",        // 1: a generated module even for registered shapes
+    "P2S_GEO_MODE",         // geometry fill mode 0 / 1 / 2
+    "P2S_XCHUNK_MB",        // large path: intermediate chunk (MB)
+    "P2S_LARGE_PS", "P2S_LARGE_OVERLAP", "P2S_LARGE_PRIO", "P2S_LARGE_USTREAMS", "P2S_LARGE_UPERSIST",
+    "P2S_LARGE_XS", "P2S_LARGE_MOMCL", "P2S_LARGE_USMEM", "P2S_LARGE_FIB",
+    "P2S_CHUNK_MB",         // two-stage scheduler chunk (MB of moments)
+    "P2S_TWO_STAGE_OVERLAP", "P2S_MOM_PRIO",
+    "P2S_HOST_CHUNK_MB",    // p2s_fill_host ring slot (MB of matrices)
+    "P2S_GEO_CHUNK_MB",     // p2s_fill_geometry alpha buffer (MB)
+};
+
+struct Options {
+  std::map<std::string, std::string> kv;
+  const char* get(const char* k) const {
+    auto it = kv.find(k);
+    if (it != kv.end()) return it->second.c_str();
+    return tuning_env(k);
+  }
+};
+
+bool parse_options(const char* text, Options* o, std::string* err) {
+  if (!text) return true;
+  std::string tok;
+  auto flush = [&]() -> bool {
+    if (tok.empty()) return true;
+    const size_t eq = tok.find('=');
+    const std::string k = tok.substr(0, eq), v = eq == std::string::npos ? "1" : tok.substr(eq + 1);
+    bool known = false;
+    for (const char* kk : kOptionKeys) known = known || k == kk;
+    if (!known) {
+      *err = "unknown option '" + k + "'";
+      return false;
+    }
+    o->kv[k] = v;
+    tok.clear();
+    return true;
+  };
+  for (const char* p = text; *p; ++p) {
+    if (*p == ';' || *p == ',' || std::isspace(static_cast<unsigned char>(*p))) {
+      if (!flush()) return false;
+    } else {
+      tok.push_back(*p);
+    }
+  }
+  return flush();
+}
+
 // ------------------------------------------------------------ registry lookup
 
 const RegEntry* find_entry(const p2s_problem& pb) {
@@ -63,9 +126,9 @@ const RegEntry* find_entry(const p2s_problem& pb) {
 }
 
 
-const V2Entry* find_v2(const p2s_problem& pb) {
+const V2Entry* find_v2(const p2s_problem& pb, const Options& o) {
   int want = 0, seen = 0;
-  if (const char* v = std::getenv("P2S_V2_VARIANT")) want = std::atoi(v);
+  if (const char* v = o.get("P2S_V2_VARIANT")) want = std::atoi(v);
   const V2Entry* first = nullptr;
   for (const V2Entry& r : v2_registry()) {
     bool ok = r.S == pb.n_terms;
@@ -80,9 +143,9 @@ const V2Entry* find_v2(const p2s_problem& pb) {
 }
 
 
-const MV2Entry* find_mv2(const p2s_problem& pb) {
+const MV2Entry* find_mv2(const p2s_problem& pb, const Options& o) {
   int want = 0, seen = 0;
-  if (const char* v = std::getenv("P2S_MV2_VARIANT")) want = std::atoi(v);
+  if (const char* v = o.get("P2S_MV2_VARIANT")) want = std::atoi(v);
   const MV2Entry* first = nullptr;
   for (const MV2Entry& r : mv2_registry()) {
     bool ok = r.S == pb.n_terms;
@@ -97,11 +160,11 @@ const MV2Entry* find_mv2(const p2s_problem& pb) {
 }
 
 
-const FusedEntry* find_fused(const p2s_problem& pb) {
-  if (const char* v = std::getenv("P2S_NO_FUSED"))
+const FusedEntry* find_fused(const p2s_problem& pb, const Options& o) {
+  if (const char* v = o.get("P2S_NO_FUSED"))
     if (v[0] == '1') return nullptr;
   int want = 0, seen = 0;
-  const char* var = std::getenv("P2S_FUSED_VARIANT");
+  const char* var = o.get("P2S_FUSED_VARIANT");
   if (var) want = std::atoi(var);
   const FusedEntry* first = nullptr;
   for (const FusedEntry& r : fused_registry()) {
@@ -139,6 +202,9 @@ const LargeEntry* find_large(const p2s_problem& pb) {
 struct p2s_ctx {
   p2s_problem pb{};
   int device = 0;
+  Options opt;
+  const reg::JitEntries* jit = nullptr;  // generated module (shapes without a registered kernel)
+  std::string jit_desc;
   p2s_sizes sz{};
   std::vector<double> x[3], w[3];
   std::vector<double> phi[kMaxTerms][3];   // [K][nq]
@@ -186,6 +252,8 @@ struct p2s_ctx {
                      // 1 per-unit recomputation inside the fused kernel; 2 one cluster per
                      // element sharing the per-point geometry through DSMEM
   double* d_geo_alpha[2]{};
+  int* d_bad = nullptr;  // non-positive Jacobian flag of the geometry entry points
+  int* h_bad = nullptr;  // (pinned host copy)
   cudaStream_t s_geo = nullptr;
   cudaEvent_t ev_geo_start = nullptr, ev_ga[2]{}, ev_gf[2]{};
   // profiling
@@ -374,7 +442,7 @@ p2s_status run_fill(p2s_ctx* c, const double* alpha, double* M, int64_t ldM, int
     cudaError_t err = c->fused->launch(alpha, M, ldM, c->sz.n_tot, n, c->pb.n_comp, c->sz.n_pairs,
                                        c->pb.order[0] * c->pb.order[1] * c->pb.order[2],
                                        c->fused_cpack, c->fused_mpack, c->d_amma_fused, st,
-                                       c->num_sms);
+                                       c->num_sms, nullptr);
     if (err != cudaSuccess) return cuda_fail(err, "fill_fused_kernel launch");
     if (c->prof) {
       cudaEventRecord(e1, st);
@@ -418,6 +486,28 @@ p2s_status run_fill(p2s_ctx* c, const double* alpha, double* M, int64_t ldM, int
   return P2S_OK;
 }
 
+// buffer sizes and moment layout of a problem (basis-independent)
+void problem_sizes(const p2s_problem& pb, p2s_sizes* sz) {
+  *sz = p2s_sizes{};
+  const int S = pb.n_terms, nc = pb.n_comp;
+  sz->n_pairs = nc * nc;
+  sz->n_tot = nc * pb.order[0] * pb.order[1] * pb.order[2];
+  sz->alpha_per_elem = static_cast<int64_t>(sz->n_pairs) * S * pb.nq[0] * pb.nq[1] * pb.nq[2];
+  int64_t off = 0;
+  for (int s = 0; s < S; ++s) {
+    sz->moment_offset[s] = off;
+    int64_t kk = 1;
+    for (int d = 0; d < 3; ++d) {
+      const int K = kernel_count(pb.kind[s][d], pb.order[d]);
+      sz->K[s][d] = K;
+      kk *= K;
+    }
+    off += kk;
+  }
+  sz->moments_per_pair = (off + 3) & ~int64_t(3);
+  sz->moments_per_elem = sz->moments_per_pair * sz->n_pairs;
+}
+
 p2s_status check_ctx(const p2s_ctx* c) {
   if (!c) return fail(P2S_INVALID_ARG, "null context");
   return P2S_OK;
@@ -431,45 +521,126 @@ extern "C" {
 
 const char* p2s_last_error(void) { return g_last_error.c_str(); }
 
-const char* p2s_version(void) { return "p2s_b200 0.1 (sm_100a)"; }
+const char* p2s_version(void) { return "p2s_b200 0.2 (sm_100a)"; }
+
+const char* p2s_jit_cache_dir(void) {
+  static thread_local std::string d;
+  d = jit::cache_dir();
+  return d.c_str();
+}
 
 const char* p2s_kernel_path(const p2s_ctx* c) {
   if (!c) return "";
-  if (c->large) return "large-order: large_moments_kernel + large_w_kernel + large_v_kernel + large_u_kernel";
   static thread_local std::string path;
-  if (c->fused) {
+  if (c->large) {
+    path = "large-order: large_moments_kernel + large_w_kernel + large_v_kernel + large_u_kernel";
+  } else if (c->fused) {
     path = std::string("fused: fill_fused_kernel (moments + contraction; ") + c->fused->desc + ")";
-    return path.c_str();
-  }
-  if (c->v2 && !c->force_generic) {
+  } else if (c->v2 && !c->force_generic) {
     path = std::string(c->mv2 ? "two-stage: moments_v2_kernel + contract_v2_kernel ("
                               : "two-stage: moments_kernel + contract_v2_kernel (") +
            c->v2->desc + ")";
-    return path.c_str();
+  } else {
+    path = c->mv2 && !c->force_generic ? "two-stage: moments_v2_kernel + contract_kernel"
+                                       : "two-stage: moments_kernel + contract_kernel (generic)";
   }
-  return c->mv2 && !c->force_generic ? "two-stage: moments_v2_kernel + contract_kernel"
-                                     : "two-stage: moments_kernel + contract_kernel (generic)";
+  if (c->jit) path += " [generated module: " + c->jit_desc + "]";
+  return path.c_str();
 }
 
 int p2s_shape_supported(const p2s_problem* spec_in) {
   if (!spec_in || validate(spec_in) != P2S_OK) return 0;
   const p2s_problem eff = effective(*spec_in);
-  return find_entry(eff) != nullptr || find_v2(eff) != nullptr || find_large(eff) != nullptr;
+  if (find_v2(eff, Options{}) != nullptr || find_large(eff) != nullptr) return 1;
+  jit::Plan pl;
+  std::string why;
+  if (jit::plan(eff, &pl, &why) && (jit::cached(pl) || jit::compiler_available())) return 1;
+  return find_entry(eff) != nullptr;
 }
 
 p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
+  return p2s_create_ex(spec_in, device, nullptr, out);
+}
+
+p2s_status p2s_shape_prepare(const p2s_problem* spec_in, char* desc, int desc_len) {
+  p2s_status st = validate(spec_in);
+  if (st != P2S_OK) return st;
+  const p2s_problem eff = effective(*spec_in);
+  std::string d;
+  if (find_v2(eff, Options{}) || find_large(eff)) {
+    d = "registered (ahead of time)";
+  } else {
+    jit::Plan pl;
+    std::string why;
+    if (!jit::plan(eff, &pl, &why)) return fail(P2S_UNSUPPORTED_SHAPE, "p2s_shape_prepare: " + why);
+    if (!jit::module(pl, &why)) return fail(P2S_UNSUPPORTED_SHAPE, "p2s_shape_prepare: " + why);
+    d = pl.desc + " | " + jit::module_path(pl);
+  }
+  if (desc && desc_len > 0) {
+    std::strncpy(desc, d.c_str(), static_cast<size_t>(desc_len) - 1);
+    desc[desc_len - 1] = '\0';
+  }
+  return P2S_OK;
+}
+
+p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* options, p2s_ctx** out) {
   if (!out) return fail(P2S_INVALID_ARG, "p2s_create: null out");
   *out = nullptr;
   p2s_status st = validate(spec_in);
   if (st != P2S_OK) return st;
+  Options opt;
+  {
+    std::string err;
+    if (!parse_options(options, &opt, &err)) return fail(P2S_INVALID_ARG, "p2s_create_ex: " + err);
+  }
   const p2s_problem eff = effective(*spec_in);
   const p2s_problem* spec = &eff;
+  auto flag = [&](const char* k) {
+    const char* v = opt.get(k);
+    return v && v[0] == '1';
+  };
+  const bool force_jit = flag("P2S_FORCE_JIT");
+  const bool no_jit = [&] {
+    const char* v = opt.get("P2S_JIT");
+    return v && v[0] == '0';
+  }();
   const RegEntry* entry = find_entry(*spec);
-  const V2Entry* v2e = find_v2(*spec);
-  const LargeEntry* lge = find_large(*spec);
+  const V2Entry* v2e = force_jit ? nullptr : find_v2(*spec, opt);
+  const LargeEntry* lge = force_jit ? nullptr : find_large(*spec);
+  const FusedEntry* fe = force_jit ? nullptr : find_fused(*spec, opt);
+  const MV2Entry* mv2e = force_jit ? nullptr : find_mv2(*spec, opt);
+  const bool want_generic = flag("P2S_FORCE_GENERIC") && entry;
+  // shapes without a shape-specialised kernel: a generated module (p2s_jit.cu)
+  const reg::JitEntries* je = nullptr;
+  std::string jit_desc;
+  if (!v2e && !lge && !want_generic && !no_jit) {
+    jit::Plan pl;
+    std::string why;
+    if (!jit::plan(*spec, &pl, &why)) {
+      if (!entry) return fail(P2S_UNSUPPORTED_SHAPE, "p2s_create: " + why);
+    } else {
+      je = jit::module(pl, &why);
+      if (!je && !entry) return fail(P2S_UNSUPPORTED_SHAPE, "p2s_create: generated module: " + why);
+      if (je && static_cast<int64_t>(je->smem) != pl.smem)
+        return fail(P2S_CUDA_ERROR, "p2s_create: generated module layout differs from the plan (" +
+                                        std::to_string(je->smem) + " vs " + std::to_string(pl.smem) + " B)");
+      jit_desc = pl.desc;
+    }
+  }
+  if (je) {
+    if (je->family == jit::kFamilyFused) {
+      v2e = &je->v2;
+      mv2e = &je->mv2;
+      fe = opt.get("P2S_NO_FUSED") && opt.get("P2S_NO_FUSED")[0] == '1' ? nullptr : &je->fused;
+    } else {
+      lge = &je->large;
+      fe = nullptr;
+      mv2e = nullptr;
+    }
+  }
   if (!entry && !v2e && !lge)
-    return fail(P2S_UNSUPPORTED_SHAPE, "p2s_create: no compiled contraction kernel for N_u=" +
-                                           std::to_string(spec->order[0]) + " with these u-kinds");
+    return fail(P2S_UNSUPPORTED_SHAPE, "p2s_create: no kernel for N_u=" + std::to_string(spec->order[0]) +
+                                           " with these u-kinds");
   int ndev = 0;
   cudaError_t err = cudaGetDeviceCount(&ndev);
   if (err != cudaSuccess || ndev == 0)
@@ -485,32 +656,21 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
   std::unique_ptr<p2s_ctx, void (*)(p2s_ctx*)> c(new p2s_ctx, &p2s_destroy);
   c->pb = *spec;
   c->device = device;
+  c->opt = opt;
+  c->jit = je;
+  c->jit_desc = jit_desc;
   c->entry = entry;
   c->v2 = v2e;
   c->num_sms = prop.multiProcessorCount;
-  if (const char* g = std::getenv("P2S_FORCE_GENERIC")) c->force_generic = entry && g[0] == '1';
-  const int S = spec->n_terms, nc = spec->n_comp;
-  c->sz.n_pairs = nc * nc;
-  c->sz.n_tot = nc * spec->order[0] * spec->order[1] * spec->order[2];
-  c->sz.alpha_per_elem =
-      static_cast<int64_t>(c->sz.n_pairs) * S * spec->nq[0] * spec->nq[1] * spec->nq[2];
-  int64_t off = 0;
+  c->force_generic = want_generic;
+  const int S = spec->n_terms;
+  problem_sizes(*spec, &c->sz);
   int kmax = 1;
-  for (int s = 0; s < S; ++s) {
-    c->sz.moment_offset[s] = off;
-    int64_t kk = 1;
-    for (int d = 0; d < 3; ++d) {
-      const int K = kernel_count(spec->kind[s][d], spec->order[d]);
-      c->sz.K[s][d] = K;
-      kk *= K;
-      kmax = std::max(kmax, K);
-    }
-    off += kk;
-  }
-  c->sz.moments_per_pair = (off + 3) & ~int64_t(3);
-  c->sz.moments_per_elem = c->sz.moments_per_pair * c->sz.n_pairs;
+  for (int s = 0; s < S; ++s)
+    for (int d = 0; d < 3; ++d) kmax = std::max(kmax, c->sz.K[s][d]);
   c->kmax = kmax <= 8 ? 8 : kmax <= 12 ? 12 : kmax <= 16 ? 16 : kmax <= 20 ? 20 : kmax <= 24 ? 24 : 32;
-  if (kmax > 32) return fail(P2S_UNSUPPORTED_SHAPE, "kernel count above 32");
+  if (kmax > 32 && !lge && !mv2e)  // the runtime-shaped moments_kernel holds <= 32 per direction
+    return fail(P2S_UNSUPPORTED_SHAPE, "kernel count above 32");
 
   // tables
   for (int d = 0; d < 3; ++d) {
@@ -538,7 +698,7 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
   std::vector<const std::vector<double>*> dense;
   for (int s = 0; s < S; ++s) dense.push_back(&c->coef[s][0]);
   if (entry) c->cu_packed = entry->pack(dense);
-  c->fused = find_fused(*spec);
+  c->fused = fe;
   if (c->fused) {
     V2Args v{};
     for (int s = 0; s < S; ++s)
@@ -551,8 +711,8 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
       P2S_CUDA(cudaMemcpy(c->d_amma_fused, A.data(), sizeof(double) * A.size(), cudaMemcpyHostToDevice));
     }
   }
-  if (const char* v = std::getenv("P2S_GEO_MODE")) c->geo_mode = std::atoi(v);
-  c->mv2 = find_mv2(*spec);
+  if (const char* v = opt.get("P2S_GEO_MODE")) c->geo_mode = std::atoi(v);
+  c->mv2 = mv2e;
   if (c->mv2) c->mv2_packed = c->mv2->pack(c->phi);
   if (v2e) {
     V2Args v{};
@@ -578,7 +738,7 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     msm = std::max(msm, t);
   }
   c->mom_smem = msm * sizeof(double);
-  if (!lge && c->mom_smem > 227 * 1024)
+  if (!lge && !c->mv2 && c->mom_smem > 227 * 1024)
     return fail(P2S_UNSUPPORTED_SHAPE, "moment stage needs more than 227 KB of shared memory");
 
   // contraction plan: G n1-values per CTA, ~256 fibers per CTA
@@ -612,9 +772,9 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     // X chunk: ~96 MB of v/w-contracted intermediates per buffer (two buffers: the
     // v/w stage of the next chunk overlaps the u stage of this one)
     int64_t xmb = 96;
-    if (const char* v = std::getenv("P2S_XCHUNK_MB")) xmb = std::max(1, std::atoi(v));
-    if (const char* v = std::getenv("P2S_LARGE_PS")) c->lpack.ps = v[0] != '0';
-    if (const char* v = std::getenv("P2S_LARGE_OVERLAP")) c->lpack.overlap = v[0] != '0';
+    if (const char* v = opt.get("P2S_XCHUNK_MB")) xmb = std::max(1, std::atoi(v));
+    if (const char* v = opt.get("P2S_LARGE_PS")) c->lpack.ps = v[0] != '0';
+    if (const char* v = opt.get("P2S_LARGE_OVERLAP")) c->lpack.overlap = v[0] != '0';
     c->xchunk = std::max<int64_t>(1, (xmb << 20) / (lge->xpu * 8));
     P2S_CUDA(cudaMalloc(&c->d_X, sizeof(double) * lge->xpu * c->xchunk * 2));
     P2S_CUDA(cudaMalloc(&c->lpack.d_Z, sizeof(double) * lge->zpu * c->xchunk));
@@ -624,19 +784,19 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     int prio_lo = 0, prio_hi = 0;
     P2S_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     bool hi = false;
-    if (const char* v = std::getenv("P2S_LARGE_PRIO")) hi = v[0] != '0';
+    if (const char* v = opt.get("P2S_LARGE_PRIO")) hi = v[0] != '0';
     P2S_CUDA(cudaStreamCreateWithPriority(&c->lpack.aux, cudaStreamNonBlocking, hi ? prio_hi : prio_lo));
     P2S_CUDA(cudaStreamCreateWithFlags(&c->lpack.aux_u, cudaStreamNonBlocking));
     P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_start, cudaEventDisableTiming));
     P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_join, cudaEventDisableTiming));
-    if (const char* v = std::getenv("P2S_LARGE_USTREAMS")) c->lpack.two_u = v[0] != '1';
+    if (const char* v = opt.get("P2S_LARGE_USTREAMS")) c->lpack.two_u = v[0] != '1';
     c->lpack.u_ctas = 2 * static_cast<int64_t>(c->num_sms);  // persistent u stage, 2 CTAs per SM
-    if (const char* v = std::getenv("P2S_LARGE_UPERSIST"))
+    if (const char* v = opt.get("P2S_LARGE_UPERSIST"))
       c->lpack.u_ctas = static_cast<int64_t>(std::max(0, std::atoi(v))) * c->num_sms;
-    if (const char* v = std::getenv("P2S_LARGE_XS")) c->lpack.u_xs = v[0] != '0';
-    if (const char* v = std::getenv("P2S_LARGE_MOMCL")) c->lpack.mom_cluster = v[0] == '1';
-    if (const char* v = std::getenv("P2S_LARGE_USMEM")) c->lpack.u_smemc = v[0] == '1';
-    if (const char* v = std::getenv("P2S_LARGE_FIB")) c->lpack.ufib = std::atoi(v) == 2 ? 2 : 1;
+    if (const char* v = opt.get("P2S_LARGE_XS")) c->lpack.u_xs = v[0] != '0';
+    if (const char* v = opt.get("P2S_LARGE_MOMCL")) c->lpack.mom_cluster = v[0] == '1';
+    if (const char* v = opt.get("P2S_LARGE_USMEM")) c->lpack.u_smemc = v[0] == '1';
+    if (const char* v = opt.get("P2S_LARGE_FIB")) c->lpack.ufib = std::atoi(v) == 2 ? 2 : 1;
     for (int b = 0; b < 2; ++b) {
       P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_vw[b], cudaEventDisableTiming));
       P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_u[b], cudaEventDisableTiming));
@@ -650,10 +810,10 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
   // costs less than the launch tails of small chunks
   const int64_t per = c->sz.moments_per_elem * 8;
   int64_t cmb = 256;
-  if (const char* v = std::getenv("P2S_CHUNK_MB")) cmb = std::max(1, std::atoi(v));
+  if (const char* v = opt.get("P2S_CHUNK_MB")) cmb = std::max(1, std::atoi(v));
   c->chunk = std::max<int64_t>(1, (cmb << 20) / per);
   bool overlap = !c->large && !c->fused;
-  if (const char* v = std::getenv("P2S_TWO_STAGE_OVERLAP")) overlap = overlap && v[0] != '0';
+  if (const char* v = opt.get("P2S_TWO_STAGE_OVERLAP")) overlap = overlap && v[0] != '0';
   P2S_CUDA(cudaMalloc(&c->d_scratch, sizeof(double) * c->sz.moments_per_elem * c->chunk * (overlap ? 2 : 1)));
   if (overlap) {
     // P2S_MOM_PRIO=1: the moments stream at the highest priority (its CTAs are
@@ -661,7 +821,7 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
     int plo = 0, phi = 0;
     P2S_CUDA(cudaDeviceGetStreamPriorityRange(&plo, &phi));
     bool mhi = false;
-    if (const char* v = std::getenv("P2S_MOM_PRIO")) mhi = v[0] == '1';
+    if (const char* v = opt.get("P2S_MOM_PRIO")) mhi = v[0] == '1';
     P2S_CUDA(cudaStreamCreateWithPriority(&c->s_mom, cudaStreamNonBlocking, mhi ? phi : plo));
     P2S_CUDA(cudaEventCreateWithFlags(&c->ev_fill_start, cudaEventDisableTiming));
     for (int b = 0; b < 2; ++b) {
@@ -694,6 +854,7 @@ void p2s_destroy(p2s_ctx* c) {
   if (c->d_X) cudaFree(c->d_X);
   if (c->lpack.d_Z) cudaFree(c->lpack.d_Z);
   if (c->lpack.d_cu) cudaFree(c->lpack.d_cu);
+  if (c->lpack.d_cvw) cudaFree(c->lpack.d_cvw);
   if (c->lpack.aux) cudaStreamDestroy(c->lpack.aux);
   if (c->lpack.aux_u) cudaStreamDestroy(c->lpack.aux_u);
   if (c->lpack.ev_start) cudaEventDestroy(c->lpack.ev_start);
@@ -709,6 +870,8 @@ void p2s_destroy(p2s_ctx* c) {
     if (c->ev_gf[b]) cudaEventDestroy(c->ev_gf[b]);
   }
   if (c->ev_geo_start) cudaEventDestroy(c->ev_geo_start);
+  if (c->d_bad) cudaFree(c->d_bad);
+  if (c->h_bad) cudaFreeHost(c->h_bad);
   if (c->s_geo) cudaStreamDestroy(c->s_geo);
   if (c->d_amma_v2) cudaFree(c->d_amma_v2);
   for (int i = 0; i < 2; ++i) {
@@ -724,6 +887,14 @@ void p2s_destroy(p2s_ctx* c) {
   harvest(c);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
+}
+
+p2s_status p2s_problem_sizes(const p2s_problem* spec, p2s_sizes* out) {
+  if (!out) return fail(P2S_INVALID_ARG, "p2s_problem_sizes: null out");
+  p2s_status st = validate(spec);
+  if (st != P2S_OK) return st;
+  problem_sizes(*spec, out);
+  return P2S_OK;
 }
 
 p2s_status p2s_get_sizes(const p2s_ctx* c, p2s_sizes* out) {
@@ -781,7 +952,7 @@ p2s_status p2s_fill_host(p2s_ctx* c, const double* h_alpha, double* h_M, int64_t
     // 64 MB 15.38 k, 256 MB 15.26 k, 1 GB 15.02 k elem/s: the D2H copy (51.7 GB/s of a
     // 56.4 GB/s PCIe peak) is the bound
     int64_t hmb = 64;
-    if (const char* v = std::getenv("P2S_HOST_CHUNK_MB")) hmb = std::max(1, std::atoi(v));
+    if (const char* v = c->opt.get("P2S_HOST_CHUNK_MB")) hmb = std::max(1, std::atoi(v));
     c->host_chunk = std::max<int64_t>(1, (hmb << 20) / (mel * 8));
     for (int i = 0; i < 2; ++i) {
       P2S_CUDA(cudaMalloc(&c->d_ring_alpha[i], sizeof(double) * ape * c->host_chunk));
@@ -883,17 +1054,43 @@ p2s_status p2s_geometry_generate(p2s_ctx* c, double lo, double hi, uint64_t seed
   return P2S_OK;
 }
 
+namespace {
+// GeometryError of the reference (assembly.cpp:95-99): the geometry entry points
+// clear a device flag, their kernels set it at any quadrature point with
+// det J <= 0, and the call waits for the stream and reports it
+p2s_status geo_flag_begin(p2s_ctx* c, cudaStream_t st) {
+  if (!c->d_bad) {
+    P2S_CUDA(cudaMalloc(&c->d_bad, sizeof(int)));
+    P2S_CUDA(cudaMallocHost(&c->h_bad, sizeof(int)));
+  }
+  P2S_CUDA(cudaMemsetAsync(c->d_bad, 0, sizeof(int), st));
+  return P2S_OK;
+}
+
+p2s_status geo_flag_end(p2s_ctx* c, cudaStream_t st, const char* where) {
+  P2S_CUDA(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  P2S_CUDA(cudaStreamSynchronize(st));
+  if (*c->h_bad)
+    return fail(P2S_GEOMETRY_ERROR, std::string(where) + ": non-positive Jacobian at a quadrature point");
+  return P2S_OK;
+}
+}  // namespace
+
 p2s_status p2s_alpha_from_geometry(p2s_ctx* c, const double* d_geom, int64_t n, double* d_alpha,
                                    void* stream) {
   if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
   if (n < 0 || (n > 0 && (!d_geom || !d_alpha)))
     return fail(P2S_INVALID_ARG, "p2s_alpha_from_geometry: bad buffer");
+  if (n == 0) return P2S_OK;
   P2S_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  p2s_status s0 = geo_flag_begin(c, st);
+  if (s0 != P2S_OK) return s0;
   const double* xs[3] = {c->d_x[0], c->d_x[1], c->d_x[2]};
   cudaError_t err = launch_alpha_geometry_fast(d_alpha, d_geom, xs, c->pb.nq, c->pb.n_comp, c->pb.n_terms,
-                                               n, c->sz.alpha_per_elem, static_cast<cudaStream_t>(stream));
+                                               n, c->sz.alpha_per_elem, c->d_bad, st);
   if (err != cudaSuccess) return cuda_fail(err, "alpha_geometry_kernel launch");
-  return P2S_OK;
+  return geo_flag_end(c, st, "p2s_alpha_from_geometry");
 }
 
 p2s_status p2s_fill_geometry(p2s_ctx* c, const double* d_geom, double* d_M, int64_t ld_M, int64_t n,
@@ -904,6 +1101,8 @@ p2s_status p2s_fill_geometry(p2s_ctx* c, const double* d_geom, double* d_M, int6
   if (!d_geom || !d_M) return fail(P2S_INVALID_ARG, "p2s_fill_geometry: null buffer");
   P2S_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  p2s_status s0 = geo_flag_begin(c, st);
+  if (s0 != P2S_OK) return s0;
   const fused_fn geo_launch = !c->fused              ? nullptr
                              : c->geo_mode == 2     ? c->fused->launch_geo_cluster
                              : c->geo_mode == 1     ? c->fused->launch_geo
@@ -914,14 +1113,14 @@ p2s_status p2s_fill_geometry(p2s_ctx* c, const double* d_geom, double* d_M, int6
     for (int d = 0; d < 3; ++d) mp.insert(mp.end(), c->x[d].begin(), c->x[d].end());
     cudaError_t err = geo_launch(d_geom, d_M, ld_M, c->sz.n_tot, n, c->pb.n_comp, c->sz.n_pairs,
                                  c->pb.order[0] * c->pb.order[1] * c->pb.order[2], c->fused_cpack, mp,
-                                 c->d_amma_fused, st, c->num_sms);
+                                 c->d_amma_fused, st, c->num_sms, c->d_bad);
     if (err != cudaSuccess) return cuda_fail(err, "fill_fused_kernel (geometry) launch");
-    return P2S_OK;
+    return geo_flag_end(c, st, "p2s_fill_geometry");
   }
   if (!c->s_geo) {  // lazily: two alpha buffers of ~48 MB (L2), a stream, events
     const int64_t per = c->sz.alpha_per_elem * 8;
     int64_t mb = 48;
-    if (const char* v = std::getenv("P2S_GEO_CHUNK_MB")) mb = std::max(1, std::atoi(v));
+    if (const char* v = c->opt.get("P2S_GEO_CHUNK_MB")) mb = std::max(1, std::atoi(v));
     c->geo_chunk = std::max<int64_t>(1, (mb << 20) / per);
     for (int b = 0; b < 2; ++b) {
       P2S_CUDA(cudaMalloc(&c->d_geo_alpha[b], static_cast<size_t>(per * c->geo_chunk)));
@@ -942,7 +1141,7 @@ p2s_status p2s_fill_geometry(p2s_ctx* c, const double* d_geom, double* d_M, int6
     if (i >= 2) P2S_CUDA(cudaStreamWaitEvent(c->s_geo, c->ev_gf[b], 0));  // buffer b free
     cudaError_t err = launch_alpha_geometry_fast(c->d_geo_alpha[b], d_geom + e0 * 28, xs, c->pb.nq,
                                                  c->pb.n_comp, c->pb.n_terms, cnt, c->sz.alpha_per_elem,
-                                                 c->s_geo);
+                                                 c->d_bad, c->s_geo);
     if (err != cudaSuccess) return cuda_fail(err, "alpha_geometry_kernel launch");
     P2S_CUDA(cudaEventRecord(c->ev_ga[b], c->s_geo));
     P2S_CUDA(cudaStreamWaitEvent(st, c->ev_ga[b], 0));
@@ -950,7 +1149,7 @@ p2s_status p2s_fill_geometry(p2s_ctx* c, const double* d_geom, double* d_M, int6
     if (s2 != P2S_OK) return s2;
     P2S_CUDA(cudaEventRecord(c->ev_gf[b], st));
   }
-  return P2S_OK;
+  return geo_flag_end(c, st, "p2s_fill_geometry");
 }
 
 p2s_status p2s_get_tables(const p2s_ctx* c, int term, int dir, double* phi, double* coef,

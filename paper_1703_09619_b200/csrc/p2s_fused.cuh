@@ -19,6 +19,7 @@ struct FusedParams {
   V2Params<Sh> c;      // contraction part (c.I unused)
   const double* alpha;
   const double* geom;  // GEO kernels: element geometry records (28 doubles each)
+  int* bad;            // GEO kernels: non-positive Jacobian flag
   double xq[Ms::Q(0) + Ms::Q(1) + Ms::Q(2)];  // GL nodes u, v, w (GEO kernels)
   int64_t prefetch_stride;  // resident CTAs on the GPU (non-persistent launch)
   double tab[Ms::TALL];
@@ -70,6 +71,7 @@ __device__ __forceinline__ void geo_cluster_phase(const GeoUnit& g, const double
     const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
                        J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
                        J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    if (!(det > 0.0)) atomicOr(g.bad, 1);
     double G[3][3];
 #pragma unroll
     for (int a1 = 0; a1 < 3; ++a1)
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
     const double* a = p.alpha + unit * (static_cast<int64_t>(Ms::S) * slab);
     if constexpr (GEO == 1) {
       __shared__ GeoUnit geo;
-      geo_unit_setup(p.geom + e * 28, gci, gcj, &geo);
+      geo_unit_setup(p.geom + e * 28, gci, gcj, &geo, p.bad);
       __syncthreads();
       static_assert(!Ms::WFIRST, "geometry mode uses the u-first pass order");
       moments_all_terms<Ms, Sh::THREADS, 1>(nullptr, p.tab, Abuf, Ibuf, &geo, p.xq);
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
       static_assert(!Ms::WFIRST, "geometry mode uses the u-first pass order");
       __shared__ GeoUnit geo;
       double* as = Abuf + FusedLayout<Sh, Ms, GEO>::AOFF;
-      geo_unit_setup(p.geom + e * 28, gci, gcj, &geo);
+      geo_unit_setup(p.geom + e * 28, gci, gcj, &geo, p.bad);
       cooperative_groups::this_cluster().sync();  // every CTA of the element resident, geo set
       if (p.c.nc == 3)
         geo_cluster_phase<Ms, 3, Sh::THREADS>(geo, p.xq, as, pair, p.c.P);

@@ -14,6 +14,8 @@
 // which rounds like the host): values agree with it to ~1e-15 relative.
 #include <cuda_runtime.h>
 
+#include "p2s_launch.cuh"
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -29,7 +31,7 @@ template <int NC, int S>
 __global__ void __launch_bounds__(256) alpha_geometry_fast_kernel(
     double* __restrict__ alpha, const double* __restrict__ geom, const double* __restrict__ x0,
     const double* __restrict__ x1, const double* __restrict__ x2, int nq0, int nq1, int nq2,
-    int64_t per_elem) {
+    int64_t per_elem, int* __restrict__ bad) {
   __shared__ double A[8][3];  // polynomial coefficients of the map, per component
   __shared__ double mat[4];
   __shared__ double xs[3][64];
@@ -83,6 +85,8 @@ __global__ void __launch_bounds__(256) alpha_geometry_fast_kernel(
         G[a1][a2] = J[0][a1] * J[0][a2] + J[1][a1] * J[1][a2] + J[2][a1] * J[2][a2];
         G[a2][a1] = G[a1][a2];
       }
+    // the reference throws GeometryError on J <= 0 (assembly.cpp:95-99): flag it
+    if (!(det > 0.0)) atomicOr(bad, 1);
     const double rdet = 1.0 / det;
     const double am = 1.0 + 0.3 * sin(mat[0] * u + mat[1] * v + mat[2] * w + mat[3]);
     const double ms = am * rdet;  // mass: am detJ (G^-1) = am cof(G) / detJ (det G = detJ^2)
@@ -112,22 +116,19 @@ __global__ void __launch_bounds__(256) alpha_geometry_fast_kernel(
 
 cudaError_t launch_alpha_geometry_fast(double* alpha, const double* geom, const double* const x[3],
                                        const int nq[3], int nc, int S, int64_t n, int64_t per_elem,
-                                       cudaStream_t stream) {
+                                       int* bad, cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
   if (nq[0] > 64 || nq[1] > 64 || nq[2] > 64) return cudaErrorInvalidValue;
   // points per thread (P2S_GEO_PPT, default 4): the per-CTA prologue (record ->
   // polynomial map, nodes) is amortised over several points per thread
-  static int ppt = -1;
-  if (ppt < 0) {
-    ppt = 4;
-    if (const char* v = std::getenv("P2S_GEO_PPT")) ppt = std::max(1, std::atoi(v));
-  }
+  int ppt = 4;
+  if (const char* v = tuning_env("P2S_GEO_PPT")) ppt = std::max(1, std::atoi(v));
   const unsigned slabs = static_cast<unsigned>((nq[0] * nq[1] * nq[2] + 256 * ppt - 1) / (256 * ppt));
   const dim3 grid(static_cast<unsigned>(n), slabs);
 #define P2S_GEO_CASE(NC_, S_)                                                                         \
   if (nc == NC_ && S == S_) {                                                                       \
     alpha_geometry_fast_kernel<NC_, S_><<<grid, 256, 0, stream>>>(alpha, geom, x[0], x[1], x[2], nq[0], \
-                                                                  nq[1], nq[2], per_elem);          \
+                                                                  nq[1], nq[2], per_elem, bad);          \
     return cudaGetLastError();                                                                      \
   }
   P2S_GEO_CASE(1, 1) P2S_GEO_CASE(1, 2) P2S_GEO_CASE(1, 3) P2S_GEO_CASE(1, 4)

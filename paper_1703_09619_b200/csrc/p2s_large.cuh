@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include "p2s_kernels.cuh"
+#include "p2s_launch.cuh"
 #include "p2s_moments_v2.cuh"  // fold_contract
 
 #ifndef P2S_LARGE_MOM_THREADS
@@ -51,8 +52,18 @@ struct LShape {
     return m;
   }
   static constexpr int NCH = (KMAX(0) + KC - 1) / KC;   // k1 chunks of the moment kernel
-  static constexpr int NQV = NV * (NV + 1) / 2, NQW = NW * (NW + 1) / 2;
+  // symmetric v kinds (PP / DD, either basis): X holds the n1 <= n2 triangle, else
+  // the full N_v x N_v square
+  static constexpr bool v_symmetric() {
+    for (int s = 0; s < S; ++s)
+      if (base_kind(kind(s, 1)) != PP && base_kind(kind(s, 1)) != DD) return false;
+    return true;
+  }
+  static constexpr bool VSYM = v_symmetric();
+  static constexpr int NQV = VSYM ? NV * (NV + 1) / 2 : NV * NV, NQW = NW * (NW + 1) / 2;
   static constexpr int tri(int a, int b, int n) { return a * n - a * (a - 1) / 2 + (b - a); }
+  // slot of (n1, n2) in X
+  static constexpr int vidx(int a, int b) { return VSYM ? (a <= b ? tri(a, b, NV) : tri(b, a, NV)) : a * NV + b; }
   static constexpr int moff(int s) {
     int o = 0;
     for (int i = 0; i < s; ++i) o += K(i, 0) * K(i, 1) * K(i, 2);
@@ -68,8 +79,9 @@ struct LShape {
   }
   static constexpr int64_t XPU = xoff(S);
   // Z block of one unit (w-contracted moments): terms back to back,
-  // [K_u][N_w][N_w][K2P], k2 fastest and padded to 32 (one lane per k2)
-  static constexpr int K2P = 32;
+  // [K_u][N_w][N_w][K2P], k2 fastest and padded to 32 (one lane per k2; 64 above
+  // 32 kernel polynomials along v, two k2 per lane)
+  static constexpr int K2P = KMAX(1) <= 32 ? 32 : 64;
   static constexpr int64_t zoff(int s) {
     int64_t o = 0;
     for (int i = 0; i < s; ++i) o += static_cast<int64_t>(K(i, 0)) * NW * NW * K2P;
@@ -118,6 +130,12 @@ struct LShape {
     return o;
   }
   static constexpr int ctot(int d) { return coff(d, S, 0, 0) > 0 ? coff(d, S, 0, 0) : 1; }
+  // band-packed coefficients travel as kernel parameters (constant bank, LDCU with
+  // immediate offsets) unless a direction's table exceeds what fits the 32 KB
+  // parameter space; then kernels read them from global memory (uniform __ldg)
+  static constexpr int kParamBytes = 30 * 1024;
+  static constexpr bool GC(int d) { return ctot(d) * 8 > kParamBytes; }
+  static constexpr int cpar(int d) { return GC(d) ? 1 : ctot(d); }
   // shared half tables [KMAX(d)][H(d)] per direction
   static constexpr int ttoff(int d) {
     int o = 0;
@@ -129,13 +147,7 @@ struct LShape {
   static constexpr size_t MOM_SMEM =
       sizeof(double) * (size_t)(KC * Q(2) * S2 + KC * KMAX(1) * S3);
   static_assert(KC % 2 == 0, "k1 chunks must be even (parity of k1 = parity of the slot)");
-  static constexpr bool sym_ok() {
-    for (int s = 0; s < S; ++s)
-      for (int d = 1; d < 3; ++d)
-        if (base_kind(kind(s, d)) != PP && base_kind(kind(s, d)) != DD) return false;
-    return true;
-  }
-  static_assert(sym_ok(), "large path needs symmetric v/w kinds (PP / DD)");
+  static_assert(KMAX(1) <= 64, "w step: at most 64 kernel polynomials along v");
   // symmetric u-kinds: the u stage forms m2 >= m1 and stores (m1, m2) and (m2, m1)
   // (as Shape::USYM); -DP2S_LARGE_NOUSYM turns it off for A/B measurements
   static constexpr bool u_symmetric() {
@@ -179,6 +191,7 @@ __device__ __forceinline__ void large_moments_term(const LMomParams<Ls>& p, cons
     cg::cluster_group cl = cg::this_cluster();
     constexpr int NCH = Ls::NCH, H = (QU + 1) / 2, Hf = QU / 2;
     constexpr int RPC = (QW * QV + NCH - 1) / NCH;  // alpha rows per CTA
+    static_assert(QU % 2 == 0, "cluster moments expect an even rule along u");
     double* peer[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) peer[c] = cl.map_shared_rank(T1, c);
@@ -213,19 +226,20 @@ __device__ __forceinline__ void large_moments_term(const LMomParams<Ls>& p, cons
     constexpr int Hf = QU / 2, H = (QU + 1) / 2;
     const int q3 = r / QV, q2 = r - (r / QV) * QV;
     double x[QU];
-    static_assert(QU % 2 == 0, "large path expects an even rule along u");
     load_row<QU>(a + static_cast<int64_t>(r) * QU, x);
-    double ev[Hf], od[Hf];
+    double ev[Hf > 0 ? Hf : 1], od[Hf > 0 ? Hf : 1];
 #pragma unroll
     for (int h = 0; h < Hf; ++h) {
       ev[h] = x[h] + x[QU - 1 - h];
       od[h] = x[h] - x[QU - 1 - h];
     }
 #pragma unroll
-    for (int j = 0; j < KC; ++j) {
+    for (int j = 0; j < KC; ++j) {  // k1 = k0 + j, k0 even: parity of j = parity of k1
       double v = 0.0;
 #pragma unroll
       for (int h = 0; h < Hf; ++h) v = fma(tu[j * H + h], (j & 1) ? od[h] : ev[h], v);
+      if constexpr (QU & 1)  // centre node (odd rule): even k only
+        if ((j & 1) == 0) v = fma(tu[j * H + Hf], x[Hf], v);
       T1[(j * QW + q3) * S2 + q2] = v;
     }
   });
@@ -285,17 +299,29 @@ template <class Ls>
 struct LWParams {
   const double* I;      // [units][MPP]
   double* Z;            // [units][ZPU]
+  const double* cg;     // device copy of cw (GC(2): read from global memory)
   int64_t n_units;
-  double cw[Ls::ctot(2)];
+  double cw[Ls::cpar(2)];
 };
 
 template <class Ls>
 struct LVParams {
   const double* Z;
   double* X;            // [units][XPU]
+  const double* cg;     // device copy of cv (GC(1))
   int64_t n_units;
-  double cv[Ls::ctot(1)];
+  double cv[Ls::cpar(1)];
 };
+
+// coefficient i of direction D: constant-bank kernel parameter, or global memory
+// when the direction's table exceeds the parameter space
+template <class Ls, int D>
+__device__ __forceinline__ double lcoef(const double* par, const double* __restrict__ glob, int i) {
+  if constexpr (Ls::GC(D))
+    return __ldg(glob + i);
+  else
+    return par[i];
+}
 
 template <class Ls, int s>
 __device__ __forceinline__ void large_w_row(const LWParams<Ls>& p, const double* cw, int64_t unit, int k1,
@@ -303,12 +329,13 @@ __device__ __forceinline__ void large_w_row(const LWParams<Ls>& p, const double*
   constexpr int NW = Ls::NW, K2P = Ls::K2P;
   constexpr int KV = Ls::K(s, 1), KW = Ls::K(s, 2), kw = Ls::kind(s, 2);
   static_assert(KV <= K2P, "w step maps k2 to lanes");
-  if (lane >= KV) return;
-  const double* src = p.I + unit * Ls::MPP + Ls::moff(s) + (k1 * KV + lane) * KW;
+#pragma unroll 1
+  for (int k2 = lane; k2 < KV; k2 += 32) {
+  const double* src = p.I + unit * Ls::MPP + Ls::moff(s) + (k1 * KV + k2) * KW;
   double y[KW];
 #pragma unroll
   for (int k3 = 0; k3 < KW; ++k3) y[k3] = src[k3];
-  double* Zk = p.Z + unit * Ls::ZPU + Ls::zoff(s) + static_cast<int64_t>(k1) * NW * NW * K2P + lane;
+  double* Zk = p.Z + unit * Ls::ZPU + Ls::zoff(s) + static_cast<int64_t>(k1) * NW * NW * K2P + k2;
   auto prow = [&](auto p1c) {
     constexpr int a = decltype(p1c)::value;
     static_for<0, NW>([&](auto p2c) {
@@ -318,7 +345,7 @@ __device__ __forceinline__ void large_w_row(const LWParams<Ls>& p, const double*
       double v = 0.0;
       static_for<0, cnt>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
-        v = fma(cw[co + j], y[lo + band_step(kw, a, b) * j], v);
+        v = fma(lcoef<Ls, 2>(cw, p.cg, co + j), y[lo + band_step(kw, a, b) * j], v);
       });
       Zk[(a * NW + b) * K2P] = v;
     });
@@ -331,6 +358,7 @@ __device__ __forceinline__ void large_w_row(const LWParams<Ls>& p, const double*
       if constexpr (NW - 1 - gg != gg) prow(std::integral_constant<int, NW - 1 - gg>{});
     }
   });
+  }
 }
 
 // w step: CTA = 8 warps on 8 consecutive (unit, row) items, all in the same p1
@@ -375,16 +403,16 @@ __global__ void __launch_bounds__(Ls::NW * Ls::NW) large_v_kernel(const __grid_c
     double* Xk = p.X + unit * Ls::XPU + Ls::xoff(s) + static_cast<int64_t>(k1) * NQV * NW * NW + t;
     static_for<0, NV>([&](auto n1c) {
       constexpr int a = decltype(n1c)::value;
-      static_for<a, NV>([&](auto n2c) {
+      static_for<(Ls::VSYM ? a : 0), NV>([&](auto n2c) {
         constexpr int c = decltype(n2c)::value;
         constexpr int lo = band_lo(kv, a, c), cnt = band_count(kv, a, c);
         constexpr int co = Ls::coff(1, s, a, c);
         double v = 0.0;
         static_for<0, cnt>([&](auto jc) {
           constexpr int j = decltype(jc)::value;
-          v = fma(p.cv[co + j], z[lo + band_step(kv, a, c) * j], v);
+          v = fma(lcoef<Ls, 1>(p.cv, p.cg, co + j), z[lo + band_step(kv, a, c) * j], v);
         });
-        Xk[Ls::tri(a, c, NV) * NW * NW] = v;
+        Xk[Ls::vidx(a, c) * NW * NW] = v;
       });
     });
   });
@@ -400,7 +428,7 @@ struct LUParams {
   int xs;               // XS mode: x classes staged in shared memory by the TMA engine
   int64_t ldM, mat_stride, n_units;
   int nc, P, Nt;
-  double cu[Ls::ctot(0)];
+  double cu[Ls::cpar(0)];
 };
 
 // PS: the (m1, m2) classes of even and odd m1+m2 run one after the other, each
@@ -424,7 +452,7 @@ __device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, const double
 #pragma unroll
   for (int f = 0; f < FIB; ++f) {
     const int n2 = n2b + f * (NV / FIB);
-    const int qv = n1 <= n2 ? Ls::tri(n1, n2, NV) : Ls::tri(n2, n1, NV);
+    const int qv = Ls::vidx(n1, n2);
     Xu[f] = p.X + (unit - unit0) * Ls::XPU + (static_cast<int64_t>(qv) * NW + p1) * NW + p2;
   }
   double* out = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt + n1 * NW + p1) * p.ldM +
@@ -467,7 +495,7 @@ __device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, const double
               constexpr int j = decltype(jc)::value;
               constexpr int xi = PAR < 0 ? Ls::kuoff(s) + lo + band_step(ku, m1, m2) * j
                                          : Ls::kpo(s, PAR) + (lo - Ls::uk0(s, PAR)) / 2 + j;
-              const double c = SMEMC ? cus[co + j] : p.cu[co + j];
+              const double c = SMEMC ? cus[co + j] : lcoef<Ls, 0>(p.cu, p.cu_g, co + j);
 #pragma unroll
               for (int f = 0; f < FIB; ++f) v[f] = fma(c, x[f][xi], v[f]);
             });
@@ -544,7 +572,7 @@ __device__ __forceinline__ void large_u_xs_issue(const LUParams<Ls>& p, int64_t 
   const int64_t unit = unit0 + b / (NV * NW);
   const int n1 = np / NW, p1 = np - (np / NW) * NW;
   const int n2 = tid / NW, p2 = tid - (tid / NW) * NW;
-  const int qv = n1 <= n2 ? Ls::tri(n1, n2, NV) : Ls::tri(n2, n1, NV);
+  const int qv = Ls::vidx(n1, n2);
   const double* Xu = p.X + (unit - unit0) * Ls::XPU + (static_cast<int64_t>(qv) * NW + p1) * NW + p2;
   auto go = [&](auto parc) {
     constexpr int PAR = decltype(parc)::value;
@@ -616,7 +644,7 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, 2)
               static_for<0, cnt>([&](auto jc) {
                 constexpr int j = decltype(jc)::value;
                 constexpr int xi = Ls::kpo(s, PAR) + (lo - Ls::uk0(s, PAR)) / 2 + j;
-                v = fma(p.cu[co + j], x[xi], v);
+                v = fma(lcoef<Ls, 0>(p.cu, p.cu_g, co + j), x[xi], v);
               });
             });
             st_cs(out + m1 * rowstep + m2 * (NV * NW), v);
@@ -636,7 +664,7 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, 2)
 }
 
 template <class Ls>
-void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps, int fib, int64_t max_ctas,
+cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps, int fib, int64_t max_ctas,
                       bool smemc, cudaStream_t st) {
   const int64_t ntiles = cnt * Ls::NV * Ls::NW;
   const unsigned grid = static_cast<unsigned>(max_ctas > 0 && max_ctas < ntiles ? max_ctas : ntiles);
@@ -644,25 +672,39 @@ void large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps
   constexpr int F2 = Ls::NV % 2 == 0 ? 2 : 1;
   constexpr size_t cs = sizeof(double) * Ls::ctot(0);
   if constexpr (!Ls::u_conforming() && Ls::NW % 2 == 0) {
+#ifdef P2S_LEAN
+    if (true) {
+#else
     if (ps && fib == 1 && p.xs) {
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(large_u_xs_kernel<Ls>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)LUXs<Ls>::SMEM);
-        attr = true;
-      }
+#endif
+      cudaError_t e = kernel_prepare(large_u_xs_kernel<Ls>, LUXs<Ls>::SMEM, T);
+      if (e != cudaSuccess) return e;
       large_u_xs_kernel<Ls><<<grid, T, LUXs<Ls>::SMEM, st>>>(p, unit0, ntiles);
-      return;
+      return cudaGetLastError();
     }
   }
-  if (ps && smemc && p.cu_g)
+#ifdef P2S_LEAN  // generated modules: the default u stage only (no measurement variants)
+  (void)smemc;
+  (void)fib;
+  (void)cs;
+  (void)F2;
+  (void)ps;
+  if constexpr (Ls::u_conforming() || Ls::NW % 2 != 0)
+    large_u_kernel<Ls, true, 1><<<grid, T, 0, st>>>(p, unit0, ntiles);
+#else
+  if (ps && smemc && p.cu_g) {
+    cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1, true>, cs, T);
+    if (e != cudaSuccess) return e;
     large_u_kernel<Ls, true, 1, true><<<grid, T, cs, st>>>(p, unit0, ntiles);
+  }
   else if (ps && fib == 2)
     large_u_kernel<Ls, true, F2><<<grid, T / F2, 0, st>>>(p, unit0, ntiles);
   else if (ps)
     large_u_kernel<Ls, true, 1><<<grid, T, 0, st>>>(p, unit0, ntiles);
   else
     large_u_kernel<Ls, false, 1><<<grid, T, 0, st>>>(p, unit0, ntiles);
+#endif
+  return cudaGetLastError();
 }
 
 }  // namespace p2s

@@ -189,18 +189,27 @@ __device__ __forceinline__ void moments_unit(const double* __restrict__ a, const
   });
   __syncthreads();
   // pass w: the thread's KW outputs are one contiguous run of I; they go to shared
-  // memory first (T1 is free after pass v) and leave in one coalesced sweep
-  static_assert(KU * KV * KW <= KU * QW * S2, "I tile must fit the T1 scratch");
+  // memory first (T1 is free after pass v) and leave in one coalesced sweep --
+  // unless the I tile is larger than T1 (fewer quadrature points than kernel
+  // polynomials along w), then straight to Iout
+  constexpr bool kStage = KU * KV * KW <= KU * QW * S2;
   for_items<KU * KV, NTHR>([&](int r) {
     const double* src = T2 + r * S3;
     double x[QW];
 #pragma unroll
     for (int q = 0; q < QW; ++q) x[q] = src[q];
-    fold_contract<QW, KW>(x, tw, [&](int k, double v) { T1[r * KW + k] = v; });
+    fold_contract<QW, KW>(x, tw, [&](int k, double v) {
+      if constexpr (kStage)
+        T1[r * KW + k] = v;
+      else
+        Iout[r * KW + k] = v;
+    });
   });
   __syncthreads();
-  for (int i = threadIdx.x; i < KU * KV * KW; i += NTHR) Iout[i] = T1[i];
-  __syncthreads();
+  if constexpr (kStage) {
+    for (int i = threadIdx.x; i < KU * KV * KW; i += NTHR) Iout[i] = T1[i];
+    __syncthreads();
+  }
 }
 
 // Element geometry for coupling factors computed in place of loaded alpha
@@ -210,10 +219,12 @@ struct GeoUnit {
   double A[8][3];
   double mat[4];
   int gi, gj;
+  int* bad;  // set when a Jacobian determinant is <= 0 (GeometryError, assembly.cpp:95-99)
 };
 
 // Per CTA: record (include/p2s_b200.h layout) -> GeoUnit in shared memory.
-__device__ __forceinline__ void geo_unit_setup(const double* __restrict__ rec, int gi, int gj, GeoUnit* g) {
+__device__ __forceinline__ void geo_unit_setup(const double* __restrict__ rec, int gi, int gj, GeoUnit* g,
+                                               int* bad) {
   if (threadIdx.x < 24) {
     const int m = threadIdx.x / 3, comp = threadIdx.x % 3;
     double acc = 0.0;
@@ -229,6 +240,7 @@ __device__ __forceinline__ void geo_unit_setup(const double* __restrict__ rec, i
   } else if (threadIdx.x == 28) {
     g->gi = gi;
     g->gj = gj;
+    g->bad = bad;
   }
 }
 
@@ -263,6 +275,7 @@ __device__ __forceinline__ void geo_row(const GeoUnit& g, double v, double w, co
     const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
                        J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
                        J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    if (!(det > 0.0)) atomicOr(g.bad, 1);
     const double G00 = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
     const double G11 = J[0][1] * J[0][1] + J[1][1] * J[1][1] + J[2][1] * J[2][1];
     const double G22 = J[0][2] * J[0][2] + J[1][2] * J[1][2] + J[2][2] * J[2][2];

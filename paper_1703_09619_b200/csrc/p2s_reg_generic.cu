@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "p2s_kernels.cuh"
+#include "p2s_launch.cuh"
 #include "p2s_registry.hpp"
 
 namespace p2s {
@@ -55,13 +56,8 @@ cudaError_t launch_contract(const ContractArgs& a, const Plan& pl, cudaStream_t 
   const int64_t n_cta = a.n_elem * a.P * pl.NG;
   p.n_cta = n_cta;
   if (n_cta == 0) return cudaSuccess;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(contract_kernel<Cfg>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = kernel_prepare(contract_kernel<Cfg>, 227 * 1024, 256);
+  if (e != cudaSuccess) return e;
   contract_kernel<Cfg><<<static_cast<unsigned>(n_cta), pl.threads, pl.smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -124,13 +120,8 @@ const std::vector<RegEntry>& registry() {
 
 template <int KMAX>
 cudaError_t launch_moments_k(const MomentParams& p, size_t smem, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(moments_kernel<KMAX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = kernel_prepare(moments_kernel<KMAX>, 227 * 1024, 256);
+  if (e != cudaSuccess) return e;
   moments_kernel<KMAX><<<static_cast<unsigned>(p.n_units), 256, smem, st>>>(p);
   return cudaGetLastError();
 }

@@ -6,71 +6,12 @@
 #include <cstring>
 #include <vector>
 
-#include "p2s_reg_common.cuh"
+#include "p2s_reg_v2.cuh"
 
 namespace p2s {
 namespace reg {
 
 // ------------------------------------------------------------ shape-specialised registry
-
-
-template <class Sh>
-cudaError_t launch_v2(const V2Args& a, const std::vector<double>& packed, cudaStream_t st,
-                      int num_sms) {
-  V2Params<Sh> p;
-  p.I = a.I;
-  p.M = a.M;
-  p.ldM = a.ldM;
-  p.mat_stride = a.n_tot * a.ldM;
-  p.n_units = a.n_elem * a.P;
-  p.nc = a.nc;
-  p.P = a.P;
-  p.Nt = a.Nt;
-  p.mom_per_elem = a.mom_per_elem;
-  p.amma = a.amma;
-  p.vec2 = vec2_ok(a.M, a.ldM);
-  std::memcpy(p.cu, packed.data(), sizeof(double) * Sh::ctot(0));
-  std::memcpy(p.cv, packed.data() + Sh::ctot(0), sizeof(double) * Sh::ctot(1));
-  std::memcpy(p.cw, packed.data() + Sh::ctot(0) + Sh::ctot(1), sizeof(double) * Sh::ctot(2));
-  if (p.n_units == 0) return cudaSuccess;
-  static int blocks_per_sm = -1;  // per instantiation (kernel attributes are process-wide)
-  if (blocks_per_sm < 0) {
-    cudaError_t e = cudaFuncSetAttribute(contract_v2_kernel<Sh>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)v2_smem<Sh>());
-    if (e != cudaSuccess) return e;
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, contract_v2_kernel<Sh>, Sh::THREADS,
-                                                      v2_smem<Sh>());
-    if (e != cudaSuccess) return e;
-    if (b < 1) return cudaErrorInvalidConfiguration;
-    blocks_per_sm = b;
-  }
-  const int64_t grid = Sh::PERSIST
-                           ? std::min<int64_t>(p.n_units, static_cast<int64_t>(blocks_per_sm) * num_sms)
-                           : p.n_units;
-  p.prefetch_stride = static_cast<int64_t>(blocks_per_sm) * num_sms;
-  if (const char* v = std::getenv("P2S_V2_NOPREFETCH"))
-    if (v[0] == '1') p.prefetch_stride = 0;
-  contract_v2_kernel<Sh><<<static_cast<unsigned>(grid), Sh::THREADS, v2_smem<Sh>(), st>>>(p);
-  return cudaGetLastError();
-}
-
-
-template <class Sh>
-V2Entry make_v2() {
-  V2Entry r{};
-  for (int d = 0; d < 3; ++d) r.order[d] = Sh::N(d);
-  r.S = Sh::S;
-  for (int s = 0; s < Sh::S; ++s)
-    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Sh::kind(s, d);
-  r.launch = &launch_v2<Sh>;
-  r.pack = &pack_v2<Sh>;
-  r.mma_pack = &pack_mma<Sh>;
-  r.smem = v2_smem<Sh>();
-  r.desc = stage_c_desc<Sh>();
-  return r;
-}
 
 
 // <N_u, N_v, N_w, n1 tile, p1 tile, threads, min CTAs/SM, A once per unit, fibers per
@@ -111,44 +52,6 @@ const std::vector<V2Entry>& v2_registry() {
 
 // ------------------------------------------------------------ shape-specialised moments
 
-
-template <class Ms>
-cudaError_t launch_mv2(const double* alpha, double* I, int64_t n_elem, int P, int64_t mom_per_elem,
-                       const std::vector<double>& packed, cudaStream_t st) {
-  MV2Params<Ms> p;
-  p.alpha = alpha;
-  p.I = I;
-  p.P = P;
-  p.n_units = n_elem * P * Ms::S;
-  p.mom_per_elem = mom_per_elem;
-  std::memcpy(p.tab, packed.data(), sizeof(double) * Ms::TALL);
-  if (p.n_units == 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(moments_v2_kernel<Ms>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ms::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  moments_v2_kernel<Ms><<<static_cast<unsigned>(p.n_units), Ms::THREADS, Ms::SMEM, st>>>(p);
-  return cudaGetLastError();
-}
-
-
-template <class Ms>
-MV2Entry make_mv2() {
-  MV2Entry r{};
-  for (int d = 0; d < 3; ++d) {
-    r.order[d] = Ms::N(d);
-    r.nq[d] = Ms::Q(d);
-  }
-  r.S = Ms::S;
-  for (int s = 0; s < Ms::S; ++s)
-    for (int d = 0; d < 3; ++d) r.kinds[s][d] = Ms::kind(s, d);
-  r.launch = &launch_mv2<Ms>;
-  r.pack = &pack_mv2<Ms>;
-  return r;
-}
 
 // <N_u, N_v, N_w, nq_u, nq_v, nq_w, threads, term kinds...>
 const std::vector<MV2Entry>& mv2_registry() {

@@ -79,9 +79,11 @@ struct MV2Entry {
   mv2_pack_fn pack;
 };
 
+// (alpha or geometry records, M, ld_M, n_tot, n_elem, n_comp, P, Nt, band-packed
+//  coefficients, weighted tables, DMMA operands, stream, SM count, Jacobian flag)
 using fused_fn = cudaError_t (*)(const double*, double*, int64_t, int64_t, int64_t, int, int, int,
                                  const std::vector<double>&, const std::vector<double>&,
-                                 const double*, cudaStream_t, int);
+                                 const double*, cudaStream_t, int, int*);
 
 struct FusedEntry {
   int order[3], nq[3], S;
@@ -106,7 +108,8 @@ struct LargeArgs {
 struct LargePack {
   std::vector<double> tab, cu, cvw;  // cvw: band-packed Cv then Cw (kernel parameters)
   double* d_Z = nullptr;             // w-step output of one chunk (ZPU x xchunk doubles)
-  double* d_cu = nullptr;            // device copy of cu (u stage with shared-memory coefficients)
+  double* d_cu = nullptr;            // device copy of cu (shared-memory / global-memory coefficients)
+  double* d_cvw = nullptr;           // device copy of cvw (global-memory coefficients)
   bool u_xs = true;                  // P2S_LARGE_XS: next class staged by cp.async (C5 29.4 k vs 28.4 k)
   bool mom_cluster = false;          // P2S_LARGE_MOMCL: one cluster per (unit, term), alpha read once (0.77 vs 0.71 ms: slower)
   bool u_smemc = false;              // P2S_LARGE_USMEM (measured 28.1 k vs 28.4 k elem/s constant-bank)
@@ -135,6 +138,19 @@ struct LargeEntry {
   large_mom_fn moments;
   large_con_fn contract;
   int64_t mpp, xpu, zpu;
+};
+
+// Registry entries of one generated per-shape module (p2s_jit.cu,
+// p2s_jit_module.cuh); kJitAbi changes whenever these structs change.
+constexpr int kJitAbi = 3;
+struct JitEntries {
+  int abi, family;   // family: 1 fused (+ two-stage entries of the shape), 2 large
+  FusedEntry fused;
+  V2Entry v2;
+  MV2Entry mv2;
+  LargeEntry large;
+  size_t smem;       // shared memory of the dominant kernel as compiled (bytes)
+  int64_t mpp;       // moment block of one pair as compiled (doubles)
 };
 
 // accessors (one translation unit each)

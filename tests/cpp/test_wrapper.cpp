@@ -11,6 +11,8 @@
 #include <stdexcept>
 #include <vector>
 
+#include <cuda_runtime_api.h>
+
 #include "p2s_b200.hpp"
 
 #define REQUIRE(c)                                                   \
@@ -57,6 +59,30 @@ int main() {
     threw = true;
   }
   REQUIRE(threw);
+
+  // counters (assembly.cpp:291-310, 665-666): 7^3 moments of the single PP term
+  REQUIRE(kt.n_integrals == 343 * n && kt.n_mass_uu_integrals == 343 * n);
+  REQUIRE(f.n_integrals == kt.n_integrals && em.n_mass_uu_integrals == kt.n_mass_uu_integrals);
+  // nq <= 0: the reference's default_quad_points (4 + 1 + 6 = 11 per direction)
+  p2s::Problem dq = pb;
+  dq.nq = {0, 0, 0};
+  REQUIRE(dq.c().nq[0] == 11 && dq.c().nq[2] == 11);
+  p2s::Context ctx3(dq, 0);
+  REQUIRE(ctx3.alpha_per_elem() == 11 * 11 * 11);
+
+  // every device of the box (the reference's thread pool, assembly.cpp:676-698):
+  // the result is independent of the device count
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 1) {
+    std::vector<double> a2(static_cast<size_t>(37 * ctx.alpha_per_elem()));
+    for (size_t i = 0; i < a2.size(); ++i) a2[i] = 1.0 + 0.25 * std::sin(0.001 * static_cast<double>(i));
+    p2s::ElementMatrices one = p2s::fill_elements(pb, a2, 1);
+    p2s::ElementMatrices all = p2s::fill_elements(pb, a2, ndev);
+    REQUIRE(one.M == all.M);
+    std::printf("fill_elements on %d devices == 1 device\n", ndev);
+  } else {
+    std::printf("fill_elements multi-device check skipped (%d device)\n", ndev);
+  }
   std::printf("cxx wrapper ok (max |M - mass| = %.3g, path: %s)\n", worst, ctx.kernel_path().c_str());
   return 0;
 }

@@ -41,7 +41,7 @@ def test_version_and_shape_registry():
     assert b"sm_100a" in capi.lib().p2s_version()
     assert capi.shape_supported(3, (6, 6, 6), [capi.PP, capi.DD], (14, 14, 14))
     assert capi.shape_supported(1, (8, 8, 8), [capi.PP, capi.DD], (20, 20, 20))
-    assert not capi.shape_supported(1, (7, 3, 3), [capi.DP], (5, 5, 5))
+    assert capi.shape_supported(1, (7, 3, 3), [capi.DP], (5, 5, 5))        # generated module
     assert not capi.shape_supported(4, (3, 3, 3), [capi.PP], (5, 5, 5))   # n_comp > 3
 
 
@@ -76,6 +76,56 @@ def test_cxx_wrapper_header_compiles():
         exe = os.path.join(d, "t")
         r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), src,
                             "-o", exe, os.path.join(ROOT, "paper_1703_09619_b200", "libp2s_b200.so"),
-                            f"-Wl,-rpath,{os.path.join(ROOT, 'paper_1703_09619_b200')}"],
+                            f"-Wl,-rpath,{os.path.join(ROOT, 'paper_1703_09619_b200')}",
+                            "-I/usr/local/cuda/include", "-L/usr/local/cuda/lib64", "-lcudart"],
                            capture_output=True, text=True)
         assert r.returncode == 0, r.stderr
+
+
+def test_every_grid_shape_is_supported():
+    """p2s_shape_supported over the drop-in grid: isotropic N = 1..18 with every
+    single kind and both bases, every two-kind mix at three orders, and the
+    seeded coverage grid (no device needed: plans only, compiler present)."""
+    from paper_1703_09619_b200 import shape_grid
+    PP, DD, DP, PD = capi.PP, capi.DD, capi.DP, capi.PD
+    cases = []
+    for n in range(1, 19):
+        for k in (PP, DD, DP, PD):
+            for basis in (0, 1) if n >= 2 else (0,):
+                cases.append((1, (n, n, n), [k], (n + 7,) * 3, basis))
+    for n in (3, 11, 18):
+        for k1 in (PP, DD, DP, PD):
+            for k2 in (PP, DD, DP, PD):
+                cases.append((3, (n, max(1, n - 2), 2), [(k1, k2, k1), (k2, k1, PP)], (n + 3, n, 4), 0))
+    cases += [(1, (18, 18, 18), [PP, DD, DP, PD], (64, 64, 64), 1), (1, (1, 1, 1), [DD], (1, 1, 1), 0)]
+    cases += shape_grid.ALL
+    missing = [c for c in cases if not capi.shape_supported_basis(*c)]
+    assert not missing, missing[:5]
+
+
+def test_cxx_host_logic_without_gpu():
+    """Partition, first-exception rethrow, sizes and nq default of the C++ API
+    (tests/cpp/test_wrapper_cpu.cpp), run here without a GPU."""
+    import shutil
+    import subprocess
+    import tempfile
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present: the rethrow check expects no device")
+    except Exception:
+        pass
+    libdir = os.path.join(ROOT, "paper_1703_09619_b200")
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "t")
+        r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                            os.path.join(ROOT, "tests", "cpp", "test_wrapper_cpu.cpp"), "-o", exe,
+                            os.path.join(libdir, "libp2s_b200.so"), f"-Wl,-rpath,{libdir}", "-lpthread",
+                            "-L/usr/local/cuda/lib64", "-lcudart"],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "cxx host logic ok" in r.stdout

@@ -27,7 +27,11 @@ def _fill(ctx, alpha):
 
 CASES = [
     # n_comp, order, kinds, nq, env, expected path prefix
-    (1, (4, 4, 4), [PP], (8, 8, 8), {}, "two-stage"),
+    (1, (4, 4, 4), [PP], (8, 8, 8), {}, "fused"),                        # generated module
+    (1, (4, 4, 4), [PP], (8, 8, 8), {"P2S_FORCE_GENERIC": "1"}, "two-stage"),
+    (1, (4, 4, 4), [PP], (8, 8, 8), {"P2S_NO_FUSED": "1"}, "two-stage: moments_v2_kernel + contract_v2"),
+    (1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7), {"P2S_FORCE_JIT": "1"}, "fused"),
+    (1, (7, 6, 5), [(DP, PD, PP), (PD, DP, DD)], (9, 8, 7), {}, "large-order"),  # generated large
     (3, (3, 3, 3), [PP, DD], (6, 6, 6), {}, "two-stage: moments_v2_kernel + contract_v2"),
     (3, (3, 3, 3), [PP, DD], (6, 6, 6), {"P2S_FORCE_GENERIC": "1"}, "two-stage"),
     (1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7), {}, "two-stage"),
@@ -41,7 +45,7 @@ CASES = [
 def test_conforming_fill_matches_oracle(case, monkeypatch):
     n_comp, order, kinds, nq, env, path = case
     for k, v in env.items():
-        monkeypatch.setenv(k, v)
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, k, v)
     if n_comp == "c2":
         cfg = CONFIGS["c2"]
         n_comp, order, kinds, nq = cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq

@@ -50,7 +50,7 @@ def test_empty_batches_touch_nothing():
 @pytest.mark.parametrize("n", [1, 7, 33])
 def test_ragged_batches_match_oracle(n, path_env, monkeypatch):
     for k, v in path_env.items():
-        monkeypatch.setenv(k, v)
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, k, v)
     pb = (3, (3, 3, 3), [PP, DD], (6, 6, 6))
     ctx = capi.Context(*pb)
     o = oracle_for(*pb)
@@ -91,7 +91,7 @@ def test_grid_beyond_65535_ctas(env, monkeypatch):
     """70 000 C1 elements: one CTA per (element, pair) unit in the fused kernel,
     70 000 moment CTAs in the two-stage path."""
     for k, v in env.items():
-        monkeypatch.setenv(k, v)
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, k, v)
     cfg = CONFIGS["c1"]
     ctx = capi.Context(**cfg.problem())
     n = 70000
@@ -124,11 +124,16 @@ def test_argument_limits(bad):
         capi.DirectContext(args["n_comp"], args["order"], args["kinds"], args["nq"], basis=args["basis"])
 
 
-def test_unsupported_orders_report_unsupported_shape():
-    # valid problem, no compiled contraction for N_u = 11 with these u-kinds
-    assert not capi.shape_supported(1, (11, 3, 3), [PP], (12, 4, 4))
+def test_unregistered_orders_need_a_generated_module():
+    # valid problem with no ahead-of-time kernel for N_u = 11: accepted through a
+    # generated module; with generated modules switched off it is unsupported
+    assert capi.shape_supported(1, (11, 3, 3), [PP], (12, 4, 4))
+    ctx = capi.Context(1, (11, 3, 3), [PP], (12, 4, 4))
+    assert "generated module" in ctx.kernel_path, ctx.kernel_path
     with pytest.raises(capi.UnsupportedShape):
-        capi.Context(1, (11, 3, 3), [PP], (12, 4, 4))
+        capi.Context(1, (11, 3, 3), [PP], (12, 4, 4), options={"P2S_JIT": "0"})
+    with pytest.raises(capi.InvalidArgument):
+        capi.Context(1, (4, 4, 4), [PP], (8, 8, 8), options={"P2S_NO_SUCH_KNOB": "1"})
 
 
 GUARD = 8192  # doubles of canary on each side of the output matrices
@@ -140,7 +145,9 @@ GUARD = 8192  # doubles of canary on each side of the output matrices
     ((1, (8, 8, 8), [PP, DD], (20, 20, 20)), {}),                                   # C3 fused
     ((3, (10, 6, 4), [PP, DD], (16, 16, 16)), {}),                                  # C4 fused
     ((3, (5, 4, 3), [PP, DD], (8, 8, 6)), {"P2S_XCHUNK_MB": "1"}),                 # large path
-    ((1, (2, 3, 4), [PP], (5, 6, 7)), {}),                                          # generic kernels
+    ((1, (2, 3, 4), [PP], (5, 6, 7)), {"P2S_FORCE_GENERIC": "1"}),                 # generic kernels
+    ((1, (2, 3, 4), [PP], (5, 6, 7)), {}),                                          # generated fused
+    ((1, (9, 5, 4), [PP, DD], (11, 7, 6)), {"P2S_XCHUNK_MB": "1"}),                # generated large
 ])
 @pytest.mark.parametrize("odd_ld", [False, True])
 def test_writes_stay_inside_the_output(problem, env, odd_ld, monkeypatch):
@@ -148,7 +155,7 @@ def test_writes_stay_inside_the_output(problem, env, odd_ld, monkeypatch):
     untouched by every kernel path; compute-sanitizer is unavailable on the pool,
     so out-of-bounds stores are caught by value here."""
     for k, v in env.items():
-        monkeypatch.setenv(k, v)
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, k, v)
     ctx = capi.Context(*problem)
     n = 7
     ld = ctx.n_tot + (1 if odd_ld else 0)
@@ -177,7 +184,7 @@ def test_two_stage_chunk_pipeline_matches_oracle(env, monkeypatch):
     scratch, the next chunk's moments on a side stream) gives the oracle's
     matrices; C3 runs this path by default."""
     for k, v in env.items():
-        monkeypatch.setenv(k, v)
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, k, v)
     cfg = CONFIGS["c3"]
     ctx = capi.Context(**cfg.problem())
     assert ctx.kernel_path.startswith("two-stage"), ctx.kernel_path

@@ -49,7 +49,7 @@ def test_fill_geometry_matches_two_step_fill_and_oracle(mode, monkeypatch):
     p2s_fill(p2s_alpha_from_geometry(...)); 1: each pair's CTA recomputes the
     geometry; 2: one cluster of 9 CTAs per element shares the per-point geometry
     through DSMEM.  All against the oracle on host alpha."""
-    monkeypatch.setenv("P2S_GEO_MODE", str(mode))
+    monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_GEO_MODE", str(mode))
     chunked = mode == 0
     cfg, ctx = _ctx("c2")
     assert "fused" in ctx.kernel_path

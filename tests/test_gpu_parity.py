@@ -108,9 +108,9 @@ def test_moment_kernel_variants_match_oracle(name, variant, monkeypatch):
     # every registered moments_v2 thread-count variant (P2S_MV2_VARIANT) and the
     # large-order moment kernel (both modes) reproduce the oracle's moment integrals
     if variant == "cluster":
-        monkeypatch.setenv("P2S_LARGE_MOMCL", "1")
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_LARGE_MOMCL", "1")
     else:
-        monkeypatch.setenv("P2S_MV2_VARIANT", str(variant))
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_MV2_VARIANT", str(variant))
     cfg = CONFIGS[name]
     o = oracle_for(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
     ctx = capi.Context(**cfg.problem())
@@ -133,8 +133,8 @@ def test_moment_kernel_variants_match_oracle(name, variant, monkeypatch):
 def test_two_stage_contraction_variants_match_oracle(name, variant, monkeypatch):
     # every registered contract_v2 variant of the benchmark shapes (P2S_V2_VARIANT,
     # two-stage path) gives the oracle's matrices
-    monkeypatch.setenv("P2S_NO_FUSED", "1")
-    monkeypatch.setenv("P2S_V2_VARIANT", str(variant))
+    monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_NO_FUSED", "1")
+    monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_V2_VARIANT", str(variant))
     cfg = CONFIGS[name]
     ctx = capi.Context(**cfg.problem())
     assert ctx.kernel_path.startswith("two-stage"), ctx.kernel_path
@@ -146,7 +146,7 @@ def test_two_stage_contraction_variants_match_oracle(name, variant, monkeypatch)
 def test_every_fused_variant_matches_oracle(name, variant, monkeypatch):
     # every registered fill_fused_kernel variant of the benchmark shapes
     # (P2S_FUSED_VARIANT; indices past the last fall back to the first)
-    monkeypatch.setenv("P2S_FUSED_VARIANT", str(variant))
+    monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_FUSED_VARIANT", str(variant))
     cfg = CONFIGS[name]
     ctx = capi.Context(**cfg.problem())
     assert ctx.kernel_path.startswith("fused"), ctx.kernel_path
@@ -278,7 +278,7 @@ def test_large_order_path_chunk_schedules(env, monkeypatch):
     # the chunked v/w -> u pipeline over many X chunks (double buffer reuse,
     # alternating u streams) gives the oracle's matrices
     for k, v in env.items():
-        monkeypatch.setenv(k, v)
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, k, v)
     ctx = capi.Context(3, (5, 4, 3), [PP, DD], (8, 8, 6))
     assert ctx.kernel_path.startswith("large-order")
     _check_case(3, (5, 4, 3), [PP, DD], (8, 8, 6), O.ALPHA_JACOBIAN, 0.5, 3.0, n_elem=40)
@@ -291,7 +291,7 @@ def test_c5_u_stage_schedules_match_oracle(env, monkeypatch):
     # (default; across tiles of the persistent CTAs and across X chunks) and with
     # direct L2 loads
     for k, v in env.items():
-        monkeypatch.setenv(k, v)
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, k, v)
     cfg = CONFIGS["c5"]
     worst = _check_case(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq, cfg.alpha_kind,
                         cfg.alpha_lo, cfg.alpha_hi, n_elem=3, seed=7, threads=16)
@@ -312,7 +312,7 @@ def _select_variant(monkeypatch, problem, env_var, marker):
     """Set env_var (P2S_FUSED_VARIANT / P2S_V2_VARIANT) to the first registered
     variant of `problem` whose kernel_path contains `marker`."""
     for v in range(24):
-        monkeypatch.setenv(env_var, str(v))
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, env_var, str(v))
         ctx = capi.Context(*problem)
         if marker in ctx.kernel_path:
             return ctx
@@ -360,7 +360,7 @@ def test_stage_c_variants_match_oracle(case, two_stage, marker, n_elem, odd_ld, 
         n_comp, order, kinds, nq = case
         ak, lo, hi = O.ALPHA_SINE, 0.5, 3.0
     if two_stage:
-        monkeypatch.setenv("P2S_NO_FUSED", "1")
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_NO_FUSED", "1")
     ctx = _select_variant(monkeypatch, (n_comp, order, kinds, nq),
                           "P2S_V2_VARIANT" if two_stage else "P2S_FUSED_VARIANT", marker)
     o = oracle_for(n_comp, order, kinds, nq)
