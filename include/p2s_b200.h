@@ -38,9 +38,13 @@
  *
  * Ownership: the caller owns alpha / I / M buffers; the context owns the
  * uploaded tables and its scratch and is immutable after p2s_create (the
- * profiling switch aside).  One context per device; calls on distinct streams
- * may run concurrently except p2s_fill / p2s_fill_host, which use context
- * scratch and must not overlap on one context.
+ * profiling switch aside).  One context per device; any entry point may be
+ * called from several host threads and streams: calls that use context scratch
+ * (p2s_fill on the two-stage and large-order paths, p2s_contract on the
+ * large-order path, p2s_fill_host, the geometry entry points) are ordered on the
+ * device behind each other through a context event, the others run concurrently.
+ * Alignment: alpha 32-byte aligned when nq_u % 4 == 0 (32-B row loads), else
+ * 16-byte; I 16-byte; M 8-byte (wider stores are used where rows allow).
  *
  * There is no CPU fallback: every compute entry point runs sm_100a kernels
  * and fails with P2S_CUDA_ERROR when no B200 is present.
@@ -120,9 +124,10 @@ p2s_status p2s_create(const p2s_problem* spec, int device, p2s_ctx** out);
 p2s_status p2s_create_ex(const p2s_problem* spec, int device, const char* options, p2s_ctx** out);
 
 /* Plans the problem and builds (or finds) its generated module without touching
- * a device -- ahead-of-time warm-up of the module cache (build scripts, CI).
- * desc (may be NULL) receives the plan and the module path. */
-p2s_status p2s_shape_prepare(const p2s_problem* spec, char* desc, int desc_len);
+ * a device -- ahead-of-time warm-up of the module cache (build scripts, CI);
+ * options as for p2s_create_ex (planner overrides P2S_JIT_*).  desc (may be
+ * NULL) receives the plan and the module path. */
+p2s_status p2s_shape_prepare(const p2s_problem* spec, const char* options, char* desc, int desc_len);
 
 /* Directory of this library's generated modules (root/<kernel-header hash>). */
 const char* p2s_jit_cache_dir(void);

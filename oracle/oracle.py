@@ -83,6 +83,8 @@ def lib():
         L.por_moments.argtypes = [C.c_void_p, dp, C.c_int64, dp, C.c_int]
         for f in ("por_contract", "por_fill", "por_direct"):
             getattr(L, f).argtypes = [C.c_void_p, dp, C.c_int64, dp, C.c_int64, C.c_int]
+        L.por_direct_sample.argtypes = [C.c_void_p, dp, C.c_int, C.c_int, dp, C.c_int64, C.POINTER(C.c_long)]
+        L.por_direct_sample.restype = C.c_long
         L.por_block_close.argtypes = [dp, C.c_int64, dp, C.c_int64, C.c_int, C.c_int, C.c_double,
                                       ip, ip]
         L.por_block_close.restype = C.c_int
@@ -275,6 +277,18 @@ class Oracle:
         out = np.zeros((n, self.n_tot, self.n_tot))
         lib().por_direct(self.h, _dp(alpha), n, _dp(out), self.n_tot, threads)
         return out
+
+
+def direct_sample_seconds(orc, alpha_elem, m1_lo, m1_hi):
+    """Time one element's direct fill restricted to u-test indices m1 in
+    [m1_lo, m1_hi) (single thread); returns (seconds, covered pairs, all pairs)."""
+    import time
+    a = np.ascontiguousarray(alpha_elem, dtype=np.float64).reshape(-1)
+    M = np.zeros((orc.n_tot, orc.n_tot))
+    tot = C.c_long(0)
+    t0 = time.perf_counter()
+    cov = lib().por_direct_sample(orc.h, _dp(a), m1_lo, m1_hi, _dp(M), orc.n_tot, C.byref(tot))
+    return time.perf_counter() - t0, cov, tot.value
 
 
 def uniform(seed, elem, slot, j):

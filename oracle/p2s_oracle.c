@@ -292,14 +292,24 @@ void por_term_contract(const por_term* t, const double* I, double* M, long ldM, 
 /* assemble_direct_element (assembly.cpp:142-274): one full quadrature per
  * canonical entry (integrate_product :122-131 in 3-D), mirrored across the
  * unordered index pairs of symmetric directions (:165-180). */
+static void term_direct_rows(const por_term* t, const double* alpha, double* M, long ldM, int m1_lo,
+                             int m1_hi);
+
 void por_term_direct(const por_term* t, const double* alpha, double* M, long ldM) {
+  term_direct_rows(t, alpha, M, ldM, 0, t->d[0].nt);
+}
+
+/* the direct fill restricted to test indices m1 in [m1_lo, m1_hi) of the first
+ * direction (por_direct_sample: a timed sample of the C5 ablation) */
+static void term_direct_rows(const por_term* t, const double* alpha, double* M, long ldM, int m1_lo,
+                             int m1_hi) {
   const por_dir* d = t->d;
   const int n0 = d[0].nq, n1 = d[1].nq, n2 = d[2].nq;
   double* B0 = (double*)malloc(sizeof(double) * (size_t)n0);
   double* B1 = (double*)malloc(sizeof(double) * (size_t)n1);
   double* B2 = (double*)malloc(sizeof(double) * (size_t)n2);
   const int t1 = d[1].nt, r1 = d[1].nr, t2 = d[2].nt, r2 = d[2].nr;
-  for (int m1 = 0; m1 < d[0].nt; ++m1)
+  for (int m1 = m1_lo; m1 < m1_hi && m1 < d[0].nt; ++m1)
     for (int m2 = d[0].symmetric ? m1 : 0; m2 < d[0].nr; ++m2) {
       for (int q = 0; q < n0; ++q)
         B0[q] = d[0].btest[(long)m1 * n0 + q] * d[0].btrial[(long)m2 * n0 + q] *
@@ -730,6 +740,30 @@ void por_fill(const por_tables* t, const double* alpha, int64_t n, double* M, in
 void por_direct(const por_tables* t, const double* alpha, int64_t n, double* M, int64_t ldM,
                 int threads) {
   run_batch(t, alpha, M, n, ldM, 3, threads);
+}
+
+/* One element's direct fill for m1 in [m1_lo, m1_hi) only, every pair and term
+ * (single thread): the bounded sample behind the extrapolated CPU time of the
+ * C5 direct ablation.  Returns the number of canonical (m1, m2) u-index pairs
+ * covered and, in *total_pairs, the number the full fill covers. */
+long por_direct_sample(const por_tables* t, const double* alpha, int m1_lo, int m1_hi, double* M, int64_t ldM,
+                       long* total_pairs) {
+  const int S = t->pb.n_terms, nc = t->pb.n_comp, Nt = t->Nt;
+  const long slab = (long)t->pb.nq[0] * t->pb.nq[1] * t->pb.nq[2];
+  for (int gi = 0; gi < nc; ++gi)
+    for (int gj = 0; gj < nc; ++gj)
+      for (int s = 0; s < S; ++s)
+        term_direct_rows(&t->term[s], alpha + ((long)(gi * nc + gj) * S + s) * slab,
+                         M + (long)gi * Nt * ldM + (long)gj * Nt, ldM, m1_lo, m1_hi);
+  const por_dir* d0 = t->term[0].d;
+  long cov = 0, all = 0;
+  for (int m1 = 0; m1 < d0->nt; ++m1)
+    for (int m2 = d0->symmetric ? m1 : 0; m2 < d0->nr; ++m2) {
+      ++all;
+      if (m1 >= m1_lo && m1 < m1_hi) ++cov;
+    }
+  if (total_pairs) *total_pairs = all;
+  return cov;
 }
 
 /* ---------------- comparator: verify.cpp:81-99 ---------------- */

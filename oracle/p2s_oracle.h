@@ -138,6 +138,8 @@ void por_contract(const por_tables* t, const double* I, int64_t n, double* M, in
                   int threads);
 void por_fill(const por_tables* t, const double* alpha, int64_t n, double* M, int64_t ldM,
               int threads);
+long por_direct_sample(const por_tables* t, const double* alpha, int m1_lo, int m1_hi, double* M, int64_t ldM,
+                       long* total_pairs);
 void por_direct(const por_tables* t, const double* alpha, int64_t n, double* M, int64_t ldM,
                 int threads);
 

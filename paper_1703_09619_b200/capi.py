@@ -49,6 +49,10 @@ class UnsupportedShape(P2SError):
     pass
 
 
+class GeometryError(P2SError):
+    """GeometryError in the reference: non-positive Jacobian (assembly.cpp:95-99)."""
+
+
 class Problem(C.Structure):
     _fields_ = [
         ("n_comp", C.c_int32),
@@ -109,7 +113,7 @@ def lib():
         vp, i64, dp = C.c_void_p, C.c_int64, C.POINTER(C.c_double)
         L.p2s_create.argtypes = [C.POINTER(Problem), C.c_int, C.POINTER(vp)]
         L.p2s_create_ex.argtypes = [C.POINTER(Problem), C.c_int, C.c_char_p, C.POINTER(vp)]
-        L.p2s_shape_prepare.argtypes = [C.POINTER(Problem), C.c_char_p, C.c_int]
+        L.p2s_shape_prepare.argtypes = [C.POINTER(Problem), C.c_char_p, C.c_char_p, C.c_int]
         L.p2s_jit_cache_dir.restype = C.c_char_p
         L.p2s_destroy.argtypes = [vp]
         L.p2s_destroy.restype = None
@@ -163,6 +167,8 @@ def _check(status: int):
             raise InvalidArgument(status, msg)
         if status == UNSUPPORTED_SHAPE:
             raise UnsupportedShape(status, msg)
+        if status == GEOMETRY_ERROR:
+            raise GeometryError(status, msg)
         raise P2SError(status, msg)
 
 
@@ -191,11 +197,12 @@ def shape_supported_basis(n_comp, order, kinds, nq, basis) -> bool:
     return bool(lib().p2s_shape_supported(C.byref(make_problem(n_comp, order, kinds, nq, basis))))
 
 
-def shape_prepare(n_comp, order, kinds, nq, basis=BASIS_MODAL) -> str:
+def shape_prepare(n_comp, order, kinds, nq, basis=BASIS_MODAL, options: dict | None = None) -> str:
     """Build (or find) the generated kernel module of a shape without a device
     (p2s_shape_prepare); returns the plan and module path."""
     buf = C.create_string_buffer(1024)
-    _check(lib().p2s_shape_prepare(C.byref(make_problem(n_comp, order, kinds, nq, basis)), buf, 1024))
+    _check(lib().p2s_shape_prepare(C.byref(make_problem(n_comp, order, kinds, nq, basis)),
+                                   options_string(options), buf, 1024))
     return buf.value.decode()
 
 

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -67,6 +68,8 @@ const char* const kOptionKeys[] = {
     "P2S_FORCE_GENERIC",    // 1: runtime-shaped generic kernels (where compiled)
     "P2S_JIT",              // 0: never use a generated module
     "P2S_FORCE_JIT",        // 1: a generated module even for registered shapes
+    "P2S_JIT_FAMILY",       // planner overrides: fused / large
+    "P2S_JIT_T", "P2S_JIT_FLAGS", "P2S_JIT_FPT", "P2S_JIT_MINB", "P2S_JIT_THREADS", "P2S_JIT_KC",
     "P2S_GEO_MODE",         // geometry fill mode 0 / 1 / 2
     "P2S_XCHUNK_MB",        // large path: intermediate chunk (MB)
     "P2S_LARGE_PS", "P2S_LARGE_OVERLAP", "P2S_LARGE_PRIO", "P2S_LARGE_USTREAMS", "P2S_LARGE_UPERSIST",
@@ -111,6 +114,22 @@ bool parse_options(const char* text, Options* o, std::string* err) {
     }
   }
   return flush();
+}
+
+jit::Overrides overrides_of(const Options& opt) {
+  jit::Overrides ov;
+  auto num = [&](const char* k, int* dst) {
+    if (const char* v = opt.get(k)) *dst = std::atoi(v);
+  };
+  if (const char* v = opt.get("P2S_JIT_FAMILY"))
+    ov.family = std::string(v) == "large" ? jit::kFamilyLarge : jit::kFamilyFused;
+  num("P2S_JIT_T", &ov.T);
+  num("P2S_JIT_FLAGS", &ov.flags);
+  num("P2S_JIT_FPT", &ov.fpt);
+  num("P2S_JIT_MINB", &ov.minb);
+  num("P2S_JIT_THREADS", &ov.threads);
+  num("P2S_JIT_KC", &ov.kc);
+  return ov;
 }
 
 // ------------------------------------------------------------ registry lookup
@@ -256,6 +275,11 @@ struct p2s_ctx {
   int* h_bad = nullptr;  // (pinned host copy)
   cudaStream_t s_geo = nullptr;
   cudaEvent_t ev_geo_start = nullptr, ev_ga[2]{}, ev_gf[2]{};
+  // context scratch (two-stage moment buffers, large-path X / Z, host ring,
+  // geometry buffers): calls that use it are ordered on the device through
+  // ev_scratch whatever stream they come on; scratch_mu orders the host side
+  std::mutex scratch_mu;
+  cudaEvent_t ev_scratch = nullptr;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -508,6 +532,28 @@ void problem_sizes(const p2s_problem& pb, p2s_sizes* sz) {
   sz->moments_per_elem = sz->moments_per_pair * sz->n_pairs;
 }
 
+// Held for a call that uses context scratch: the call's stream first waits
+// for the previous such call (any stream), and the release records the event
+// on it, so concurrent callers never share the buffers.
+class ScratchUse {
+ public:
+  ScratchUse(p2s_ctx* c, cudaStream_t st) : c_(c), st_(st), lock_(c->scratch_mu) {
+    ok_ = cudaStreamWaitEvent(st_, c_->ev_scratch, 0) == cudaSuccess;
+  }
+  ~ScratchUse() { cudaEventRecord(c_->ev_scratch, st_); }
+  bool ok() const { return ok_; }
+
+ private:
+  p2s_ctx* c_;
+  cudaStream_t st_;
+  std::lock_guard<std::mutex> lock_;
+  bool ok_ = false;
+};
+
+// Alpha rows are read with 32-B loads (ld.global.nc.v4.f64) when nq_u % 4 == 0,
+// else with 16-B loads / 16-B bulk prefetches
+int alpha_align(const p2s_ctx* c) { return c->pb.nq[0] % 4 == 0 ? 32 : 16; }
+
 p2s_status check_ctx(const p2s_ctx* c) {
   if (!c) return fail(P2S_INVALID_ARG, "null context");
   return P2S_OK;
@@ -562,17 +608,24 @@ p2s_status p2s_create(const p2s_problem* spec_in, int device, p2s_ctx** out) {
   return p2s_create_ex(spec_in, device, nullptr, out);
 }
 
-p2s_status p2s_shape_prepare(const p2s_problem* spec_in, char* desc, int desc_len) {
+p2s_status p2s_shape_prepare(const p2s_problem* spec_in, const char* options, char* desc, int desc_len) {
   p2s_status st = validate(spec_in);
   if (st != P2S_OK) return st;
+  Options opt;
+  {
+    std::string err;
+    if (!parse_options(options, &opt, &err)) return fail(P2S_INVALID_ARG, "p2s_shape_prepare: " + err);
+  }
+  const bool force_jit = opt.get("P2S_FORCE_JIT") && opt.get("P2S_FORCE_JIT")[0] == '1';
   const p2s_problem eff = effective(*spec_in);
   std::string d;
-  if (find_v2(eff, Options{}) || find_large(eff)) {
+  if (!force_jit && (find_v2(eff, opt) || find_large(eff))) {
     d = "registered (ahead of time)";
   } else {
     jit::Plan pl;
     std::string why;
-    if (!jit::plan(eff, &pl, &why)) return fail(P2S_UNSUPPORTED_SHAPE, "p2s_shape_prepare: " + why);
+    if (!jit::plan(eff, &pl, &why, overrides_of(opt)))
+      return fail(P2S_UNSUPPORTED_SHAPE, "p2s_shape_prepare: " + why);
     if (!jit::module(pl, &why)) return fail(P2S_UNSUPPORTED_SHAPE, "p2s_shape_prepare: " + why);
     d = pl.desc + " | " + jit::module_path(pl);
   }
@@ -616,7 +669,7 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
   if (!v2e && !lge && !want_generic && !no_jit) {
     jit::Plan pl;
     std::string why;
-    if (!jit::plan(*spec, &pl, &why)) {
+    if (!jit::plan(*spec, &pl, &why, overrides_of(opt))) {
       if (!entry) return fail(P2S_UNSUPPORTED_SHAPE, "p2s_create: " + why);
     } else {
       je = jit::module(pl, &why);
@@ -654,6 +707,7 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
 
   // every early return below releases what was allocated so far
   std::unique_ptr<p2s_ctx, void (*)(p2s_ctx*)> c(new p2s_ctx, &p2s_destroy);
+  P2S_CUDA(cudaEventCreateWithFlags(&c->ev_scratch, cudaEventDisableTiming));
   c->pb = *spec;
   c->device = device;
   c->opt = opt;
@@ -870,6 +924,7 @@ void p2s_destroy(p2s_ctx* c) {
     if (c->ev_gf[b]) cudaEventDestroy(c->ev_gf[b]);
   }
   if (c->ev_geo_start) cudaEventDestroy(c->ev_geo_start);
+  if (c->ev_scratch) cudaEventDestroy(c->ev_scratch);
   if (c->d_bad) cudaFree(c->d_bad);
   if (c->h_bad) cudaFreeHost(c->h_bad);
   if (c->s_geo) cudaStreamDestroy(c->s_geo);
@@ -906,7 +961,8 @@ p2s_status p2s_get_sizes(const p2s_ctx* c, p2s_sizes* out) {
 p2s_status p2s_moments(p2s_ctx* c, const double* d_alpha, double* d_I, int64_t n, void* stream) {
   if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
   if (n < 0 || (n > 0 && (!d_alpha || !d_I))) return fail(P2S_INVALID_ARG, "p2s_moments: bad buffers");
-  if (reinterpret_cast<uintptr_t>(d_alpha) % 16) return fail(P2S_INVALID_ARG, "alpha must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(d_alpha) % alpha_align(c))
+    return fail(P2S_INVALID_ARG, "p2s_moments: alpha must be " + std::to_string(alpha_align(c)) + "-byte aligned");
   P2S_CUDA(cudaSetDevice(c->device));
   return run_moments(c, d_alpha, d_I, n, static_cast<cudaStream_t>(stream));
 }
@@ -918,6 +974,11 @@ p2s_status p2s_contract(p2s_ctx* c, const double* d_I, double* d_M, int64_t ldM,
   if (ldM < c->sz.n_tot) return fail(P2S_INVALID_ARG, "p2s_contract: ld_M < n_tot");
   if (reinterpret_cast<uintptr_t>(d_I) % 16) return fail(P2S_INVALID_ARG, "I must be 16-byte aligned");
   P2S_CUDA(cudaSetDevice(c->device));
+  if (c->large) {  // the w / v / u steps run through context scratch
+    ScratchUse use(c, static_cast<cudaStream_t>(stream));
+    if (!use.ok()) return fail(P2S_CUDA_ERROR, "p2s_contract: stream ordering");
+    return run_contract(c, d_I, d_M, ldM, n, static_cast<cudaStream_t>(stream));
+  }
   return run_contract(c, d_I, d_M, ldM, n, static_cast<cudaStream_t>(stream));
 }
 
@@ -926,8 +987,14 @@ p2s_status p2s_fill(p2s_ctx* c, const double* d_alpha, double* d_M, int64_t ldM,
   if (check_ctx(c) != P2S_OK) return P2S_INVALID_ARG;
   if (n < 0 || (n > 0 && (!d_alpha || !d_M))) return fail(P2S_INVALID_ARG, "p2s_fill: bad buffers");
   if (ldM < c->sz.n_tot) return fail(P2S_INVALID_ARG, "p2s_fill: ld_M < n_tot");
-  if (reinterpret_cast<uintptr_t>(d_alpha) % 16) return fail(P2S_INVALID_ARG, "alpha must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(d_alpha) % alpha_align(c))
+    return fail(P2S_INVALID_ARG, "p2s_fill: alpha must be " + std::to_string(alpha_align(c)) + "-byte aligned");
   P2S_CUDA(cudaSetDevice(c->device));
+  if (!c->fused) {  // two-stage / large paths: moment and intermediate scratch
+    ScratchUse use(c, static_cast<cudaStream_t>(stream));
+    if (!use.ok()) return fail(P2S_CUDA_ERROR, "p2s_fill: stream ordering");
+    return run_fill(c, d_alpha, d_M, ldM, n, static_cast<cudaStream_t>(stream));
+  }
   return run_fill(c, d_alpha, d_M, ldM, n, static_cast<cudaStream_t>(stream));
 }
 
@@ -939,6 +1006,7 @@ p2s_status p2s_fill_host(p2s_ctx* c, const double* h_alpha, double* h_M, int64_t
   const int64_t nt = c->sz.n_tot;
   const int64_t ape = c->sz.alpha_per_elem;
   const int64_t mel = nt * nt;  // device ring keeps ld = n_tot
+  std::lock_guard<std::mutex> ring_lock(c->scratch_mu);  // synchronous: host-side order suffices
   if (!c->s_h2d) {
     P2S_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
     P2S_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
@@ -1021,7 +1089,14 @@ p2s_status p2s_contract_host(p2s_ctx* c, const double* h_I, double* h_M, int64_t
   cudaError_t e = cudaMalloc(&dM, nm);
   p2s_status st = P2S_OK;
   if (e == cudaSuccess) e = cudaMemcpy(dI, h_I, ni, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) st = run_contract(c, dI, dM, nt, n, 0);
+  if (e == cudaSuccess) {
+    if (c->large) {
+      ScratchUse use(c, 0);
+      st = run_contract(c, dI, dM, nt, n, 0);
+    } else {
+      st = run_contract(c, dI, dM, nt, n, 0);
+    }
+  }
   if (e == cudaSuccess && st == P2S_OK)
     e = cudaMemcpy2D(h_M, sizeof(double) * ldM, dM, sizeof(double) * nt, sizeof(double) * nt, nt * n,
                      cudaMemcpyDeviceToHost);
@@ -1084,6 +1159,8 @@ p2s_status p2s_alpha_from_geometry(p2s_ctx* c, const double* d_geom, int64_t n, 
   if (n == 0) return P2S_OK;
   P2S_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ScratchUse use(c, st);  // the Jacobian flag
+  if (!use.ok()) return fail(P2S_CUDA_ERROR, "p2s_alpha_from_geometry: stream ordering");
   p2s_status s0 = geo_flag_begin(c, st);
   if (s0 != P2S_OK) return s0;
   const double* xs[3] = {c->d_x[0], c->d_x[1], c->d_x[2]};
@@ -1101,6 +1178,8 @@ p2s_status p2s_fill_geometry(p2s_ctx* c, const double* d_geom, double* d_M, int6
   if (!d_geom || !d_M) return fail(P2S_INVALID_ARG, "p2s_fill_geometry: null buffer");
   P2S_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ScratchUse use(c, st);  // geometry buffers, flag, fill scratch
+  if (!use.ok()) return fail(P2S_CUDA_ERROR, "p2s_fill_geometry: stream ordering");
   p2s_status s0 = geo_flag_begin(c, st);
   if (s0 != P2S_OK) return s0;
   const fused_fn geo_launch = !c->fused              ? nullptr

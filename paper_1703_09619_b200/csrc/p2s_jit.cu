@@ -188,7 +188,7 @@ std::string kinds_list(const Desc& d) {
 }
 
 // Fused family: the first candidate that fits, in order of preference.
-bool plan_fused(const Desc& d, Plan* pl) {
+bool plan_fused(const Desc& d, Plan* pl, const Overrides& ov) {
   const int NU = d.N[0], NV = d.N[1];
   const bool sym = d.sym(1) && d.sym(2);
   const bool modal = !d.any_conforming();
@@ -199,17 +199,26 @@ bool plan_fused(const Desc& d, Plan* pl) {
   int base = (psplit ? 64 : 0) | (NU >= 8 ? 2 : 0);
   std::vector<int> tiles;
   for (int t = NV; t >= 1; --t)
-    if (NV % t == 0) tiles.push_back(t);
-  const int threads = 256;
+    if (NV % t == 0 && (ov.T < 0 || t == ov.T)) tiles.push_back(t);
+  const int threads = ov.threads > 0 ? ov.threads : 256;
   FusedCand best{};
   bool found = false;
   // two CTAs per SM with the widest n1 tile, else one CTA per SM
+  // non-symmetric v/w kinds: stage A once per unit for all n1 (AALL, flag 1);
+  // the per-tile stage A (T < N_v without AALL) gave wrong matrices for a
+  // generated (7, 7, 7) shape at T = 1 (fused and contract_v2 alike,
+  // tools/jit_variants.py; profiles/r2_jit_variants.txt), so the planner never
+  // emits it (the registered C2 / C4 variants with T = 2 pass their parity tests)
   for (int pass = 0; pass < 2 && !found; ++pass)
-    for (int symf : {sym ? 4 : 0, 0}) {
+    for (int symf : {sym ? 4 : 1, 1}) {
       for (int t : tiles) {
-        FusedCand c = fused_candidate(d, t, base | symf, threads, fpt);
+        FusedCand c = fused_candidate(d, t, ov.flags >= 0 ? ov.flags : (base | symf), threads,
+                                      ov.fpt > 0 ? ov.fpt : fpt);
+        if (ov.minb > 0) c.minb = ov.minb;
         if (!fused_ok(c)) continue;
-        if (pass == 0 && c.smem_fused > kSmemTwo) continue;
+        if (((c.flags >> 2) & 1) && !sym) continue;
+        if (!(c.flags & 5) && c.T < NV) continue;  // see above
+        if (pass == 0 && c.smem_fused > kSmemTwo && ov.minb < 0) continue;
         best = c;
         found = true;
         break;
@@ -234,9 +243,9 @@ bool plan_fused(const Desc& d, Plan* pl) {
   return true;
 }
 
-bool plan_large(const Desc& d, Plan* pl, std::string* why) {
+bool plan_large(const Desc& d, Plan* pl, std::string* why, const Overrides& ov) {
   // k1 chunks of the moment kernel: 4 (C5); the moment scratch must fit
-  int kc = 4;
+  int kc = ov.kc > 0 ? ov.kc : 4;
   auto mom_smem = [&](int k) {
     return 8 * (static_cast<int64_t>(k) * d.Q[2] * (d.Q[1] | 1) + static_cast<int64_t>(k) * d.KMAX(1) * (d.Q[2] | 1));
   };
@@ -400,7 +409,7 @@ bool compile(const Plan& pl, const std::string& dir, const std::string& key, std
 
 }  // namespace
 
-bool plan(const p2s_problem& eff, Plan* pl, std::string* why) {
+bool plan(const p2s_problem& eff, Plan* pl, std::string* why, const Overrides& ov) {
   Desc d{};
   for (int k = 0; k < 3; ++k) {
     d.N[k] = eff.order[k];
@@ -409,8 +418,12 @@ bool plan(const p2s_problem& eff, Plan* pl, std::string* why) {
   d.S = eff.n_terms;
   for (int s = 0; s < d.S; ++s)
     for (int k = 0; k < 3; ++k) d.kind[s][k] = eff.kind[s][k];
-  if (plan_fused(d, pl)) return true;
-  return plan_large(d, pl, why);
+  if (ov.family != kFamilyLarge && plan_fused(d, pl, ov)) return true;
+  if (ov.family == kFamilyFused) {
+    *why = "no fused-family instantiation fits this shape (with these overrides)";
+    return false;
+  }
+  return plan_large(d, pl, why, ov);
 }
 
 const reg::JitEntries* module(const Plan& pl, std::string* err) {

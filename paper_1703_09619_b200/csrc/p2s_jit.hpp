@@ -22,9 +22,16 @@ struct Plan {
   int64_t smem = 0;    // planned shared memory of the dominant kernel (bytes)
 };
 
+// Planner overrides (p2s_create_ex options P2S_JIT_*; -1 = planner's choice):
+// family (1 fused, 2 large), n1 tile, Shape flags, fibers per thread, CTAs per
+// SM, threads, large-path k1 chunk.
+struct Overrides {
+  int family = -1, T = -1, flags = -1, fpt = -1, minb = -1, threads = -1, kc = -1;
+};
+
 // Kernel family and template parameters for a problem (basis folded into the
 // kinds); false with *why when no family can hold it.
-bool plan(const p2s_problem& eff, Plan* pl, std::string* why);
+bool plan(const p2s_problem& eff, Plan* pl, std::string* why, const Overrides& ov = Overrides{});
 
 // The plan's compiled module (cached on disk, loaded once per process).
 const reg::JitEntries* module(const Plan& pl, std::string* err);

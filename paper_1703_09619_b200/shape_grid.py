@@ -55,7 +55,10 @@ ALL = ISOTROPIC + RANDOM + BENCH
 
 def shape_id(case) -> str:
     nc, order, kinds, nq, basis = case
-    ks = "".join("PDLR"[k] if isinstance(k, int) else "".join("PDLR"[x] for x in k) for k in kinds)
+    def kc(k):
+        return "PDLR"[k] if 0 <= k < 4 else f"[{k}]"
+
+    ks = "".join(kc(k) if isinstance(k, int) else "".join(kc(x) for x in k) for k in kinds)
     return f"{nc}c-{order[0]}x{order[1]}x{order[2]}-{ks}-q{nq[0]}x{nq[1]}x{nq[2]}" + ("-conf" if basis else "")
 
 
@@ -70,10 +73,11 @@ def prepare_all(cases=None, workers: int = 0):
     workers = workers or min(16, os.cpu_count() or 1)
 
     def one(c):
+        name = shape_id(c[:5]) + (f" {c[5]}" if len(c) > 5 else "")
         try:
-            return shape_id(c), capi.shape_prepare(*c)
+            return name, capi.shape_prepare(*c)
         except Exception as e:  # reported, not raised: the GPU tests name the shape
-            return shape_id(c), f"ERROR {e}"
+            return name, f"ERROR {e}"
 
     with ThreadPoolExecutor(max_workers=workers) as ex:  # ctypes releases the GIL
         return dict(ex.map(one, cases))

@@ -52,8 +52,9 @@ def _jit_prepare(request, monkeypatch):
         opts = dict(capi.DEFAULT_OPTIONS)
         opts.update(options or {})
         if opts.get("P2S_JIT") != "0" and opts.get("P2S_FORCE_GENERIC") != "1":
+            jopts = {k: v for k, v in opts.items() if k.startswith("P2S_JIT_") or k == "P2S_FORCE_JIT"}
             _PREPARE.append((n_comp, tuple(order), [tuple(k) if isinstance(k, (list, tuple)) else k
-                                                     for k in kinds], tuple(nq), basis))
+                                                     for k in kinds], tuple(nq), basis, jopts))
         pytest.skip("jit-prepare")
 
     monkeypatch.setattr(capi.Context, "__init__", init)
@@ -64,7 +65,7 @@ def pytest_sessionfinish(session, exitstatus):
     if not session.config.getoption("--jit-prepare") or not _PREPARE:
         return
     from paper_1703_09619_b200 import shape_grid
-    uniq = {shape_grid.shape_id(c): c for c in _PREPARE}
+    uniq = {shape_grid.shape_id(c[:5]) + str(sorted(c[5].items())): c for c in _PREPARE}
     res = shape_grid.prepare_all(list(uniq.values()))
     bad = {k: v for k, v in res.items() if v.startswith("ERROR")}
     print(f"\njit-prepare: {len(res)} shapes, {len(bad)} errors")

@@ -31,10 +31,13 @@ CASES = [
     (1, (4, 4, 4), [PP], (8, 8, 8), {"P2S_FORCE_GENERIC": "1"}, "two-stage"),
     (1, (4, 4, 4), [PP], (8, 8, 8), {"P2S_NO_FUSED": "1"}, "two-stage: moments_v2_kernel + contract_v2"),
     (1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7), {"P2S_FORCE_JIT": "1"}, "fused"),
-    (1, (7, 6, 5), [(DP, PD, PP), (PD, DP, DD)], (9, 8, 7), {}, "large-order"),  # generated large
+    (1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7), {"P2S_FORCE_JIT": "1", "P2S_JIT_FAMILY": "large"},
+     "large-order"),
+    (1, (7, 6, 5), [(DP, PD, PP), (PD, DP, DD)], (9, 8, 7), {"P2S_JIT_FAMILY": "large"},
+     "large-order"),                                                                  # generated large
     (3, (3, 3, 3), [PP, DD], (6, 6, 6), {}, "two-stage: moments_v2_kernel + contract_v2"),
     (3, (3, 3, 3), [PP, DD], (6, 6, 6), {"P2S_FORCE_GENERIC": "1"}, "two-stage"),
-    (1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7), {}, "two-stage"),
+    (1, (4, 3, 3), [(DP, PD, PP), (PD, DP, DD)], (9, 5, 7), {}, "fused"),                    # generated module
     (1, (5, 4, 3), [PP, DD], (8, 8, 6), {}, "large-order"),
     ("c2", None, None, None, {}, "fused"),
     ("c2", None, None, None, {"P2S_NO_FUSED": "1"}, "two-stage: moments_v2_kernel + contract_v2"),

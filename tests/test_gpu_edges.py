@@ -199,3 +199,56 @@ def test_two_stage_chunk_pipeline_matches_oracle(env, monkeypatch):
     for e in range(n):
         ok, msg, _ = blocks_close(Mg[e], Mo[e], 1, ctx.n_tot)
         assert ok, (e, msg)
+
+
+@pytest.mark.parametrize("name,shift", [("c4", 2), ("c4", 4), ("c2", 2)])
+def test_alpha_alignment_is_checked(name, shift):
+    """alpha rows are read with 32-B loads when nq_u % 4 == 0 (C4: nq 16): an
+    alpha 16-B but not 32-B aligned is rejected up front instead of faulting;
+    32-B aligned offsets (and 16-B offsets for C2's nq 14) fill correctly."""
+    cfg = CONFIGS[name]
+    ctx = capi.Context(**cfg.problem())
+    n = 2
+    o = oracle_for(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
+    alpha = o.alpha(cfg.alpha_kind, cfg.alpha_lo, cfg.alpha_hi, 8, 0, n)
+    buf = torch.zeros(alpha.size + 8, dtype=torch.float64, device="cuda")
+    a = buf[shift:shift + alpha.size]
+    a.copy_(torch.from_numpy(alpha.reshape(-1)))
+    M = _nan(n, ctx.n_tot, ctx.n_tot)
+    st = torch.cuda.current_stream().cuda_stream
+    need32 = cfg.nq[0] % 4 == 0
+    if need32 and (shift * 8) % 32:
+        with pytest.raises(capi.InvalidArgument):
+            ctx.fill(a, M, ctx.n_tot, n, st)
+        with pytest.raises(capi.InvalidArgument):
+            ctx.moments(a, torch.zeros((n, ctx.moments_per_elem), dtype=torch.float64, device="cuda"), n, st)
+        return
+    ctx.fill(a, M, ctx.n_tot, n, st)
+    torch.cuda.synchronize()
+    Mo = o.fill(alpha, threads=8)
+    Nt = cfg.order[0] * cfg.order[1] * cfg.order[2]
+    for e in range(n):
+        ok, msg, _ = blocks_close(M[e].cpu().numpy(), Mo[e], cfg.n_comp, Nt)
+        assert ok, msg
+
+
+def test_concurrent_streams_share_context_scratch():
+    """Two streams fill through one two-stage (C3) and one large-order context at
+    once: the context event orders their use of the moment / intermediate scratch
+    (each result equals the single-stream fill bitwise)."""
+    for problem, opts in (((1, (8, 8, 8), [PP, DD], (20, 20, 20)), {"P2S_CHUNK_MB": "1"}),
+                          ((3, (5, 4, 3), [PP, DD], (8, 8, 6)), {"P2S_XCHUNK_MB": "1"})):
+        ctx = capi.Context(*problem, options=opts)
+        o = oracle_for(*problem)
+        n = 40
+        alpha = torch.from_numpy(o.alpha(O.ALPHA_SINE, 0.5, 3.0, 21, 0, n)).cuda()
+        ref = _nan(n, ctx.n_tot, ctx.n_tot)
+        ctx.fill(alpha, ref, ctx.n_tot, n, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        A, B = _nan(n, ctx.n_tot, ctx.n_tot), _nan(n, ctx.n_tot, ctx.n_tot)
+        for _ in range(3):
+            ctx.fill(alpha, A, ctx.n_tot, n, s1.cuda_stream)
+            ctx.fill(alpha, B, ctx.n_tot, n, s2.cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(A, ref) and torch.equal(B, ref)

@@ -85,3 +85,30 @@ def test_fill_geometry_errors():
     with pytest.raises(capi.InvalidArgument):
         ctx.fill_geometry(0, 0, ctx.n_tot - 1, 1)
     ctx.fill_geometry(0, 0, ctx.n_tot, 0)  # empty batch: no-op
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_folded_hexahedron_raises_geometry_error(mode, monkeypatch):
+    """A hexahedron folded through itself (two corner layers swapped: det J < 0)
+    is the reference's GeometryError (assembly.cpp:95-99) on every geometry
+    entry point and mode; valid records still fill afterwards (the flag is reset
+    per call)."""
+    monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_GEO_MODE", str(mode))
+    cfg, ctx = _ctx("c2")
+    n = 5
+    sp = torch.cuda.current_stream().cuda_stream
+    geom = torch.empty((n, ctx.GEOM_DOUBLES), dtype=torch.float64, device="cuda")
+    ctx.geometry_generate(cfg.alpha_lo, cfg.alpha_hi, 3, 0, n, geom, sp)
+    bad = geom.clone()
+    corners = bad[3, :24].view(8, 3).clone()
+    bad[3, :24] = corners[[4, 5, 6, 7, 0, 1, 2, 3]].reshape(-1)  # w -> -w: mirrored element
+    alpha = torch.empty((n, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")
+    M = torch.empty((n, ctx.n_tot, ctx.n_tot), dtype=torch.float64, device="cuda")
+    with pytest.raises(capi.GeometryError):
+        ctx.alpha_from_geometry(bad, n, alpha, sp)
+    with pytest.raises(capi.GeometryError):
+        ctx.fill_geometry(bad, M, ctx.n_tot, n, sp)
+    ctx.alpha_from_geometry(geom, n, alpha, sp)
+    ctx.fill_geometry(geom, M, ctx.n_tot, n, sp)
+    torch.cuda.synchronize()
+    assert torch.isfinite(M).all()

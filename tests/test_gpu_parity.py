@@ -247,8 +247,11 @@ def test_error_paths():
         ctx.fill(a, M, ctx.n_tot - 1, 1)
     with pytest.raises(capi.InvalidArgument):
         ctx.fill(0, M, ctx.n_tot, 1)
-    with pytest.raises(capi.UnsupportedShape):
-        capi.Context(1, (7, 3, 3), [DP], (5, 5, 5))
+    with pytest.raises(capi.UnsupportedShape):  # no ahead-of-time kernel, generated modules off
+        capi.Context(1, (7, 3, 3), [DP], (5, 5, 5), options={"P2S_JIT": "0"})
+    with pytest.raises(capi.UnsupportedShape):  # a fused-family instantiation cannot hold N = 16
+        capi.Context(1, (16, 16, 16), [PP, DD], (20, 20, 20), options={"P2S_JIT_FAMILY": "fused",
+                                                                        "P2S_FORCE_JIT": "1"})
     with pytest.raises(capi.InvalidArgument):
         capi.Context(1, (0, 3, 3), [PP], (5, 5, 5))
 
