@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-subconfigs", action="store_true",
                     help="skip the C3 / C4 / C5 / c12 lines of the default (c2) run")
     ap.add_argument("--sub-steps", type=int, default=10)
+    ap.add_argument("--options", default="",
+                    help="p2s_create_ex test / tuning hooks for every context, 'KEY=VALUE;...' "
+                         "(measurement sweeps; not used by the driver's runs)")
     return ap.parse_args()
 
 
@@ -579,6 +582,12 @@ def reference_2d_context(threads):
 
 def main():
     args = parse()
+    if args.options:
+        from paper_1703_09619_b200 import capi
+        for kv in args.options.split(";"):
+            if kv.strip():
+                k, _, v = kv.partition("=")
+                capi.DEFAULT_OPTIONS[k.strip()] = v.strip() or "1"
     from paper_1703_09619_b200.configs import CONFIGS
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cctype>
+#include <cmath>
 #include <cstdio>
 #include <map>
 #include <cstdlib>
@@ -73,7 +74,7 @@ const char* const kOptionKeys[] = {
     "P2S_GEO_MODE",         // geometry fill mode 0 / 1 / 2
     "P2S_XCHUNK_MB",        // large path: intermediate chunk (MB)
     "P2S_LARGE_PS", "P2S_LARGE_OVERLAP", "P2S_LARGE_PRIO", "P2S_LARGE_USTREAMS", "P2S_LARGE_UPERSIST",
-    "P2S_LARGE_XS", "P2S_LARGE_MOMCL", "P2S_LARGE_USMEM", "P2S_LARGE_FIB",
+    "P2S_LARGE_XS", "P2S_LARGE_UBULK", "P2S_LARGE_UROLL", "P2S_LARGE_UPAIR", "P2S_LARGE_MOMCL", "P2S_LARGE_USMEM", "P2S_LARGE_FIB",
     "P2S_CHUNK_MB",         // two-stage scheduler chunk (MB of moments)
     "P2S_TWO_STAGE_OVERLAP", "P2S_MOM_PRIO",
     "P2S_HOST_CHUNK_MB",    // p2s_fill_host ring slot (MB of matrices)
@@ -825,11 +826,24 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
     if (!lge->pack(la, c->lpack)) return fail(P2S_CUDA_ERROR, "p2s_create: large-path table upload");
     // X chunk: ~96 MB of v/w-contracted intermediates per buffer (two buffers: the
     // v/w stage of the next chunk overlaps the u stage of this one)
-    int64_t xmb = 96;
-    if (const char* v = opt.get("P2S_XCHUNK_MB")) xmb = std::max(1, std::atoi(v));
+    // X chunk (units per v/u round): L2-resident (<= 32 MB, the double buffer
+    // within the 126 MB L2) when that still gives the u stage >= 2.5 waves of
+    // (n1, p1) tiles over 2 CTAs per SM, else >= 6 waves (amortised tails) up to
+    // 96 MB.  Measured (r2j): c12 (3.95 MB / unit) 24 MB 0.60 vs 96 MB 0.53 of
+    // HBM; C5 (16.7 MB / unit) 96 MB 0.65 vs 48 MB 0.59.
+    const int64_t tiles_per_unit = static_cast<int64_t>(spec->order[1]) * spec->order[2];
+    const int64_t ctas = 2 * static_cast<int64_t>(c->num_sms);
+    const int64_t xbytes = lge->xpu * 8;
+    auto units_for_waves = [&](double w) {
+      return static_cast<int64_t>(std::ceil(w * static_cast<double>(ctas) / static_cast<double>(tiles_per_unit)));
+    };
+    int64_t units = units_for_waves(2.5);
+    if (units * xbytes > (int64_t(32) << 20))
+      units = std::max<int64_t>(1, std::min(units_for_waves(6), (int64_t(96) << 20) / xbytes));
+    if (const char* v = opt.get("P2S_XCHUNK_MB")) units = ((int64_t(std::max(1, std::atoi(v)))) << 20) / xbytes;
     if (const char* v = opt.get("P2S_LARGE_PS")) c->lpack.ps = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_OVERLAP")) c->lpack.overlap = v[0] != '0';
-    c->xchunk = std::max<int64_t>(1, (xmb << 20) / (lge->xpu * 8));
+    c->xchunk = std::max<int64_t>(1, units);
     P2S_CUDA(cudaMalloc(&c->d_X, sizeof(double) * lge->xpu * c->xchunk * 2));
     P2S_CUDA(cudaMalloc(&c->lpack.d_Z, sizeof(double) * lge->zpu * c->xchunk));
     // P2S_LARGE_PRIO=1 puts the v/w steps on a high-priority stream (the block
@@ -844,10 +858,16 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
     P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_start, cudaEventDisableTiming));
     P2S_CUDA(cudaEventCreateWithFlags(&c->lpack.ev_join, cudaEventDisableTiming));
     if (const char* v = opt.get("P2S_LARGE_USTREAMS")) c->lpack.two_u = v[0] != '1';
-    c->lpack.u_ctas = 2 * static_cast<int64_t>(c->num_sms);  // persistent u stage, 2 CTAs per SM
-    if (const char* v = opt.get("P2S_LARGE_UPERSIST"))
-      c->lpack.u_ctas = static_cast<int64_t>(std::max(0, std::atoi(v))) * c->num_sms;
+    c->lpack.u_ctas = -1;  // persistent u stage, every resident CTA slot (occupancy x SMs)
+    c->lpack.num_sms = c->num_sms;
+    if (const char* v = opt.get("P2S_LARGE_UPERSIST")) {  // k CTAs per SM; 0: one per tile; < 0: occupancy
+      const int k = std::atoi(v);
+      c->lpack.u_ctas = k < 0 ? -1 : static_cast<int64_t>(k) * c->num_sms;
+    }
     if (const char* v = opt.get("P2S_LARGE_XS")) c->lpack.u_xs = v[0] != '0';
+    if (const char* v = opt.get("P2S_LARGE_UBULK")) c->lpack.u_bulk = v[0] != '0';
+    if (const char* v = opt.get("P2S_LARGE_UROLL")) c->lpack.u_roll = v[0] == '1' ? 1 : 0;
+    if (const char* v = opt.get("P2S_LARGE_UPAIR")) c->lpack.u_pair = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_MOMCL")) c->lpack.mom_cluster = v[0] == '1';
     if (const char* v = opt.get("P2S_LARGE_USMEM")) c->lpack.u_smemc = v[0] == '1';
     if (const char* v = opt.get("P2S_LARGE_FIB")) c->lpack.ufib = std::atoi(v) == 2 ? 2 : 1;

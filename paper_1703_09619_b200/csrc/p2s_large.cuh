@@ -160,6 +160,11 @@ struct LShape {
 #else
   static constexpr bool USYM = u_symmetric();
 #endif
+  // u stage: one thread per fiber (n2, p2); CTAs per SM the launch bounds ask
+  // for (register cap 65536 / (UT * UMINB)): 3 CTAs of 144 threads for N = 12
+  // (ncu: 2 CTAs left the SM at 15 % occupancy, latency-bound), 2 of 256 for C5
+  static constexpr int UT = NV * NW;
+  static constexpr int UMINB = UT <= 96 ? 4 : UT <= 170 ? 3 : UT <= 256 ? 2 : 1;
 };
 
 // ------------------------------------------------------------------ moments
@@ -426,6 +431,9 @@ struct LUParams {
   double* M;
   const double* cu_g;   // device copy of cu (SMEMC: staged into shared memory per CTA)
   int xs;               // XS mode: x classes staged in shared memory by the TMA engine
+  int bulk;             // BULK mode: rows written with TMA bulk stores (M rows 16-B aligned)
+  int roll;             // XS kernel: runtime row loop (1) or every row unrolled (0)
+  int pair;             // PAIR mode: two adjacent fibers per thread, 16-B stores (M rows 16-B aligned)
   int64_t ldM, mat_stride, n_units;
   int nc, P, Nt;
   double cu[Ls::cpar(0)];
@@ -535,7 +543,7 @@ __device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, const double
 // into shared memory (coalesced) and read as uniform-address LDS; else they are
 // constant-bank operands (LDCU).
 template <class Ls, bool PS, int FIB, bool SMEMC = false>
-__global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? 2 : P2S_LARGE_FIB2_MINB) : 1)
+__global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? Ls::UMINB : P2S_LARGE_FIB2_MINB) : 1)
     large_u_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
   extern __shared__ __align__(16) double cus[];
   if constexpr (SMEMC) {
@@ -594,8 +602,8 @@ __device__ __forceinline__ void large_u_xs_issue(const LUParams<Ls>& p, int64_t 
     go(std::integral_constant<int, 1>{});
 }
 
-template <class Ls>
-__global__ void __launch_bounds__(Ls::NV * Ls::NW, 2)
+template <class Ls, bool ROLL = true>
+__global__ void __launch_bounds__(Ls::NV * Ls::NW, Ls::UMINB)
     large_u_xs_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
   constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S;
   static_assert(NW % 2 == 0, "bulk-copy rows must be 16-byte multiples");
@@ -652,6 +660,255 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, 2)
           }
         });
       };
+      if constexpr (ROLL) {  // runtime row loop: bounded code and scheduling window (C5)
+#pragma unroll 1
+        for (int m1 = 0; m1 < NU; ++m1)
+          static_for<0, NU>([&](auto m1c) {
+            if (m1 == decltype(m1c)::value) row(m1c);
+          });
+      } else {  // every row unrolled: no per-row dispatch branch
+        static_for<0, NU>([&](auto m1c) { row(m1c); });
+      }
+    };
+    run(std::integral_constant<int, 0>{});
+    run(std::integral_constant<int, 1>{});
+  }
+}
+
+// BULK mode (u stage with TMA bulk stores): as the XS kernel, but a row of
+// outputs (m1 fixed, every m2 of the parity class) goes to shared memory first --
+// one STS per output instead of one (USYM: two) 8-byte STG -- and one thread
+// writes each (m1, m2) block (the CTA's N_v N_w contiguous doubles of one matrix
+// row) with a bulk copy, and again at (m2, m1) for symmetric u kinds.  Three row
+// buffers rotate: after committing row r the issuing thread waits until row
+// r-1's copies have read shared memory, so one barrier per row orders the reuse
+// of row r-2's buffer by row r+1.
+template <class Ls>
+struct LUBulk {
+  static constexpr int T = Ls::NV * Ls::NW;
+  static constexpr int SL = (Ls::NU + 1) / 2;  // outputs of one row in one parity class
+  static constexpr int NBUF = 3;
+  static constexpr size_t SMEM = sizeof(double) * (static_cast<size_t>(LUXs<Ls>::KXM) * T + NBUF * SL * T) + 16;
+};
+
+template <class Ls>
+__global__ void __launch_bounds__(Ls::NV * Ls::NW, Ls::UMINB)
+    large_u_bulk_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
+  constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S, T = LUBulk<Ls>::T, SL = LUBulk<Ls>::SL;
+  static_assert(T % 2 == 0, "bulk-store rows must be 16-byte multiples");
+  extern __shared__ __align__(128) double xbuf[];
+  double* obuf = xbuf + LUXs<Ls>::KXM * T;  // [NBUF][SL][T]
+  const int tid = threadIdx.x;
+  int64_t b = blockIdx.x;
+  if (b >= ntiles) return;
+  const uint64_t policy = evict_first_policy();
+  large_u_xs_issue<Ls>(p, unit0, b, 0, xbuf);
+  int ring = 0;
+#pragma unroll 1
+  for (; b < ntiles; b += gridDim.x) {
+    const int np = static_cast<int>(b % (NV * NW));
+    const int64_t unit = unit0 + b / (NV * NW);
+    const int n1 = np / NW, p1 = np - (np / NW) * NW;
+    const int64_t e = unit / p.P;
+    const int pair = static_cast<int>(unit - e * p.P);
+    const int gci = pair / p.nc, gcj = pair - gci * p.nc;
+    double* rowbase = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt + n1 * NW + p1) * p.ldM + gcj * p.Nt;
+    const int64_t rowstep = static_cast<int64_t>(T) * p.ldM;
+    auto run = [&](auto parc) {
+      constexpr int PAR = decltype(parc)::value;
+      constexpr int KX = Ls::KX(PAR);
+      double x[KX];
+      asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < KX; ++j) x[j] = xbuf[j * T + tid];
+      __syncthreads();
+      if (PAR == 0)
+        large_u_xs_issue<Ls>(p, unit0, b, 1, xbuf);
+      else if (b + gridDim.x < ntiles)
+        large_u_xs_issue<Ls>(p, unit0, b + gridDim.x, 0, xbuf);
+      auto row = [&](auto m1c) {
+        constexpr int m1 = decltype(m1c)::value;
+        constexpr int m2s = Ls::USYM ? m1 : 0;
+        constexpr int first = m2s + (((m1 + m2s) % 2 == PAR) ? 0 : 1);
+        constexpr int cnt_row = first < NU ? (NU - first + 1) / 2 : 0;
+        static_assert(cnt_row <= SL, "row slots");
+        if constexpr (cnt_row > 0) {
+          double* ob = obuf + ring * (SL * T);
+          static_for<first, NU>([&](auto m2c) {
+            constexpr int m2 = decltype(m2c)::value;
+            if constexpr ((m2 - first) % 2 == 0) {
+              double v = 0.0;
+              static_for<0, S>([&](auto sc) {
+                constexpr int s = decltype(sc)::value;
+                constexpr int ku = Ls::kind(s, 0);
+                constexpr int lo = band_lo(ku, m1, m2), cnt = band_count(ku, m1, m2);
+                constexpr int co = Ls::coff(0, s, m1, m2);
+                static_for<0, cnt>([&](auto jc) {
+                  constexpr int j = decltype(jc)::value;
+                  constexpr int xi = Ls::kpo(s, PAR) + (lo - Ls::uk0(s, PAR)) / 2 + j;
+                  v = fma(lcoef<Ls, 0>(p.cu, p.cu_g, co + j), x[xi], v);
+                });
+              });
+              ob[((m2 - first) / 2) * T + tid] = v;
+            }
+          });
+          fence_proxy_async_smem();  // this thread's outputs visible to the bulk copies
+          __syncthreads();
+          if (tid == 0) {
+            static_for<first, NU>([&](auto m2c) {
+              constexpr int m2 = decltype(m2c)::value;
+              if constexpr ((m2 - first) % 2 == 0) {
+                const double* src = ob + ((m2 - first) / 2) * T;
+                bulk_s2g(rowbase + m1 * rowstep + m2 * T, src, T * 8u, policy);
+                if constexpr (Ls::USYM && m2 != m1) bulk_s2g(rowbase + m2 * rowstep + m1 * T, src, T * 8u, policy);
+              }
+            });
+            bulk_commit();
+            bulk_wait_read<1>();  // row r-1's copies have read their buffer
+          }
+          ring = ring == LUBulk<Ls>::NBUF - 1 ? 0 : ring + 1;
+        }
+      };
+#pragma unroll 1
+      for (int m1 = 0; m1 < NU; ++m1)
+        static_for<0, NU>([&](auto m1c) {
+          if (m1 == decltype(m1c)::value) row(m1c);
+        });
+    };
+    run(std::integral_constant<int, 0>{});
+    run(std::integral_constant<int, 1>{});
+  }
+  if (tid == 0) bulk_wait<0>();  // every copy complete before the CTA's shared memory goes away
+}
+
+// PAIR mode: a thread owns two adjacent fibers (n2, p2), (n2, p2 + 1) of a tile
+// (N_w even), so every constant-bank coefficient feeds two DFMAs, x arrives with
+// one 16-B shared-memory load per k1 for both fibers, and each output pair (and
+// its USYM mirror) leaves with one 16-B streaming store -- half the LDCU and STG
+// instructions of the XS kernel per output.  TPC tiles per CTA keep the CTA a
+// whole number of warps (c12: 4 tiles x 72 threads; C5: 1 tile x 128).
+constexpr int pair_tpc(int th) {
+  int t = 1;
+  while ((t * th) % 32 != 0 && t < 32) ++t;
+  while (t * th < 96 && t < 32) t *= 2;
+  return t;
+}
+
+template <class Ls>
+struct LUPair {
+  static constexpr int T = Ls::NV * Ls::NW, TH = T / 2;
+  static constexpr int TPC = pair_tpc(TH);
+  static constexpr int THREADS = TPC * TH;
+  static constexpr int MINB = 65536 / (THREADS * 136) > 0 ? 65536 / (THREADS * 136) : 1;
+  static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(LUXs<Ls>::KXM) * T * TPC + 16;
+};
+
+template <class Ls>
+__device__ __forceinline__ void large_u_pair_issue(const LUParams<Ls>& p, int64_t unit0, int64_t b, int cls,
+                                                   double* xb, int q) {
+  constexpr int NV = Ls::NV, NW = Ls::NW, NQV = Ls::NQV, S = Ls::S, T = NV * NW;
+  const int np = static_cast<int>(b % T);
+  const int64_t unit = unit0 + b / T;
+  const int n1 = np / NW, p1 = np - (np / NW) * NW;
+  const int c0 = 2 * q;
+  const int n2 = c0 / NW, p2 = c0 - (c0 / NW) * NW;
+  const double* Xu = p.X + (unit - unit0) * Ls::XPU + (static_cast<int64_t>(Ls::vidx(n1, n2)) * NW + p1) * NW + p2;
+  auto go = [&](auto parc) {
+    constexpr int PAR = decltype(parc)::value;
+    static_for<0, S>([&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+#pragma unroll
+      for (int j = 0; j < Ls::ucnt(s, PAR); ++j) {
+        const double* src = Xu + Ls::xoff(s) + static_cast<int64_t>(Ls::uk0(s, PAR) + 2 * j) * NQV * NW * NW;
+        double* dst = xb + (Ls::kpo(s, PAR) + j) * T + c0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+      }
+    });
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (cls == 0)
+    go(std::integral_constant<int, 0>{});
+  else
+    go(std::integral_constant<int, 1>{});
+}
+
+template <class Ls>
+__global__ void __launch_bounds__(LUPair<Ls>::THREADS, LUPair<Ls>::MINB)
+    large_u_pair_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
+  constexpr int NU = Ls::NU, NW = Ls::NW, S = Ls::S, T = LUPair<Ls>::T, TH = LUPair<Ls>::TH;
+  constexpr int TPC = LUPair<Ls>::TPC;
+  static_assert(NW % 2 == 0, "fiber pairs need an even N_w");
+  extern __shared__ __align__(128) double xbuf[];
+  const int g = threadIdx.x / TH, q = threadIdx.x - (threadIdx.x / TH) * TH;
+  double* xb = xbuf + g * (LUXs<Ls>::KXM * T);
+  const int64_t nit = (ntiles + TPC - 1) / TPC;  // CTA iterations: TPC consecutive tiles
+  int64_t it = blockIdx.x;
+  if (it >= nit) return;
+  {
+    const int64_t b = it * TPC + g;
+    if (b < ntiles) large_u_pair_issue<Ls>(p, unit0, b, 0, xb, q);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+#pragma unroll 1
+  for (; it < nit; it += gridDim.x) {
+    const int64_t b = it * TPC + g;
+    const bool live = b < ntiles;
+    const int64_t bb = live ? b : 0;
+    const int np = static_cast<int>(bb % T);
+    const int64_t unit = unit0 + bb / T;
+    const int n1 = np / NW, p1 = np - (np / NW) * NW;
+    const int64_t e = unit / p.P;
+    const int pair = static_cast<int>(unit - e * p.P);
+    const int gci = pair / p.nc, gcj = pair - gci * p.nc;
+    double* out = p.M + e * p.mat_stride + static_cast<int64_t>(gci * p.Nt + n1 * NW + p1) * p.ldM + gcj * p.Nt +
+                  2 * q;
+    const int64_t rowstep = static_cast<int64_t>(T) * p.ldM;
+    auto run = [&](auto parc) {
+      constexpr int PAR = decltype(parc)::value;
+      constexpr int KX = Ls::KX(PAR);
+      double xa[KX], xc[KX];
+      asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < KX; ++j) {
+        const double2 v = *reinterpret_cast<const double2*>(xb + j * T + 2 * q);
+        xa[j] = v.x;
+        xc[j] = v.y;
+      }
+      __syncthreads();
+      if (PAR == 0) {
+        if (live) large_u_pair_issue<Ls>(p, unit0, b, 1, xb, q);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+      } else {
+        const int64_t b2 = b + static_cast<int64_t>(gridDim.x) * TPC;
+        if (b2 < ntiles) large_u_pair_issue<Ls>(p, unit0, b2, 0, xb, q);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      auto row = [&](auto m1c) {
+        constexpr int m1 = decltype(m1c)::value;
+        static_for<(Ls::USYM ? m1 : 0), NU>([&](auto m2c) {
+          constexpr int m2 = decltype(m2c)::value;
+          if constexpr ((m1 + m2) % 2 == PAR) {
+            double va = 0.0, vc = 0.0;
+            static_for<0, S>([&](auto sc) {
+              constexpr int s = decltype(sc)::value;
+              constexpr int ku = Ls::kind(s, 0);
+              constexpr int lo = band_lo(ku, m1, m2), cnt = band_count(ku, m1, m2);
+              constexpr int co = Ls::coff(0, s, m1, m2);
+              static_for<0, cnt>([&](auto jc) {
+                constexpr int j = decltype(jc)::value;
+                constexpr int xi = Ls::kpo(s, PAR) + (lo - Ls::uk0(s, PAR)) / 2 + j;
+                const double c = lcoef<Ls, 0>(p.cu, p.cu_g, co + j);
+                va = fma(c, xa[xi], va);
+                vc = fma(c, xc[xi], vc);
+              });
+            });
+            if (live) {
+              st_cs2(out + m1 * rowstep + m2 * T, va, vc);
+              if constexpr (Ls::USYM && m2 != m1) st_cs2(out + m2 * rowstep + m1 * T, va, vc);
+            }
+          }
+        });
+      };
 #pragma unroll 1
       for (int m1 = 0; m1 < NU; ++m1)
         static_for<0, NU>([&](auto m1c) {
@@ -665,20 +922,55 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, 2)
 
 template <class Ls>
 cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, bool ps, int fib, int64_t max_ctas,
-                      bool smemc, cudaStream_t st) {
+                      bool smemc, int num_sms, cudaStream_t st) {
   const int64_t ntiles = cnt * Ls::NV * Ls::NW;
-  const unsigned grid = static_cast<unsigned>(max_ctas > 0 && max_ctas < ntiles ? max_ctas : ntiles);
+  // max_ctas > 0: persistent grid of that many CTAs; 0: one CTA per tile; < 0:
+  // persistent, as many CTAs as are resident (occupancy x SMs)
+  auto grid_of = [&](int bps) {
+    const int64_t cap = max_ctas < 0 ? static_cast<int64_t>(bps) * num_sms : max_ctas;
+    return static_cast<unsigned>(cap > 0 && cap < ntiles ? cap : ntiles);
+  };
+  unsigned grid = grid_of(2);
   constexpr int T = Ls::NV * Ls::NW;
   constexpr int F2 = Ls::NV % 2 == 0 ? 2 : 1;
   constexpr size_t cs = sizeof(double) * Ls::ctot(0);
   if constexpr (!Ls::u_conforming() && Ls::NW % 2 == 0) {
+#ifndef P2S_LEAN
+    if (p.pair) {
+      int bps = 0;
+      cudaError_t e = kernel_prepare(large_u_pair_kernel<Ls>, LUPair<Ls>::SMEM, LUPair<Ls>::THREADS, false, &bps);
+      if (e != cudaSuccess) return e;
+      const int64_t nit = (ntiles + LUPair<Ls>::TPC - 1) / LUPair<Ls>::TPC;
+      const int64_t cap = max_ctas < 0 ? static_cast<int64_t>(bps) * num_sms : max_ctas;
+      const unsigned pg = static_cast<unsigned>(cap > 0 && cap < nit ? cap : nit);
+      large_u_pair_kernel<Ls><<<pg, LUPair<Ls>::THREADS, LUPair<Ls>::SMEM, st>>>(p, unit0, ntiles);
+      return cudaGetLastError();
+    }
+    if (p.bulk) {
+      int bps = 0;
+      cudaError_t e = kernel_prepare(large_u_bulk_kernel<Ls>, LUBulk<Ls>::SMEM, T, false, &bps);
+      if (e != cudaSuccess) return e;
+      large_u_bulk_kernel<Ls><<<grid_of(bps), T, LUBulk<Ls>::SMEM, st>>>(p, unit0, ntiles);
+      return cudaGetLastError();
+    }
+#endif
 #ifdef P2S_LEAN
     if (true) {
 #else
     if (ps && fib == 1 && p.xs) {
 #endif
-      cudaError_t e = kernel_prepare(large_u_xs_kernel<Ls>, LUXs<Ls>::SMEM, T);
+      int bps = 0;
+#ifndef P2S_LEAN
+      if (!p.roll) {
+        cudaError_t e = kernel_prepare(large_u_xs_kernel<Ls, false>, LUXs<Ls>::SMEM, T, false, &bps);
+        if (e != cudaSuccess) return e;
+        large_u_xs_kernel<Ls, false><<<grid_of(bps), T, LUXs<Ls>::SMEM, st>>>(p, unit0, ntiles);
+        return cudaGetLastError();
+      }
+#endif
+      cudaError_t e = kernel_prepare(large_u_xs_kernel<Ls>, LUXs<Ls>::SMEM, T, false, &bps);
       if (e != cudaSuccess) return e;
+      grid = grid_of(bps);
       large_u_xs_kernel<Ls><<<grid, T, LUXs<Ls>::SMEM, st>>>(p, unit0, ntiles);
       return cudaGetLastError();
     }
@@ -689,8 +981,12 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
   (void)cs;
   (void)F2;
   (void)ps;
-  if constexpr (Ls::u_conforming() || Ls::NW % 2 != 0)
-    large_u_kernel<Ls, true, 1><<<grid, T, 0, st>>>(p, unit0, ntiles);
+  if constexpr (Ls::u_conforming() || Ls::NW % 2 != 0) {
+    int bps = 0;
+    cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1>, 0, T, false, &bps);
+    if (e != cudaSuccess) return e;
+    large_u_kernel<Ls, true, 1><<<grid_of(bps), T, 0, st>>>(p, unit0, ntiles);
+  }
 #else
   if (ps && smemc && p.cu_g) {
     cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1, true>, cs, T);

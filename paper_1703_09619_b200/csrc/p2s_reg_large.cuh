@@ -112,6 +112,13 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
   std::memcpy(up.cu, pk.cu.data(), sizeof(double) * Ls::cpar(0));
   up.cu_g = pk.d_cu;
   up.xs = pk.u_xs ? 1 : 0;
+  up.roll = pk.u_roll == 0 ? 0 : 1;  // unrolled rows measured slower (c12 0.535 vs 0.583)
+  up.pair = pk.u_pair && (reinterpret_cast<uintptr_t>(M) % 16 == 0) && (ldM % 2 == 0) ? 1 : 0;
+  // bulk stores need 16-B aligned rows: M base, ld_M and N_v N_w even
+  up.bulk = pk.u_bulk && (reinterpret_cast<uintptr_t>(M) % 16 == 0) && (ldM % 2 == 0) &&
+                    ((Ls::NV * Ls::NW) % 2 == 0)
+                ? 1
+                : 0;
   LWParams<Ls> wp;
   wp.Z = pk.d_Z;
   wp.cg = pk.d_cvw + Ls::ctot(1);
@@ -153,7 +160,7 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
     // u stage: absolute units u0 .. u0+cnt-1; Xb holds the chunk
     up.X = Xb;
     up.n_units = cnt;
-    if ((e = large_u_dispatch<Ls>(up, u0, cnt, pk.ps, pk.ufib, pk.u_ctas, pk.u_smemc, us)) != cudaSuccess)
+    if ((e = large_u_dispatch<Ls>(up, u0, cnt, pk.ps, pk.ufib, pk.u_ctas, pk.u_smemc, pk.num_sms, us)) != cudaSuccess)
       return e;
     if (ov && (e = cudaEventRecord(pk.ev_u[b], us)) != cudaSuccess) return e;
   }

@@ -111,6 +111,11 @@ struct LargePack {
   double* d_cu = nullptr;            // device copy of cu (shared-memory / global-memory coefficients)
   double* d_cvw = nullptr;           // device copy of cvw (global-memory coefficients)
   bool u_xs = true;                  // P2S_LARGE_XS: next class staged by cp.async (C5 29.4 k vs 28.4 k)
+  bool u_bulk = false;               // P2S_LARGE_UBULK: u-stage rows written with TMA bulk stores
+                                     // (measured slower: c12 0.56 vs 0.59, C5 0.55 vs 0.65 of HBM)
+  bool u_pair = false;               // P2S_LARGE_UPAIR: two adjacent fibers per u-stage thread
+                                     // (measured slower: c12 0.53 vs 0.58, C5 0.59 vs 0.65 of HBM)
+  int u_roll = 1;                    // P2S_LARGE_UROLL: runtime row loop (1) or unrolled rows (0, slower)
   bool mom_cluster = false;          // P2S_LARGE_MOMCL: one cluster per (unit, term), alpha read once (0.77 vs 0.71 ms: slower)
   bool u_smemc = false;              // P2S_LARGE_USMEM (measured 28.1 k vs 28.4 k elem/s constant-bank)
   // runtime: parity-split u stage; v/w of chunk i+1 on `aux` overlapping u of
@@ -118,7 +123,8 @@ struct LargePack {
   // consecutive chunks alternate between the caller's stream and `aux_u`, so the
   // tail wave of one overlaps the start of the next
   bool ps = true, overlap = true, two_u = true;
-  int64_t u_ctas = 0;  // u-stage grid cap (persistent CTAs; 0: one CTA per tile)
+  int64_t u_ctas = -1;  // u-stage grid: persistent, resident CTAs (-1), k CTAs (> 0), one per tile (0)
+  int num_sms = 148;
   int ufib = 1;  // u-stage fibers per thread (P2S_LARGE_FIB; 2 measured 18 % slower)
   cudaStream_t aux = nullptr, aux_u = nullptr;
   cudaEvent_t ev_start = nullptr, ev_join = nullptr, ev_vw[2]{}, ev_u[2]{};
