@@ -74,7 +74,7 @@ const char* const kOptionKeys[] = {
     "P2S_GEO_MODE",         // geometry fill mode 0 / 1 / 2
     "P2S_XCHUNK_MB",        // large path: intermediate chunk (MB)
     "P2S_LARGE_PS", "P2S_LARGE_OVERLAP", "P2S_LARGE_PRIO", "P2S_LARGE_USTREAMS", "P2S_LARGE_UPERSIST",
-    "P2S_LARGE_XS", "P2S_LARGE_UBULK", "P2S_LARGE_UROLL", "P2S_LARGE_UPAIR", "P2S_LARGE_MOMCL", "P2S_LARGE_USMEM", "P2S_LARGE_FIB",
+    "P2S_LARGE_XS", "P2S_LARGE_UBULK", "P2S_LARGE_UROLL", "P2S_LARGE_UPAIR", "P2S_LARGE_MSPLIT", "P2S_LARGE_MOMCL", "P2S_LARGE_USMEM", "P2S_LARGE_FIB",
     "P2S_CHUNK_MB",         // two-stage scheduler chunk (MB of moments)
     "P2S_TWO_STAGE_OVERLAP", "P2S_MOM_PRIO",
     "P2S_HOST_CHUNK_MB",    // p2s_fill_host ring slot (MB of matrices)
@@ -868,6 +868,11 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
     if (const char* v = opt.get("P2S_LARGE_UBULK")) c->lpack.u_bulk = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_UROLL")) c->lpack.u_roll = v[0] == '1' ? 1 : 0;
     if (const char* v = opt.get("P2S_LARGE_UPAIR")) c->lpack.u_pair = v[0] != '0';
+    if (const char* v = opt.get("P2S_LARGE_MSPLIT")) c->lpack.mom_split = v[0] != '0';
+    if (c->lpack.mom_split) {  // ~24 MB of u-pass scratch: stays in L2 for the v/w passes
+      c->lpack.t1_units = std::max<int64_t>(1, (int64_t(24) << 20) / (lge->t1u * 8));
+      P2S_CUDA(cudaMalloc(&c->lpack.d_T1, sizeof(double) * lge->t1u * c->lpack.t1_units));
+    }
     if (const char* v = opt.get("P2S_LARGE_MOMCL")) c->lpack.mom_cluster = v[0] == '1';
     if (const char* v = opt.get("P2S_LARGE_USMEM")) c->lpack.u_smemc = v[0] == '1';
     if (const char* v = opt.get("P2S_LARGE_FIB")) c->lpack.ufib = std::atoi(v) == 2 ? 2 : 1;
@@ -929,6 +934,7 @@ void p2s_destroy(p2s_ctx* c) {
   if (c->lpack.d_Z) cudaFree(c->lpack.d_Z);
   if (c->lpack.d_cu) cudaFree(c->lpack.d_cu);
   if (c->lpack.d_cvw) cudaFree(c->lpack.d_cvw);
+  if (c->lpack.d_T1) cudaFree(c->lpack.d_T1);
   if (c->lpack.aux) cudaStreamDestroy(c->lpack.aux);
   if (c->lpack.aux_u) cudaStreamDestroy(c->lpack.aux_u);
   if (c->lpack.ev_start) cudaEventDestroy(c->lpack.ev_start);

@@ -288,6 +288,119 @@ __global__ void __launch_bounds__(P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM <= 110 * 1
   });
 }
 
+// Split moments (default): the u pass of every (unit, term) computes ALL its
+// K_u outputs per alpha row at once -- each row is read and folded once, 18 FMAs
+// per k1 against 36 loaded values instead of 4 k1 per pass -- into a
+// k1-major scratch T1g [K_u][Q_w][Q_v] (L2-resident: the launcher walks the
+// batch in sub-batches); then one CTA per (unit, term, k1 chunk) loads its T1
+// rows into shared memory and runs the v and w passes as above.  (The fused
+// per-chunk kernel re-read and re-folded every alpha row once per k1 chunk:
+// 0.33 of the FP64 peak on C5.)
+template <class Ls>
+struct LMomSplit {
+  static constexpr int QU = Ls::Q(0), QV = Ls::Q(1), QW = Ls::Q(2);
+  static constexpr int64_t T1U = static_cast<int64_t>(Ls::KMAX(0)) * QW * QV;  // per (unit, term)
+  static constexpr int ROWS = 128;  // alpha rows (threads) per u-pass CTA
+  static constexpr size_t VW_SMEM = Ls::MOM_SMEM;
+};
+
+template <class Ls>
+__global__ void __launch_bounds__(LMomSplit<Ls>::ROWS)
+    large_mom_u_kernel(const __grid_constant__ LMomParams<Ls> p, double* __restrict__ T1g, int64_t ut0) {
+  constexpr int QU = Ls::Q(0), QV = Ls::Q(1), QW = Ls::Q(2), S = Ls::S;
+  constexpr int RB = (QW * QV + LMomSplit<Ls>::ROWS - 1) / LMomSplit<Ls>::ROWS;  // row blocks per (unit, term)
+  const int64_t ut = blockIdx.x / RB;                 // (unit, term) within the sub-batch
+  const int r = static_cast<int>(blockIdx.x % RB) * LMomSplit<Ls>::ROWS + threadIdx.x;
+  if (r >= QW * QV) return;
+  const int s = static_cast<int>((ut0 + ut) % S);
+  constexpr int slab = QU * QV * QW;
+  double x[QU];
+  load_row<QU>(p.alpha + (ut0 + ut) * slab + static_cast<int64_t>(r) * QU, x);
+  constexpr int Hf = QU / 2, H = (QU + 1) / 2;
+  double ev[Hf > 0 ? Hf : 1], od[Hf > 0 ? Hf : 1];
+#pragma unroll
+  for (int h = 0; h < Hf; ++h) {
+    ev[h] = x[h] + x[QU - 1 - h];
+    od[h] = x[h] - x[QU - 1 - h];
+  }
+  const double* tu = p.tab + Ls::ttoff(0);
+  double* out = T1g + ut * LMomSplit<Ls>::T1U + r;
+  static_for<0, S>([&](auto sc) {
+    constexpr int ss = decltype(sc)::value;
+    if (s == ss) {
+#pragma unroll 4
+      for (int k = 0; k < Ls::K(ss, 0); ++k) {
+        double v = 0.0;
+        if (k & 1) {
+#pragma unroll
+          for (int h = 0; h < Hf; ++h) v = fma(tu[k * H + h], od[h], v);
+        } else {
+#pragma unroll
+          for (int h = 0; h < Hf; ++h) v = fma(tu[k * H + h], ev[h], v);
+          if constexpr (QU & 1) v = fma(tu[k * H + Hf], x[Hf], v);
+        }
+        __stcg(out + static_cast<int64_t>(k) * QW * QV, v);  // L2: read back by the v/w pass
+      }
+    }
+  });
+}
+
+template <class Ls, int s>
+__device__ __forceinline__ void large_mom_vw_term(const LMomParams<Ls>& p, const double* T1u, double* Iout,
+                                                  int chunk, double* sm) {
+  constexpr int QV = Ls::Q(1), QW = Ls::Q(2);
+  constexpr int KU = Ls::K(s, 0), KV = Ls::K(s, 1), KW = Ls::K(s, 2), KC = Ls::KC;
+  constexpr int S2 = Ls::S2, S3 = Ls::S3;
+  constexpr int NT = P2S_LARGE_MOM_THREADS;
+  const int k0 = chunk * KC;
+  if (k0 >= KU) return;
+  double* T1 = sm;                         // [KC][QW][S2]
+  double* T2 = sm + KC * QW * S2;          // [KC*KV][S3]
+  const int nrow = (KU - k0 < KC ? KU - k0 : KC) * QW * QV;
+  const double* src = T1u + static_cast<int64_t>(k0) * QW * QV;
+  for (int i = threadIdx.x; i < nrow; i += NT) {
+    const int jq = i / QV, q2 = i - (i / QV) * QV;
+    T1[jq * S2 + q2] = __ldcg(src + i);
+  }
+  __syncthreads();
+  const double* tv = p.tab + Ls::ttoff(1);
+  for_items<KC * QW, NT>([&](int r) {
+    const int j = r / QW, q3 = r - (r / QW) * QW;
+    double x[QV];
+#pragma unroll
+    for (int q = 0; q < QV; ++q) x[q] = T1[(j * QW + q3) * S2 + q];
+    fold_contract<QV, KV>(x, tv, [&](int k, double v) { T2[(j * KV + k) * S3 + q3] = v; });
+  });
+  __syncthreads();
+  const double* tw = p.tab + Ls::ttoff(2);
+  for_items<KC * KV, NT>([&](int r) {
+    const int j = r / KV, k2 = r - (r / KV) * KV;
+    if (k0 + j >= KU) return;
+    double x[QW];
+#pragma unroll
+    for (int q = 0; q < QW; ++q) x[q] = T2[(j * KV + k2) * S3 + q];
+    double* out = Iout + ((k0 + j) * KV + k2) * KW;
+    fold_contract<QW, KW>(x, tw, [&](int k, double v) { out[k] = v; });
+  });
+}
+
+template <class Ls>
+__global__ void __launch_bounds__(P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM <= 110 * 1024 ? P2S_LARGE_MOM_MINB : 1)
+    large_mom_vw_kernel(const __grid_constant__ LMomParams<Ls> p, const double* __restrict__ T1g, int64_t ut0) {
+  extern __shared__ __align__(16) double sm[];
+  const int64_t b = blockIdx.x;
+  const int chunk = static_cast<int>(b % Ls::NCH);
+  const int64_t ut = b / Ls::NCH;
+  const int64_t us = ut0 + ut;                    // global (unit, term)
+  const int s = static_cast<int>(us % Ls::S);
+  const int64_t unit = us / Ls::S;
+  double* Ib = p.I + unit * Ls::MPP;
+  static_for<0, Ls::S>([&](auto sc) {
+    constexpr int ss = decltype(sc)::value;
+    if (s == ss) large_mom_vw_term<Ls, ss>(p, T1g + ut * LMomSplit<Ls>::T1U, Ib + Ls::moff(ss), chunk, sm);
+  });
+}
+
 // ------------------------------------------------------------------ v/w stage
 // Two steps, both "fiber in registers, compile-time bands, constant-bank
 // coefficients, coalesced stores" kernels:

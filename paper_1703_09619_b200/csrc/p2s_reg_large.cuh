@@ -72,6 +72,22 @@ cudaError_t launch_large_moments(const double* alpha, double* I, int64_t n_units
   cudaError_t e = kernel_prepare(large_moments_kernel<Ls>, Ls::MOM_SMEM, P2S_LARGE_MOM_THREADS);
   if (e != cudaSuccess) return e;
   const unsigned grid = static_cast<unsigned>(n_units * Ls::S * Ls::NCH);
+  if (pk.mom_split && pk.d_T1) {
+    // split moments: u pass (all k1 per alpha row) into the L2-resident T1
+    // scratch, then v/w passes per k1 chunk, over sub-batches of (unit, term)s
+    if ((e = kernel_prepare(large_mom_vw_kernel<Ls>, Ls::MOM_SMEM, P2S_LARGE_MOM_THREADS)) != cudaSuccess) return e;
+    constexpr int RB = (Ls::Q(1) * Ls::Q(2) + LMomSplit<Ls>::ROWS - 1) / LMomSplit<Ls>::ROWS;
+    const int64_t total = n_units * Ls::S;
+    for (int64_t u0 = 0; u0 < total; u0 += pk.t1_units) {
+      const int64_t cnt = std::min(pk.t1_units, total - u0);
+      large_mom_u_kernel<Ls><<<static_cast<unsigned>(cnt * RB), LMomSplit<Ls>::ROWS, 0, st>>>(p, pk.d_T1, u0);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      large_mom_vw_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::NCH), P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM, st>>>(
+          p, pk.d_T1, u0);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
 #ifndef P2S_LEAN
   if constexpr (Ls::Q(0) % 2 == 0 && Ls::NCH <= 8)
   if (pk.mom_cluster) {
@@ -186,6 +202,7 @@ LargeEntry make_large() {
   r.moments = &launch_large_moments<Ls>;
   r.contract = &launch_large_contract<Ls>;
   r.mpp = Ls::MPP;
+  r.t1u = LMomSplit<Ls>::T1U;
   r.xpu = Ls::XPU;
   r.zpu = Ls::ZPU;
   return r;

@@ -110,6 +110,10 @@ struct LargePack {
   double* d_Z = nullptr;             // w-step output of one chunk (ZPU x xchunk doubles)
   double* d_cu = nullptr;            // device copy of cu (shared-memory / global-memory coefficients)
   double* d_cvw = nullptr;           // device copy of cvw (global-memory coefficients)
+  double* d_T1 = nullptr;            // split moments: u-pass output of a sub-batch (L2-resident)
+  int64_t t1_units = 0;              // (unit, term)s per sub-batch
+  bool mom_split = false;            // P2S_LARGE_MSPLIT: split moment stage (u pass / v-w passes;
+                                     // measured C5 1.33 vs 1.27 us/elem: the v/w passes dominate)
   bool u_xs = true;                  // P2S_LARGE_XS: next class staged by cp.async (C5 29.4 k vs 28.4 k)
   bool u_bulk = false;               // P2S_LARGE_UBULK: u-stage rows written with TMA bulk stores
                                      // (measured slower: c12 0.56 vs 0.59, C5 0.55 vs 0.65 of HBM)
@@ -144,11 +148,12 @@ struct LargeEntry {
   large_mom_fn moments;
   large_con_fn contract;
   int64_t mpp, xpu, zpu;
+  int64_t t1u;  // split moments: T1 scratch per (unit, term), doubles
 };
 
 // Registry entries of one generated per-shape module (p2s_jit.cu,
 // p2s_jit_module.cuh); kJitAbi changes whenever these structs change.
-constexpr int kJitAbi = 3;
+constexpr int kJitAbi = 4;
 struct JitEntries {
   int abi, family;   // family: 1 fused (+ two-stage entries of the shape), 2 large
   FusedEntry fused;
