@@ -134,7 +134,9 @@ def cpu_baseline(cfg, seconds: float, seed: int, threads: int, batch: int = 0, e
     import numpy as np
 
     from oracle import oracle as O
-    o = O.Oracle(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq)
+    # liboracle_fast.so: the oracle's source built with FMA contraction and
+    # unrolling (oracle/Makefile FASTFLAGS) -- the checker build stays strict
+    o = O.Oracle(cfg.n_comp, cfg.order, list(cfg.kinds), cfg.nq, fast=True)
     batch = batch or max(threads, min(256, int(2e9 // (8 * o.n_tot * o.n_tot))))
     out = np.empty((batch, o.n_tot, o.n_tot))
     done, elapsed = 0, 0.0
@@ -174,8 +176,8 @@ def run_reference(args, cfg):
         "cpu_baseline": {"value": value, "unit": "elem/s", "cores": threads, "kind": "port",
                          "cpu_model": cpu_model(),
                          "sample": f"~{sample} {cfg.name} elements per step (>= {secs:.0f} s of "
-                                   f"moments + banded contraction, oracle/p2s_oracle.c, "
-                                   f"{threads} threads)"},
+                                   f"moments + banded contraction, oracle/p2s_oracle.c built -O3 -mavx2 "
+                                   f"-mfma -ffp-contract=fast, {threads} threads)"},
         "e2e": {"value": value, "unit": "elem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -533,7 +535,8 @@ def run_b200(args, cfg):
         line["cpu_baseline"] = {"value": rate, "unit": "elem/s", "cores": threads, "kind": "port",
                                 "cpu_model": cpu_model(), "value_1thread": rate1,
                                 "sample": f"{n} {cfg.name} elements, {dt:.1f} s (moments + banded "
-                                          f"contraction, oracle/p2s_oracle.c, {threads} threads); 1 thread: "
+                                          f"contraction, oracle/p2s_oracle.c built -O3 -mavx2 -mfma "
+                                          f"-ffp-contract=fast, {threads} threads); 1 thread: "
                                           f"{n1} elements, {dt1:.1f} s"}
         if args.config == "c2" and not args.no_subconfigs:
             line["cpu_baseline"]["c5_direct_ablation"] = c5_direct_sample(args.seed)

@@ -16,6 +16,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# the same source built for speed (-ffp-contract=fast, FMA): CPU-baseline timing
+# only (bench.py), never the checker
+_LIB_FAST_PATH = os.path.join(_HERE, "liboracle_fast.so")
 
 PP, DD, DP, PD = 0, 1, 2, 3
 ALPHA_SINE, ALPHA_JACOBIAN, ALPHA_EXPSIN = 0, 1, 2
@@ -24,8 +27,8 @@ MAX_TERMS = 4
 
 
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with oracle/Makefile (gcc)."""
-    if force or not os.path.exists(_LIB_PATH):
+    """Compile liboracle.so (and liboracle_fast.so) with oracle/Makefile (gcc)."""
+    if force or not os.path.exists(_LIB_PATH) or not os.path.exists(_LIB_FAST_PATH):
         subprocess.run(["make", "-C", _HERE, "-s"], check=True)
     return _LIB_PATH
 
@@ -41,14 +44,13 @@ class Problem(C.Structure):
     ]
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(fast: bool = False):
+    if fast not in _libs:
         build()
-        L = C.CDLL(_LIB_PATH)
+        L = C.CDLL(_LIB_FAST_PATH if fast else _LIB_PATH)
         dp = C.POINTER(C.c_double)
         ip = C.POINTER(C.c_int)
         L.por_gauss_legendre.argtypes = [C.c_int, dp, dp]
@@ -93,8 +95,8 @@ def lib():
         L.por_cheb_p2s.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, ip, ip]
         L.por_cheb_p2s.restype = C.c_int
         L.por_cheb2d_element.argtypes = [C.c_int, C.c_int, C.c_int, dp, dp, dp, dp, dp, dp, dp, dp]
-        _lib = L
-    return _lib
+        _libs[fast] = L
+    return _libs[fast]
 
 
 def _dp(a: np.ndarray):
@@ -194,7 +196,8 @@ def conforming_matrix(n):
 class Oracle:
     """3-D Legendre p2s problem on the CPU oracle."""
 
-    def __init__(self, n_comp, order, kinds, nq, basis=0):
+    def __init__(self, n_comp, order, kinds, nq, basis=0, fast=False):
+        self._L = lib(fast)
         pb = Problem()
         pb.basis = basis
         pb.n_comp = n_comp
@@ -211,56 +214,56 @@ class Oracle:
         self.order = tuple(order)
         self.kinds = [tuple(k) if isinstance(k, (tuple, list)) else (k, k, k) for k in kinds]
         self.nq = tuple(nq)
-        self.h = lib().por_create(C.byref(pb))
+        self.h = self._L.por_create(C.byref(pb))
         if not self.h:
             raise ValueError("oracle: invalid problem")
-        L = lib()
+        L = self._L
         self.alpha_per_elem = L.por_alpha_per_elem(self.h)
         self.moments_per_elem = L.por_moments_per_elem(self.h)
         self.n_tot = L.por_n_tot(self.h)
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().por_destroy(self.h)
+            self._L.por_destroy(self.h)
             self.h = None
 
     def K(self, term, d):
-        return lib().por_K(self.h, term, d)
+        return self._L.por_K(self.h, term, d)
 
     def moment_offset(self, pair, term):
-        return lib().por_moment_offset(self.h, pair, term)
+        return self._L.por_moment_offset(self.h, pair, term)
 
     def nodes(self, d):
-        return np.ctypeslib.as_array(lib().por_nodes(self.h, d), shape=(self.nq[d],)).copy()
+        return np.ctypeslib.as_array(self._L.por_nodes(self.h, d), shape=(self.nq[d],)).copy()
 
     def weights(self, d):
-        return np.ctypeslib.as_array(lib().por_weights(self.h, d), shape=(self.nq[d],)).copy()
+        return np.ctypeslib.as_array(self._L.por_weights(self.h, d), shape=(self.nq[d],)).copy()
 
     def phi(self, term, d):
         K = self.K(term, d)
-        return np.ctypeslib.as_array(lib().por_phi(self.h, term, d), shape=(K, self.nq[d])).copy()
+        return np.ctypeslib.as_array(self._L.por_phi(self.h, term, d), shape=(K, self.nq[d])).copy()
 
     def coef(self, term, d):
         K, N = self.K(term, d), self.order[d]
-        return np.ctypeslib.as_array(lib().por_coef(self.h, term, d), shape=(N, N, K)).copy()
+        return np.ctypeslib.as_array(self._L.por_coef(self.h, term, d), shape=(N, N, K)).copy()
 
     def alpha(self, kind, lo, hi, seed, e0, n):
         a = np.zeros(n * self.alpha_per_elem)
-        lib().por_alpha_gen(self.h, kind, lo, hi, seed, e0, n, _dp(a))
+        self._L.por_alpha_gen(self.h, kind, lo, hi, seed, e0, n, _dp(a))
         return a.reshape(n, self.alpha_per_elem)
 
     def moments(self, alpha, threads=1):
         alpha = np.ascontiguousarray(alpha, dtype=np.float64)
         n = alpha.size // self.alpha_per_elem
         out = np.zeros((n, self.moments_per_elem))
-        lib().por_moments(self.h, _dp(alpha), n, _dp(out), threads)
+        self._L.por_moments(self.h, _dp(alpha), n, _dp(out), threads)
         return out
 
     def contract(self, I, threads=1):
         I = np.ascontiguousarray(I, dtype=np.float64)
         n = I.size // self.moments_per_elem
         out = np.zeros((n, self.n_tot, self.n_tot))
-        lib().por_contract(self.h, _dp(I), n, _dp(out), self.n_tot, threads)
+        self._L.por_contract(self.h, _dp(I), n, _dp(out), self.n_tot, threads)
         return out
 
     def fill(self, alpha, threads=1, out=None):
@@ -268,14 +271,14 @@ class Oracle:
         n = alpha.size // self.alpha_per_elem
         if out is None:
             out = np.zeros((n, self.n_tot, self.n_tot))
-        lib().por_fill(self.h, _dp(alpha), n, _dp(out), self.n_tot, threads)
+        self._L.por_fill(self.h, _dp(alpha), n, _dp(out), self.n_tot, threads)
         return out
 
     def direct(self, alpha, threads=1):
         alpha = np.ascontiguousarray(alpha, dtype=np.float64)
         n = alpha.size // self.alpha_per_elem
         out = np.zeros((n, self.n_tot, self.n_tot))
-        lib().por_direct(self.h, _dp(alpha), n, _dp(out), self.n_tot, threads)
+        self._L.por_direct(self.h, _dp(alpha), n, _dp(out), self.n_tot, threads)
         return out
 
 
@@ -287,7 +290,7 @@ def direct_sample_seconds(orc, alpha_elem, m1_lo, m1_hi):
     M = np.zeros((orc.n_tot, orc.n_tot))
     tot = C.c_long(0)
     t0 = time.perf_counter()
-    cov = lib().por_direct_sample(orc.h, _dp(a), m1_lo, m1_hi, _dp(M), orc.n_tot, C.byref(tot))
+    cov = orc._L.por_direct_sample(orc.h, _dp(a), m1_lo, m1_hi, _dp(M), orc.n_tot, C.byref(tot))
     return time.perf_counter() - t0, cov, tot.value
 
 
