@@ -235,6 +235,22 @@ p2s_status p2s_scatter_add(const double* d_elem, int64_t elem_stride, int64_t ld
                            const int32_t* d_dof_free, const double* d_dof_sign, int64_t n_elem,
                            double* d_G, int64_t ld_G, void* stream);
 
+/* Deterministic scatter: the reference's summation order (elements ascending,
+ * then local row; assembly.cpp:626-641) and arithmetic (G += (s_i s_j) E, no
+ * FMA contraction), so G equals the reference's serial sum bit for bit.  The plan
+ * (per global row, its (element, local row) contributions in that order) is
+ * built once per mesh from the HOST copy of the free-index map
+ * h_dof_free[n_elem][n_local]; the device copy passed to the scatter calls must
+ * hold the same values.  One CTA per global row, no atomics.  Requires that no
+ * element lists one free index twice. */
+typedef struct p2s_scatter_plan p2s_scatter_plan;
+p2s_status p2s_scatter_plan_create(const int32_t* h_dof_free, int64_t n_elem, int32_t n_local, int32_t n_free,
+                                   int device, p2s_scatter_plan** out);
+void p2s_scatter_plan_destroy(p2s_scatter_plan* plan);
+p2s_status p2s_scatter_add_ordered(const p2s_scatter_plan* plan, const double* d_elem, int64_t elem_stride,
+                                   int64_t ld_elem, const int32_t* d_dof_free, const double* d_dof_sign,
+                                   double* d_G, int64_t ld_G, void* stream);
+
 /* 1 if p2s_create accepts the problem here: an ahead-of-time kernel, or a
  * generated module that is cached or can be compiled (nvcc present). */
 int p2s_shape_supported(const p2s_problem* spec);
@@ -294,6 +310,11 @@ p2s_status p2s_cheb2d_scatter(const p2s_cheb2d_ctx* ctx, const double* d_blocks,
                               int64_t ld_G, void* stream);
 p2s_status p2s_cheb2d_assemble(p2s_cheb2d_ctx* ctx, const double* d_tables, double* d_blocks,
                                int64_t n_elem, void* stream);
+/* p2s_cheb2d_scatter in the reference's summation order, bit for bit (plan from
+ * p2s_scatter_plan_create with n_local = n_eu + n_ev). */
+p2s_status p2s_cheb2d_scatter_ordered(const p2s_cheb2d_ctx* ctx, const p2s_scatter_plan* plan,
+                                      const double* d_blocks, const int32_t* d_dof_free, const double* d_dof_sign,
+                                      double* d_S, double* d_M, int64_t ld_G, void* stream);
 
 #ifdef __cplusplus
 }

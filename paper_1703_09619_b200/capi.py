@@ -32,7 +32,9 @@ EXPORTS = ("p2s_create", "p2s_destroy", "p2s_get_sizes", "p2s_moments", "p2s_con
            "p2s_direct_create", "p2s_direct_destroy", "p2s_direct_fill",
            "p2s_scatter_add", "p2s_cheb2d_scatter",
            "p2s_geometry_generate", "p2s_alpha_from_geometry", "p2s_fill_geometry",
-           "p2s_create_ex", "p2s_shape_prepare", "p2s_jit_cache_dir", "p2s_problem_sizes")
+           "p2s_create_ex", "p2s_shape_prepare", "p2s_jit_cache_dir", "p2s_problem_sizes",
+           "p2s_scatter_plan_create", "p2s_scatter_plan_destroy", "p2s_scatter_add_ordered",
+           "p2s_cheb2d_scatter_ordered")
 
 
 class P2SError(RuntimeError):
@@ -151,9 +153,14 @@ def lib():
         L.p2s_fill_geometry.argtypes = [vp, vp, vp, i64, i64, vp]
         L.p2s_scatter_add.argtypes = [vp, i64, i64, C.c_int32, vp, vp, i64, vp, i64, vp]
         L.p2s_cheb2d_scatter.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp]
+        L.p2s_scatter_plan_create.argtypes = [vp, i64, C.c_int32, C.c_int32, C.c_int, C.POINTER(vp)]
+        L.p2s_scatter_plan_destroy.argtypes = [vp]
+        L.p2s_scatter_plan_destroy.restype = None
+        L.p2s_scatter_add_ordered.argtypes = [vp, vp, i64, i64, vp, vp, vp, i64, vp]
+        L.p2s_cheb2d_scatter_ordered.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, vp]
         for f in EXPORTS:
             if f not in ("p2s_destroy", "p2s_shape_supported", "p2s_last_error", "p2s_version",
-                         "p2s_jit_cache_dir",
+                         "p2s_jit_cache_dir", "p2s_scatter_plan_destroy",
                          "p2s_kernel_path", "p2s_cheb2d_destroy", "p2s_direct_destroy"):
                 getattr(L, f).restype = C.c_int
         _lib = L
@@ -384,6 +391,11 @@ class Cheb2dContext:
         _check(lib().p2s_cheb2d_assemble(self.h, _ptr(d_tables), _ptr(d_blocks), n_elem,
                                          _ptr(stream)))
 
+    def scatter_ordered(self, plan, d_blocks, d_dof_free, d_dof_sign, d_S, d_M, ld_G, stream=0):
+        """p2s_cheb2d_scatter_ordered: the reference's summation order, bit for bit."""
+        _check(lib().p2s_cheb2d_scatter_ordered(self.h, plan.h, _ptr(d_blocks), _ptr(d_dof_free),
+                                                _ptr(d_dof_sign), _ptr(d_S), _ptr(d_M), ld_G, _ptr(stream)))
+
     def scatter(self, d_blocks, d_dof_free, d_dof_sign, n_elem, d_S, d_M, ld_G, stream=0):
         """assemble_global (assembly.cpp:594-652) from the eight blocks, on the device."""
         _check(lib().p2s_cheb2d_scatter(self.h, _ptr(d_blocks), _ptr(d_dof_free), _ptr(d_dof_sign),
@@ -433,3 +445,33 @@ def scatter_add(d_elem, elem_stride, ld_elem, n_local, d_dof_free, d_dof_sign, n
     assembly.cpp:594-652) on the device."""
     _check(lib().p2s_scatter_add(_ptr(d_elem), elem_stride, ld_elem, n_local, _ptr(d_dof_free),
                                  _ptr(d_dof_sign), n_elem, _ptr(d_G), ld_G, _ptr(stream)))
+
+
+class ScatterPlan:
+    """p2s_scatter_plan: per global row, the (element, local row) contributions in
+    the reference's order (assemble_global, assembly.cpp:626-641), from the host
+    free-index map dof_free[n_elem][n_local] (numpy int32)."""
+
+    def __init__(self, dof_free, n_free: int, device: int = 0):
+        import numpy as np
+        f = np.ascontiguousarray(dof_free, dtype=np.int32)
+        self.n_elem, self.n_local = f.shape
+        self.n_free = n_free
+        h = C.c_void_p()
+        _check(lib().p2s_scatter_plan_create(f.ctypes.data, self.n_elem, self.n_local, n_free, device, C.byref(h)))
+        self.h = h
+
+    def add(self, d_elem, elem_stride, ld_elem, d_dof_free, d_dof_sign, d_G, ld_G, stream=0):
+        _check(lib().p2s_scatter_add_ordered(self.h, _ptr(d_elem), elem_stride, ld_elem, _ptr(d_dof_free),
+                                             _ptr(d_dof_sign), _ptr(d_G), ld_G, _ptr(stream)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().p2s_scatter_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

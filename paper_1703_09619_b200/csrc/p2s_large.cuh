@@ -484,7 +484,7 @@ __device__ __forceinline__ void large_w_row(const LWParams<Ls>& p, const double*
 // the group) in lockstep -- constant-cache hits.  (Mapping the groups to the
 // warps of one row instead put 8 different coefficient regions of the N = 16
 // table (26 KB) on an SM at once: LDCU misses, 4 % issue.)
-constexpr int kLargeWWarps = 4;  // 4 warps (128 threads): a w-step CTA fits beside the u stage's CTAs on an SM
+constexpr int kLargeWWarps = 8;
 
 template <class Ls>
 __global__ void __launch_bounds__(32 * kLargeWWarps) large_w_kernel(const __grid_constant__ LWParams<Ls> p) {
