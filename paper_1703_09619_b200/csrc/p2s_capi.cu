@@ -664,6 +664,11 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
   const FusedEntry* fe = force_jit ? nullptr : find_fused(*spec, opt);
   const MV2Entry* mv2e = force_jit ? nullptr : find_mv2(*spec, opt);
   const bool want_generic = flag("P2S_FORCE_GENERIC") && entry;
+  // a registered contraction whose moment kernel is registered for other nq
+  // would pair with the runtime-shaped moments_kernel (0.18-0.69 of HBM on the
+  // coverage grid): a generated module instantiates both for this shape instead
+  if (v2e && !mv2e && !fe && !no_jit && !want_generic && !opt.get("P2S_NO_FUSED") && !opt.get("P2S_V2_VARIANT"))
+    v2e = nullptr;
   // shapes without a shape-specialised kernel: a generated module (p2s_jit.cu)
   const reg::JitEntries* je = nullptr;
   std::string jit_desc;

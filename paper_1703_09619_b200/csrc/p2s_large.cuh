@@ -501,13 +501,24 @@ __global__ void __launch_bounds__(32 * kLargeWWarps) large_w_kernel(const __grid
   });
 }
 
+// v-step CTA: VR consecutive (unit, k1) rows of N_w^2 threads each (>= 128
+// threads: small N_w would otherwise launch CTAs of a few threads)
 template <class Ls>
-__global__ void __launch_bounds__(Ls::NW * Ls::NW) large_v_kernel(const __grid_constant__ LVParams<Ls> p) {
+struct LVRows {
+  static constexpr int F = Ls::NW * Ls::NW;
+  static constexpr int VR = F >= 128 ? 1 : (128 + F - 1) / F;
+};
+
+template <class Ls>
+__global__ void __launch_bounds__(LVRows<Ls>::VR * Ls::NW * Ls::NW) large_v_kernel(const __grid_constant__ LVParams<Ls> p) {
   constexpr int NV = Ls::NV, NW = Ls::NW, NQV = Ls::NQV, K2P = Ls::K2P;
-  const int64_t b = blockIdx.x;
+  constexpr int F = LVRows<Ls>::F;
+  const int rl = LVRows<Ls>::VR == 1 ? 0 : static_cast<int>(threadIdx.x) / F;
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * LVRows<Ls>::VR + rl;
   const int row = static_cast<int>(b % Ls::KUTOT());
   const int64_t unit = b / Ls::KUTOT();
-  const int t = threadIdx.x;  // p1 * N_w + p2
+  if (unit >= p.n_units) return;
+  const int t = static_cast<int>(threadIdx.x) - rl * F;  // p1 * N_w + p2
   static_for<0, Ls::S>([&](auto sc) {
     constexpr int s = decltype(sc)::value;
     constexpr int KV = Ls::K(s, 1), kv = Ls::kind(s, 1);
@@ -559,13 +570,13 @@ struct LUParams {
 // DFMAs (half the LDCU per DFMA at FIB = 2, 3 CTAs of 128 threads per SM).
 template <class Ls, bool PS, int FIB, bool SMEMC>
 __device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, const double* cus, int64_t unit0,
-                                             int64_t b) {
+                                             int64_t b, int tid) {
   constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S, NQV = Ls::NQV;
   static_assert(NV % FIB == 0, "fibers per thread must divide N_v");
   const int np = static_cast<int>(b % (NV * NW));
   const int64_t unit = unit0 + b / (NV * NW);
   const int n1 = np / NW, p1 = np - (np / NW) * NW;
-  const int n2b = threadIdx.x / NW, p2 = threadIdx.x - (threadIdx.x / NW) * NW;
+  const int n2b = tid / NW, p2 = tid - (tid / NW) * NW;
   const int64_t e = unit / p.P;
   const int pair = static_cast<int>(unit - e * p.P);
   const int gci = pair / p.nc, gcj = pair - gci * p.nc;
@@ -655,18 +666,35 @@ __device__ __forceinline__ void large_u_tile(const LUParams<Ls>& p, const double
 // SMEMC: the coefficients are copied once per (persistent) CTA from global memory
 // into shared memory (coalesced) and read as uniform-address LDS; else they are
 // constant-bank operands (LDCU).
+// tiles per CTA of the plain u stage (one fiber per thread): as LUXs
+template <class Ls, int FIB>
+struct LUPlain {
+  static constexpr int T = Ls::NV * Ls::NW / FIB;
+  static constexpr int TPC = (FIB == 1 && T < 128) ? (128 + T - 1) / T : 1;
+  static constexpr int THREADS = TPC * T;
+  static constexpr int MINB = THREADS <= 96 ? 4 : THREADS <= 170 ? 3 : THREADS <= 256 ? 2 : 1;
+};
+
 template <class Ls, bool PS, int FIB, bool SMEMC = false>
-__global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? Ls::UMINB : P2S_LARGE_FIB2_MINB) : 1)
+__global__ void __launch_bounds__(LUPlain<Ls, FIB>::THREADS,
+                                  PS ? (FIB == 1 ? LUPlain<Ls, FIB>::MINB : P2S_LARGE_FIB2_MINB) : 1)
     large_u_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
   extern __shared__ __align__(16) double cus[];
   if constexpr (SMEMC) {
     for (int i = threadIdx.x; i < Ls::ctot(0); i += blockDim.x) cus[i] = __ldg(p.cu_g + i);
     __syncthreads();
   }
-  // one (unit, n1, p1) tile per CTA, or a grid-stride loop over the tiles when the
-  // grid is smaller (persistent CTAs: P2S_LARGE_UPERSIST CTAs per SM)
+  // TPC tiles per CTA iteration (group g = tile it * TPC + g), grid-stride over the
+  // iterations when the grid is smaller (persistent CTAs); tiles are independent
+  constexpr int T = LUPlain<Ls, FIB>::T, TPC = LUPlain<Ls, FIB>::TPC;
+  const int g = TPC == 1 ? 0 : static_cast<int>(threadIdx.x) / T;
+  const int tid = static_cast<int>(threadIdx.x) - g * T;
+  const int64_t nit = (ntiles + TPC - 1) / TPC;
 #pragma unroll 1
-  for (int64_t b = blockIdx.x; b < ntiles; b += gridDim.x) large_u_tile<Ls, PS, FIB, SMEMC>(p, cus, unit0, b);
+  for (int64_t it = blockIdx.x; it < nit; it += gridDim.x) {
+    const int64_t b = it * TPC + g;
+    if (b < ntiles) large_u_tile<Ls, PS, FIB, SMEMC>(p, cus, unit0, b, tid);
+  }
 }
 
 // XS mode (persistent, parity split, one fiber per thread): each thread's x
@@ -677,18 +705,23 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW / FIB, PS ? (FIB == 1 ? Ls::UM
 // warp ran at 21.4 k elem/s vs 28.5 k: the TMA engine is slow on tiny copies.)
 template <class Ls>
 struct LUXs {
-  static constexpr int NV = Ls::NV, NW = Ls::NW;
+  static constexpr int NV = Ls::NV, NW = Ls::NW, T = NV * NW;
   static constexpr int KXM = Ls::KX(0) > Ls::KX(1) ? Ls::KX(0) : Ls::KX(1);
-  static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(KXM) * NV * NW + 16;
+  // tiles per CTA: a tile has only N_v N_w fibers (threads); anisotropic shapes
+  // with few (e.g. 17 x 3) would run 2-warp CTAs at a few CTAs per SM, so a CTA
+  // takes TPC consecutive tiles (>= 128 threads; 1 for c12 / C5)
+  static constexpr int TPC = T >= 128 ? 1 : (128 + T - 1) / T;
+  static constexpr int THREADS = TPC * T;
+  static constexpr int MINB = THREADS <= 96 ? 4 : THREADS <= 170 ? 3 : THREADS <= 256 ? 2 : 1;
+  static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(KXM) * T * TPC + 16;
 };
 
 // Per-thread asynchronous copy (cp.async, 8 bytes) of the thread's own x values
 // of one parity class of tile b into its shared-memory slots xbuf[j][tid].
 template <class Ls>
 __device__ __forceinline__ void large_u_xs_issue(const LUParams<Ls>& p, int64_t unit0, int64_t b, int cls,
-                                                 double* xbuf) {
+                                                 double* xbuf, int tid) {
   constexpr int NV = Ls::NV, NW = Ls::NW, NQV = Ls::NQV, S = Ls::S;
-  const int tid = threadIdx.x;
   const int np = static_cast<int>(b % (NV * NW));
   const int64_t unit = unit0 + b / (NV * NW);
   const int n1 = np / NW, p1 = np - (np / NW) * NW;
@@ -716,20 +749,31 @@ __device__ __forceinline__ void large_u_xs_issue(const LUParams<Ls>& p, int64_t 
 }
 
 template <class Ls, bool ROLL = true>
-__global__ void __launch_bounds__(Ls::NV * Ls::NW, Ls::UMINB)
+__global__ void __launch_bounds__(LUXs<Ls>::THREADS, LUXs<Ls>::MINB)
     large_u_xs_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
-  constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S;
+  constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S, T = NV * NW, TPC = LUXs<Ls>::TPC;
   static_assert(NW % 2 == 0, "bulk-copy rows must be 16-byte multiples");
-  extern __shared__ __align__(128) double xbuf[];
-  const int tid = threadIdx.x;
-  int64_t b = blockIdx.x;
-  if (b >= ntiles) return;
-  large_u_xs_issue<Ls>(p, unit0, b, 0, xbuf);
+  extern __shared__ __align__(128) double xsm[];
+  // thread group g of the CTA works on tile it * TPC + g; tid = its fiber (n2, p2)
+  const int g = TPC == 1 ? 0 : static_cast<int>(threadIdx.x) / T;
+  const int tid = static_cast<int>(threadIdx.x) - g * T;
+  double* xbuf = xsm + g * (LUXs<Ls>::KXM * T);
+  const int64_t nit = (ntiles + TPC - 1) / TPC;
+  int64_t it = blockIdx.x;
+  if (it >= nit) return;
+  int64_t b = it * TPC + g;
+  if (b < ntiles)
+    large_u_xs_issue<Ls>(p, unit0, b, 0, xbuf, tid);
+  else
+    asm volatile("cp.async.commit_group;" ::: "memory");
   const int n2 = tid / NW, p2 = tid - (tid / NW) * NW;
 #pragma unroll 1
-  for (; b < ntiles; b += gridDim.x) {
-    const int np = static_cast<int>(b % (NV * NW));
-    const int64_t unit = unit0 + b / (NV * NW);
+  for (; it < nit; it += gridDim.x) {
+    b = it * TPC + g;
+    const bool live = b < ntiles;  // the last CTA iteration's spare groups idle (uniform per group)
+    const int64_t bb = live ? b : 0;
+    const int np = static_cast<int>(bb % (NV * NW));
+    const int64_t unit = unit0 + bb / (NV * NW);
     const int n1 = np / NW, p1 = np - (np / NW) * NW;
     const int64_t e = unit / p.P;
     const int pair = static_cast<int>(unit - e * p.P);
@@ -743,14 +787,17 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, Ls::UMINB)
       double x[KX];
       asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
-      for (int j = 0; j < KX; ++j) x[j] = xbuf[j * NV * NW + tid];
+      for (int j = 0; j < KX; ++j) x[j] = xbuf[j * T + tid];
       // bar.sync completes the shared-memory loads above before the next class's
       // copies are issued into the same slots
       __syncthreads();
-      if (PAR == 0)
-        large_u_xs_issue<Ls>(p, unit0, b, 1, xbuf);
-      else if (b + gridDim.x < ntiles)
-        large_u_xs_issue<Ls>(p, unit0, b + gridDim.x, 0, xbuf);
+      const int64_t bn = b + static_cast<int64_t>(gridDim.x) * TPC;
+      if (PAR == 0 && live)
+        large_u_xs_issue<Ls>(p, unit0, b, 1, xbuf, tid);
+      else if (PAR == 1 && bn < ntiles)
+        large_u_xs_issue<Ls>(p, unit0, bn, 0, xbuf, tid);
+      else
+        asm volatile("cp.async.commit_group;" ::: "memory");
       auto row = [&](auto m1c) {
         constexpr int m1 = decltype(m1c)::value;
         static_for<(Ls::USYM ? m1 : 0), NU>([&](auto m2c) {
@@ -768,8 +815,10 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, Ls::UMINB)
                 v = fma(lcoef<Ls, 0>(p.cu, p.cu_g, co + j), x[xi], v);
               });
             });
-            st_cs(out + m1 * rowstep + m2 * (NV * NW), v);
-            if constexpr (Ls::USYM && m2 != m1) st_cs(out + m2 * rowstep + m1 * (NV * NW), v);
+            if (live) {
+              st_cs(out + m1 * rowstep + m2 * (NV * NW), v);
+              if constexpr (Ls::USYM && m2 != m1) st_cs(out + m2 * rowstep + m1 * (NV * NW), v);
+            }
           }
         });
       };
@@ -815,7 +864,7 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, Ls::UMINB)
   int64_t b = blockIdx.x;
   if (b >= ntiles) return;
   const uint64_t policy = evict_first_policy();
-  large_u_xs_issue<Ls>(p, unit0, b, 0, xbuf);
+  large_u_xs_issue<Ls>(p, unit0, b, 0, xbuf, tid);
   int ring = 0;
 #pragma unroll 1
   for (; b < ntiles; b += gridDim.x) {
@@ -836,9 +885,9 @@ __global__ void __launch_bounds__(Ls::NV * Ls::NW, Ls::UMINB)
       for (int j = 0; j < KX; ++j) x[j] = xbuf[j * T + tid];
       __syncthreads();
       if (PAR == 0)
-        large_u_xs_issue<Ls>(p, unit0, b, 1, xbuf);
+        large_u_xs_issue<Ls>(p, unit0, b, 1, xbuf, tid);
       else if (b + gridDim.x < ntiles)
-        large_u_xs_issue<Ls>(p, unit0, b + gridDim.x, 0, xbuf);
+        large_u_xs_issue<Ls>(p, unit0, b + gridDim.x, 0, xbuf, tid);
       auto row = [&](auto m1c) {
         constexpr int m1 = decltype(m1c)::value;
         constexpr int m2s = Ls::USYM ? m1 : 0;
@@ -1075,16 +1124,20 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
       int bps = 0;
 #ifndef P2S_LEAN
       if (!p.roll) {
-        cudaError_t e = kernel_prepare(large_u_xs_kernel<Ls, false>, LUXs<Ls>::SMEM, T, false, &bps);
+        cudaError_t e = kernel_prepare(large_u_xs_kernel<Ls, false>, LUXs<Ls>::SMEM, LUXs<Ls>::THREADS, false, &bps);
         if (e != cudaSuccess) return e;
-        large_u_xs_kernel<Ls, false><<<grid_of(bps), T, LUXs<Ls>::SMEM, st>>>(p, unit0, ntiles);
+        const int64_t nit = (ntiles + LUXs<Ls>::TPC - 1) / LUXs<Ls>::TPC;
+        large_u_xs_kernel<Ls, false><<<static_cast<unsigned>(std::min<int64_t>(nit, int64_t(bps) * num_sms)),
+                                       LUXs<Ls>::THREADS, LUXs<Ls>::SMEM, st>>>(p, unit0, ntiles);
         return cudaGetLastError();
       }
 #endif
-      cudaError_t e = kernel_prepare(large_u_xs_kernel<Ls>, LUXs<Ls>::SMEM, T, false, &bps);
+      cudaError_t e = kernel_prepare(large_u_xs_kernel<Ls>, LUXs<Ls>::SMEM, LUXs<Ls>::THREADS, false, &bps);
       if (e != cudaSuccess) return e;
-      grid = grid_of(bps);
-      large_u_xs_kernel<Ls><<<grid, T, LUXs<Ls>::SMEM, st>>>(p, unit0, ntiles);
+      const int64_t nit = (ntiles + LUXs<Ls>::TPC - 1) / LUXs<Ls>::TPC;
+      const int64_t cap = max_ctas < 0 ? static_cast<int64_t>(bps) * num_sms : max_ctas;
+      grid = static_cast<unsigned>(cap > 0 && cap < nit ? cap : nit);
+      large_u_xs_kernel<Ls><<<grid, LUXs<Ls>::THREADS, LUXs<Ls>::SMEM, st>>>(p, unit0, ntiles);
       return cudaGetLastError();
     }
   }
@@ -1095,23 +1148,27 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
   (void)F2;
   (void)ps;
   if constexpr (Ls::u_conforming() || Ls::NW % 2 != 0) {
+    using PL = LUPlain<Ls, 1>;
     int bps = 0;
-    cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1>, 0, T, false, &bps);
+    cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1>, 0, PL::THREADS, false, &bps);
     if (e != cudaSuccess) return e;
-    large_u_kernel<Ls, true, 1><<<grid_of(bps), T, 0, st>>>(p, unit0, ntiles);
+    const int64_t nit = (ntiles + PL::TPC - 1) / PL::TPC;
+    const int64_t cap = max_ctas < 0 ? static_cast<int64_t>(bps) * num_sms : max_ctas;
+    large_u_kernel<Ls, true, 1><<<static_cast<unsigned>(cap > 0 && cap < nit ? cap : nit), PL::THREADS, 0, st>>>(
+        p, unit0, ntiles);
   }
 #else
   if (ps && smemc && p.cu_g) {
-    cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1, true>, cs, T);
+    cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1, true>, cs, LUPlain<Ls, 1>::THREADS);
     if (e != cudaSuccess) return e;
-    large_u_kernel<Ls, true, 1, true><<<grid, T, cs, st>>>(p, unit0, ntiles);
+    large_u_kernel<Ls, true, 1, true><<<grid, LUPlain<Ls, 1>::THREADS, cs, st>>>(p, unit0, ntiles);
   }
   else if (ps && fib == 2)
     large_u_kernel<Ls, true, F2><<<grid, T / F2, 0, st>>>(p, unit0, ntiles);
   else if (ps)
-    large_u_kernel<Ls, true, 1><<<grid, T, 0, st>>>(p, unit0, ntiles);
+    large_u_kernel<Ls, true, 1><<<grid, LUPlain<Ls, 1>::THREADS, 0, st>>>(p, unit0, ntiles);
   else
-    large_u_kernel<Ls, false, 1><<<grid, T, 0, st>>>(p, unit0, ntiles);
+    large_u_kernel<Ls, false, 1><<<grid, LUPlain<Ls, 1>::THREADS, 0, st>>>(p, unit0, ntiles);
 #endif
   return cudaGetLastError();
 }

@@ -166,7 +166,10 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
     const int64_t wblocks = (cnt * Ls::KUTOT() + kLargeWWarps - 1) / kLargeWWarps * Ls::NGRP;
     large_w_kernel<Ls><<<static_cast<unsigned>(wblocks), 32 * kLargeWWarps, 0, vs>>>(wp);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    large_v_kernel<Ls><<<static_cast<unsigned>(cnt * Ls::KUTOT()), Ls::NW * Ls::NW, 0, vs>>>(vp);
+    {
+      constexpr int VR = LVRows<Ls>::VR;
+      large_v_kernel<Ls><<<static_cast<unsigned>((cnt * Ls::KUTOT() + VR - 1) / VR), VR * Ls::NW * Ls::NW, 0, vs>>>(vp);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     cudaStream_t us = (two && b == 1) ? pk.aux_u : st;
     if (ov) {
