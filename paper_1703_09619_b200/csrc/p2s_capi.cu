@@ -73,7 +73,7 @@ const char* const kOptionKeys[] = {
     "P2S_JIT_T", "P2S_JIT_FLAGS", "P2S_JIT_FPT", "P2S_JIT_MINB", "P2S_JIT_THREADS", "P2S_JIT_KC",
     "P2S_GEO_MODE",         // geometry fill mode 0 / 1 / 2
     "P2S_XCHUNK_MB",        // large path: intermediate chunk (MB)
-    "P2S_LARGE_PS", "P2S_LARGE_OVERLAP", "P2S_LARGE_PRIO", "P2S_LARGE_USTREAMS", "P2S_LARGE_UPERSIST",
+    "P2S_LARGE_PS", "P2S_LARGE_OVERLAP", "P2S_LARGE_PRIO", "P2S_LARGE_USTREAMS", "P2S_LARGE_UPERSIST", "P2S_LARGE_URESERVE",
     "P2S_LARGE_XS", "P2S_LARGE_UBULK", "P2S_LARGE_UROLL", "P2S_LARGE_UPAIR", "P2S_LARGE_MSPLIT", "P2S_LARGE_MOMCL", "P2S_LARGE_USMEM", "P2S_LARGE_FIB",
     "P2S_CHUNK_MB",         // two-stage scheduler chunk (MB of moments)
     "P2S_TWO_STAGE_OVERLAP", "P2S_MOM_PRIO",
@@ -869,6 +869,8 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
       const int k = std::atoi(v);
       c->lpack.u_ctas = k < 0 ? -1 : static_cast<int64_t>(k) * c->num_sms;
     }
+    if (const char* v = opt.get("P2S_LARGE_URESERVE"))  // CTA slots of the persistent u grid left free
+      if (c->lpack.u_ctas < 0) c->lpack.u_ctas = -1 - std::max(0, std::atoi(v));
     if (const char* v = opt.get("P2S_LARGE_XS")) c->lpack.u_xs = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_UBULK")) c->lpack.u_bulk = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_UROLL")) c->lpack.u_roll = v[0] == '1' ? 1 : 0;

@@ -82,6 +82,8 @@ struct Shape {
   static constexpr int NSYM = (FLAGS_ >> 9) & 1;
   static_assert(!NSYM || (SYM && !MMA && !QUAD), "NSYM needs SYM (and the banded stage C)");
   static_assert(!NSYM || !PAIR || NW_ % 2 == 0, "NSYM pairs need an even N_w");
+  // AL1 (bit 10): the fused kernel's w-first alpha loads allocate in L1 (A/B only)
+  static constexpr int AL1 = (FLAGS_ >> 10) & 1;
   static constexpr int AALL = (FLAGS_ & 1) | SYM, ROWLOOP = (FLAGS_ >> 1) & 1;
   static constexpr int NQV = NV_ * (NV_ + 1) / 2, NQW = NW_ * (NW_ + 1) / 2;
   static constexpr int tri(int a, int b, int n) { return a * n - a * (a - 1) / 2 + (b - a); }

@@ -132,6 +132,15 @@ __device__ __forceinline__ void ld_nc4(const double* p, double& a, double& b, do
                : "l"(p));
 }
 
+// 8-B read-only load that does not allocate in L1: alpha is read once, and a
+// kernel that spills keeps its local-memory lines in the (small, mostly carved
+// out for shared memory) L1 instead of losing them to the alpha stream
+__device__ __forceinline__ double ld_nc_na(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // 32-B streaming store of four adjacent doubles (p 32-B aligned; sm_100 STG.256)
 __device__ __forceinline__ void st_cs4(double* p, double a, double b, double c, double d) {
   asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)

@@ -103,6 +103,18 @@ __device__ __forceinline__ void geo_cluster_phase(const GeoUnit& g, const double
   }
 }
 
+// The w-first moment pass reads alpha with loads that do not allocate in L1
+// (ld.global.nc.L1::no_allocate; C4: 1.150 M vs 1.127 M elem/s, L2 read misses
+// 29.7 M -> 19.4 M sectors per 2048 elements, profiles/r2_c4_alpha_noalloc.txt).
+// Shape FLAGS bit 10 (AL1) restores the allocating loads for A/B runs.
+template <class Sh>
+constexpr bool alpha_no_allocate() {
+  if constexpr (Sh::WLAST)
+    return true;
+  else
+    return Sh::AL1 == 0;
+}
+
 // GEO: 0 alpha from HBM; 1 the moment phase computes the coupling factors
 // from the element's geometry record per unit; 2 cluster mode (one cluster of
 // P CTAs per element shares the per-point geometry through DSMEM).
@@ -146,7 +158,7 @@ __global__ void __launch_bounds__(Sh::THREADS, Sh::MINB)
       if (threadIdx.x == 0 && unit + stride < p.c.n_units)
         prefetch_l2(a + stride * Ms::S * slab, static_cast<uint32_t>(Ms::S * slab * 8));
     if constexpr (Ms::WFIRST)
-      moments_all_terms_wfirst<Ms, Sh::THREADS>(a, p.tab, Abuf, Ibuf);
+      moments_all_terms_wfirst<Ms, Sh::THREADS, alpha_no_allocate<Sh>()>(a, p.tab, Abuf, Ibuf);
     else
       moments_all_terms<Ms, Sh::THREADS>(a, p.tab, Abuf, Ibuf);
     }

@@ -1087,9 +1087,10 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
                       bool smemc, int num_sms, cudaStream_t st) {
   const int64_t ntiles = cnt * Ls::NV * Ls::NW;
   // max_ctas > 0: persistent grid of that many CTAs; 0: one CTA per tile; < 0:
-  // persistent, as many CTAs as are resident (occupancy x SMs)
+  // persistent, as many CTAs as are resident (occupancy x SMs) less -1 - max_ctas
+  // slots left free for the next chunk's w / v steps
   auto grid_of = [&](int bps) {
-    const int64_t cap = max_ctas < 0 ? static_cast<int64_t>(bps) * num_sms : max_ctas;
+    const int64_t cap = max_ctas < 0 ? std::max<int64_t>(num_sms, static_cast<int64_t>(bps) * num_sms + max_ctas + 1) : max_ctas;
     return static_cast<unsigned>(cap > 0 && cap < ntiles ? cap : ntiles);
   };
   unsigned grid = grid_of(2);
@@ -1103,7 +1104,7 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
       cudaError_t e = kernel_prepare(large_u_pair_kernel<Ls>, LUPair<Ls>::SMEM, LUPair<Ls>::THREADS, false, &bps);
       if (e != cudaSuccess) return e;
       const int64_t nit = (ntiles + LUPair<Ls>::TPC - 1) / LUPair<Ls>::TPC;
-      const int64_t cap = max_ctas < 0 ? static_cast<int64_t>(bps) * num_sms : max_ctas;
+      const int64_t cap = max_ctas < 0 ? std::max<int64_t>(num_sms, static_cast<int64_t>(bps) * num_sms + max_ctas + 1) : max_ctas;
       const unsigned pg = static_cast<unsigned>(cap > 0 && cap < nit ? cap : nit);
       large_u_pair_kernel<Ls><<<pg, LUPair<Ls>::THREADS, LUPair<Ls>::SMEM, st>>>(p, unit0, ntiles);
       return cudaGetLastError();
@@ -1135,7 +1136,7 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
       cudaError_t e = kernel_prepare(large_u_xs_kernel<Ls>, LUXs<Ls>::SMEM, LUXs<Ls>::THREADS, false, &bps);
       if (e != cudaSuccess) return e;
       const int64_t nit = (ntiles + LUXs<Ls>::TPC - 1) / LUXs<Ls>::TPC;
-      const int64_t cap = max_ctas < 0 ? static_cast<int64_t>(bps) * num_sms : max_ctas;
+      const int64_t cap = max_ctas < 0 ? std::max<int64_t>(num_sms, static_cast<int64_t>(bps) * num_sms + max_ctas + 1) : max_ctas;
       grid = static_cast<unsigned>(cap > 0 && cap < nit ? cap : nit);
       large_u_xs_kernel<Ls><<<grid, LUXs<Ls>::THREADS, LUXs<Ls>::SMEM, st>>>(p, unit0, ntiles);
       return cudaGetLastError();
@@ -1153,7 +1154,7 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
     cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1>, 0, PL::THREADS, false, &bps);
     if (e != cudaSuccess) return e;
     const int64_t nit = (ntiles + PL::TPC - 1) / PL::TPC;
-    const int64_t cap = max_ctas < 0 ? static_cast<int64_t>(bps) * num_sms : max_ctas;
+    const int64_t cap = max_ctas < 0 ? std::max<int64_t>(num_sms, static_cast<int64_t>(bps) * num_sms + max_ctas + 1) : max_ctas;
     large_u_kernel<Ls, true, 1><<<static_cast<unsigned>(cap > 0 && cap < nit ? cap : nit), PL::THREADS, 0, st>>>(
         p, unit0, ntiles);
   }

@@ -504,7 +504,7 @@ __device__ __forceinline__ void moments_all_terms(const double* __restrict__ a, 
 //           consecutive q_u: every load instruction is 256 contiguous bytes)
 //   pass v: thread = (k3, q_u), fiber along q_v of W1[k3][q_v][q_u]
 //   pass u: thread = (k3, k2), fiber along q_u of W2[k3*KV + k2][q_u]
-template <class Ms, int NTHR>
+template <class Ms, int NTHR, bool NA = false>
 __device__ __forceinline__ void moments_all_terms_wfirst(const double* __restrict__ a,
                                                          const double* tab, double* scratch,
                                                          double* Iout) {
@@ -524,7 +524,8 @@ __device__ __forceinline__ void moments_all_terms_wfirst(const double* __restric
       const double* col = a + s * slab + r;
       double x[QW];
 #pragma unroll
-      for (int q = 0; q < QW; ++q) x[q] = __ldg(col + q * (QU * QV));
+      for (int q = 0; q < QW; ++q)
+        x[q] = NA ? ld_nc_na(col + q * (QU * QV)) : __ldg(col + q * (QU * QV));
 #pragma unroll
       for (int h = 0; h < Hf; ++h) {
         ev[s][h] = x[h] + x[QW - 1 - h];

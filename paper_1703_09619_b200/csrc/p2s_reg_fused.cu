@@ -14,7 +14,7 @@ namespace reg {
 // <Shape: N_u, N_v, N_w, n1 tile, p1 tile, p1 group, threads, min CTAs/SM, flags, FPT, kinds>
 // flags: 1 AALL, 2 ROWLOOP, 4 SYM, 8 PERSIST, 16 MMA (stage C on DMMA), 32 PAIR (16-B
 // stores), 64 PSPLIT (parity-split stage C), 128 NOUSYM, 256 QUAD (32-B stores),
-// 512 NSYM ((n1, n2)-symmetric stage C).  The first match of a problem is the
+// 512 NSYM ((n1, n2)-symmetric stage C), 1024 AL1 (alpha loads allocate in L1).  The first match of a problem is the
 // default; P2S_FUSED_VARIANT=k selects the k-th (tuning / A-B measurements, see
 // profiles/README.md for the numbers behind each default).
 const std::vector<FusedEntry>& fused_registry() {
@@ -58,6 +58,8 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>, false, false, false>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 70, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 256, 2, 1094, 1, kPPP, kDDD>,   // 2: default with L1-allocating alpha loads
+                 MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 70, 2, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
@@ -96,6 +98,9 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<8, 8, 8, 20, 20, 20, 256, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 582, 2, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
+      // C3 variant 7: parity split, 512 threads, row loop (as the two-stage default)
+      make_fused<Shape<8, 8, 8, 1, 8, 8, 512, 1, 70, 1, kPPP, kDDD>,
+                 MShape<8, 8, 8, 20, 20, 20, 512, kPPP, kDDD>>(),
       // (C2 at 288 / 320 threads, 96 registers: 1.694 M / 1.698 M burst, 1.486 M / 1.488 M
       // at 1000 steps vs 1.705 M / 1.504 M for the 256-thread default)
       // test shapes

@@ -28,10 +28,18 @@ const std::vector<V2Entry>& v2_registry() {
       // C3 (persistent SYM variants <..., 256, 1, 12, 1|2> were dropped: both fault with an
       // illegal address at 255 registers + 100-140 B of stack even for one element,
       // where they execute the non-persistent code path; unused, never a default)
-      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 1, kPPP, kDDD>>(),           // C3
+      // C3 default: parity-split stage C (half the register-resident fiber: 90 registers)
+      // with 512 threads and a runtime row loop: 2.45 M elem/s (0.873) vs 2.37 M (0.84) for
+      // the 256-thread banded kernels below (254 registers, 8 warps per SM);
+      // profiles/r2_c3_v2_variants.txt.  1, 2 = 256 threads banded (FPT 1 / 2), 3 = 512
+      // threads with unrolled rows (126 registers, 2.32 M), 4 = 384 threads (2.28 M)
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 512, 1, 70, 1, kPPP, kDDD>>(),          // C3
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 1, kPPP, kDDD>>(),
       make_v2<Shape<8, 8, 8, 1, 8, 8, 256, 1, 4, 2, kPPP, kDDD>>(),
-      // (C3 at 384 / 512 threads: 168 / 128 registers with 284 / 256 B of spills,
-      // 1.96 M / 2.07 M elem/s vs 2.31 M)
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 512, 1, 68, 1, kPPP, kDDD>>(),
+      make_v2<Shape<8, 8, 8, 1, 8, 8, 384, 1, 70, 1, kPPP, kDDD>>(),
+      // (C3 banded, not parity split, at 384 / 512 threads: 168 / 128 registers with
+      // 284 / 256 B of spills, 1.96 M / 2.07 M elem/s)
       make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>>(),          // C4
       make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 4, 1, kPPP, kDDD>>(),
       make_v2<Shape<10, 6, 4, 2, 4, 4, 192, 2, 2, 1, kPPP, kDDD>>(),

@@ -129,7 +129,7 @@ def test_moment_kernel_variants_match_oracle(name, variant, monkeypatch):
                 assert ok, (e, pr, s, i, j, g[i, j], r[i, j])
 
 
-@pytest.mark.parametrize("name,variant", [(c, v) for c in ("c2", "c3", "c4") for v in range(3)])
+@pytest.mark.parametrize("name,variant", [(c, v) for c in ("c2", "c3", "c4") for v in range(5)])
 def test_two_stage_contraction_variants_match_oracle(name, variant, monkeypatch):
     # every registered contract_v2 variant of the benchmark shapes (P2S_V2_VARIANT,
     # two-stage path) gives the oracle's matrices
