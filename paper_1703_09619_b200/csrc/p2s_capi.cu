@@ -73,7 +73,7 @@ const char* const kOptionKeys[] = {
     "P2S_JIT_T", "P2S_JIT_FLAGS", "P2S_JIT_FPT", "P2S_JIT_MINB", "P2S_JIT_THREADS", "P2S_JIT_KC",
     "P2S_GEO_MODE",         // geometry fill mode 0 / 1 / 2
     "P2S_XCHUNK_MB",        // large path: intermediate chunk (MB)
-    "P2S_LARGE_PS", "P2S_LARGE_OVERLAP", "P2S_LARGE_PRIO", "P2S_LARGE_USTREAMS", "P2S_LARGE_UPERSIST", "P2S_LARGE_URESERVE",
+    "P2S_LARGE_PS", "P2S_LARGE_OVERLAP", "P2S_LARGE_PRIO", "P2S_LARGE_USTREAMS", "P2S_LARGE_UPERSIST", "P2S_LARGE_URESERVE", "P2S_LARGE_VSPLIT",
     "P2S_LARGE_XS", "P2S_LARGE_UBULK", "P2S_LARGE_UROLL", "P2S_LARGE_UPAIR", "P2S_LARGE_MSPLIT", "P2S_LARGE_MOMCL", "P2S_LARGE_USMEM", "P2S_LARGE_FIB",
     "P2S_CHUNK_MB",         // two-stage scheduler chunk (MB of moments)
     "P2S_TWO_STAGE_OVERLAP", "P2S_MOM_PRIO",
@@ -836,11 +836,25 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
     // (n1, p1) tiles over 2 CTAs per SM, else >= 6 waves (amortised tails) up to
     // 96 MB.  Measured (r2j): c12 (3.95 MB / unit) 24 MB 0.60 vs 96 MB 0.53 of
     // HBM; C5 (16.7 MB / unit) 96 MB 0.65 vs 48 MB 0.59.
-    const int64_t tiles_per_unit = static_cast<int64_t>(spec->order[1]) * spec->order[2];
+    // Work items per unit of the three kernels (host mirrors of LUXs / LUPlain::TPC,
+    // LVRows::VR and the w step's 8-row CTAs): shapes with small N_v N_w pack several
+    // (n1, p1) tiles / k1 rows into one CTA, so a chunk must hold enough units to
+    // fill the GPU with CTAs of EVERY step, not only with u-stage tiles
+    const int64_t tile_threads = static_cast<int64_t>(spec->order[1]) * spec->order[2];
+    const int64_t tpc = tile_threads >= 128 ? 1 : (128 + tile_threads - 1) / tile_threads;
+    const int64_t vthreads = static_cast<int64_t>(spec->order[2]) * spec->order[2];
+    const int64_t vr = vthreads >= 128 ? 1 : (128 + vthreads - 1) / vthreads;
+    int64_t kutot = 0;
+    for (int s = 0; s < S; ++s) kutot += c->sz.K[s][0];
+    const double u_items = static_cast<double>(tile_threads) / static_cast<double>(tpc);
+    const double v_items = static_cast<double>(kutot) / static_cast<double>(vr);
+    const double w_items = static_cast<double>(kutot) / 8.0 * ((spec->order[2] + 1) / 2);
     const int64_t ctas = 2 * static_cast<int64_t>(c->num_sms);
     const int64_t xbytes = lge->xpu * 8;
-    auto units_for_waves = [&](double w) {
-      return static_cast<int64_t>(std::ceil(w * static_cast<double>(ctas) / static_cast<double>(tiles_per_unit)));
+    auto units_for_waves = [&](double w) {  // w waves of u-stage CTAs, >= one CTA per SM in the v / w steps
+      const double need = std::max(w * static_cast<double>(ctas) / u_items,
+                                   0.5 * static_cast<double>(ctas) / std::min(v_items, w_items));
+      return static_cast<int64_t>(std::ceil(need));
     };
     int64_t units = units_for_waves(2.5);
     if (units * xbytes > (int64_t(32) << 20))
@@ -871,6 +885,7 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
     }
     if (const char* v = opt.get("P2S_LARGE_URESERVE"))  // CTA slots of the persistent u grid left free
       if (c->lpack.u_ctas < 0) c->lpack.u_ctas = -1 - std::max(0, std::atoi(v));
+    if (const char* v = opt.get("P2S_LARGE_VSPLIT")) c->lpack.v_split = std::max(0, std::atoi(v));
     if (const char* v = opt.get("P2S_LARGE_XS")) c->lpack.u_xs = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_UBULK")) c->lpack.u_bulk = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_UROLL")) c->lpack.u_roll = v[0] == '1' ? 1 : 0;

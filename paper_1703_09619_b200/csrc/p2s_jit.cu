@@ -219,6 +219,12 @@ bool plan_fused(const Desc& d, Plan* pl, const Overrides& ov) {
         if (((c.flags >> 2) & 1) && !sym) continue;
         if (!(c.flags & 5) && c.T < NV) continue;  // see above
         if (pass == 0 && c.smem_fused > kSmemTwo && ov.minb < 0) continue;
+        // a two-CTA tile must still give stage C a CTA's worth of work items (a
+        // (12, 9, 3) shape at T = 1 has 41: 2.5 M elem/s vs 4.9 M for one CTA with
+        // all nine n1, profiles/r2z_sweep_fused.jsonl)
+        if (pass == 0 && ov.T < 0 && c.T < NV &&
+            static_cast<int64_t>(c.T) * d.N[2] * NV * d.N[2] / c.fpt < 128)
+          continue;
         best = c;
         found = true;
         break;
@@ -226,6 +232,19 @@ bool plan_fused(const Desc& d, Plan* pl, const Overrides& ov) {
       if (found) break;
     }
   if (!found) return false;
+  // small units (little shared memory per CTA): more, smaller CTAs per SM -- such
+  // shapes are latency-bound (a CTA is a chain of short phases between barriers),
+  // so occupancy by independent CTAs is what pays: ~600 threads per SM over up to 8
+  // CTAs.  Measured (r2z): (1, 1, 12) 64 threads x 8: 31 M elem/s vs 9.6 M at 256 x 2;
+  // (1, 3, 7) 96 x 6: 129 M vs 76 M; (13, 12, 1) 128 x 4: 18.5 M vs 13.9 M;
+  // (5, 5, 5) 192 x 3: 28.4 M vs 24.5 M.
+  if (ov.threads <= 0 && ov.minb <= 0) {
+    const int ctas = static_cast<int>(std::min<int64_t>(8, kSmemMax / (best.smem_fused + 1024)));
+    if (ctas >= 3) {
+      best.minb = ctas;
+      best.threads = std::max(64, std::min(256, (608 / ctas) / 32 * 32));
+    }
+  }
   std::ostringstream sh, ms, desc;
   sh << "p2s::Shape<" << d.N[0] << ", " << d.N[1] << ", " << d.N[2] << ", " << best.T << ", " << d.N[2]
      << ", " << d.N[2] << ", " << best.threads << ", " << best.minb << ", " << best.flags << ", " << best.fpt
@@ -271,7 +290,9 @@ bool plan_large(const Desc& d, Plan* pl, std::string* why, const Overrides& ov) 
   pl->source = "using JitLShape = " + ls.str() + ";\nP2S_JIT_LARGE(JitLShape)\n";
   desc << "large-order: moments (k1 chunks of " << kc << ") + w step + v step + u stage";
   for (int dd = 0; dd < 3; ++dd)
-    if (8 * d.ctot(dd) > 30 * 1024) desc << ", dir " << dd << " coefficients in global memory";
+    if (8 * d.ctot(dd) > 30 * 1024)
+      desc << ", dir " << dd
+           << (8 * d.ctot(dd) <= 128 * 1024 ? " coefficients staged in shared memory" : " coefficients in global memory");
   pl->desc = desc.str();
   pl->smem = mom_smem(kc);
   return true;

@@ -79,9 +79,11 @@ struct LShape {
   }
   static constexpr int64_t XPU = xoff(S);
   // Z block of one unit (w-contracted moments): terms back to back,
-  // [K_u][N_w][N_w][K2P], k2 fastest and padded to 32 (one lane per k2; 64 above
-  // 32 kernel polynomials along v, two k2 per lane)
-  static constexpr int K2P = KMAX(1) <= 32 ? 32 : 64;
+  // [K_u][N_w][N_w][K2P], k2 fastest and padded to a power of two >= 4 (32-B fiber
+  // loads in the v step; one lane per k2 up to 32, two k2 per lane above).  (A fixed
+  // pad of 32 made Z of a (10, 1, 14) shape, K_v = 1, 2.8 MB per unit written 8 bytes
+  // per 256: the w step took 0.5 ms per chunk whatever its thread mapping.)
+  static constexpr int K2P = KMAX(1) > 32 ? 64 : KMAX(1) > 16 ? 32 : KMAX(1) > 8 ? 16 : KMAX(1) > 4 ? 8 : 4;
   static constexpr int64_t zoff(int s) {
     int64_t o = 0;
     for (int i = 0; i < s; ++i) o += static_cast<int64_t>(K(i, 0)) * NW * NW * K2P;
@@ -89,6 +91,18 @@ struct LShape {
   }
   static constexpr int64_t ZPU = zoff(S);
   static constexpr int NGRP = (NW + 1) / 2;  // w-step p1 groups {g, N_w-1-g}
+  // w step: a warp's lanes are k2; with few kernel polynomials along v (small N_v)
+  // a warp takes WR = 32 / K2S consecutive k1 rows of a term (lane = (k1 offset, k2))
+  // instead of idling 32 - K_v lanes -- (10, 1, 14): K_v = 1, one lane in 32 worked
+  static constexpr int K2S = KMAX(1) > 16 ? 32 : KMAX(1) > 8 ? 16 : KMAX(1) > 4 ? 8 : KMAX(1) > 2 ? 4 : KMAX(1) > 1 ? 2 : 1;
+  static constexpr int WR = 32 / K2S;
+  static constexpr int kgrp(int s) { return (K(s, 0) + WR - 1) / WR; }  // row groups of term s
+  static constexpr int kgoff(int s) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) o += kgrp(i);
+    return o;
+  }
+  static constexpr int KGTOT() { return kgoff(S); }
   static constexpr int KUTOT() {
     int o = 0;
     for (int s = 0; s < S; ++s) o += K(s, 0);
@@ -136,6 +150,10 @@ struct LShape {
   static constexpr int kParamBytes = 30 * 1024;
   static constexpr bool GC(int d) { return ctot(d) * 8 > kParamBytes; }
   static constexpr int cpar(int d) { return GC(d) ? 1 : ctot(d); }
+  // ... staged once per CTA into shared memory (uniform-address LDS instead of one
+  // global load per FMA) while the table leaves room for the kernel's own buffers
+  static constexpr bool GS(int d) { return GC(d) && ctot(d) * 8 <= 128 * 1024; }
+  static constexpr size_t cs_bytes(int d) { return GS(d) ? sizeof(double) * static_cast<size_t>(ctot(d)) : 0; }
   // shared half tables [KMAX(d)][H(d)] per direction
   static constexpr int ttoff(int d) {
     int o = 0;
@@ -427,28 +445,48 @@ struct LVParams {
   const double* Z;
   double* X;            // [units][XPU]
   const double* cg;     // device copy of cv (GC(1))
+  int ns;               // n1 slices: CTA blockIdx % ns forms the outputs with n1 % ns == slice
   int64_t n_units;
   double cv[Ls::cpar(1)];
 };
 
 // coefficient i of direction D: constant-bank kernel parameter, or global memory
 // when the direction's table exceeds the parameter space
+// (`glob` is the CTA's shared-memory copy when Ls::GS(D): see stage_coef)
 template <class Ls, int D>
 __device__ __forceinline__ double lcoef(const double* par, const double* __restrict__ glob, int i) {
-  if constexpr (Ls::GC(D))
+  if constexpr (Ls::GS(D))
+    return glob[i];
+  else if constexpr (Ls::GC(D))
     return __ldg(glob + i);
   else
     return par[i];
 }
 
+// Copy direction D's over-size coefficient table into shared memory (all threads of
+// the CTA, coalesced; ends with a barrier) and return the pointer lcoef reads.
+template <class Ls, int D>
+__device__ __forceinline__ const double* stage_coef(const double* __restrict__ glob, double* sh) {
+  if constexpr (Ls::GS(D)) {
+    for (int i = threadIdx.x; i < Ls::ctot(D); i += blockDim.x) sh[i] = __ldg(glob + i);
+    __syncthreads();
+    return sh;
+  } else {
+    return glob;
+  }
+}
+
 template <class Ls, int s>
-__device__ __forceinline__ void large_w_row(const LWParams<Ls>& p, const double* cw, int64_t unit, int k1,
-                                            int g, int lane) {
+__device__ __forceinline__ void large_w_row(const LWParams<Ls>& p, const double* cw, const double* cg,
+                                            int64_t unit, int grp, int g, int lane) {
   constexpr int NW = Ls::NW, K2P = Ls::K2P;
-  constexpr int KV = Ls::K(s, 1), KW = Ls::K(s, 2), kw = Ls::kind(s, 2);
+  constexpr int KU = Ls::K(s, 0), KV = Ls::K(s, 1), KW = Ls::K(s, 2), kw = Ls::kind(s, 2);
   static_assert(KV <= K2P, "w step maps k2 to lanes");
+  // lane = (k1 offset, k2): WR rows of K2S lanes (WR = 1: one row, k2 = lane, lane + 32)
+  const int k1 = grp * Ls::WR + lane / Ls::K2S;
+  if (k1 >= KU) return;
 #pragma unroll 1
-  for (int k2 = lane; k2 < KV; k2 += 32) {
+  for (int k2 = lane % Ls::K2S; k2 < KV; k2 += Ls::K2S) {
   const double* src = p.I + unit * Ls::MPP + Ls::moff(s) + (k1 * KV + k2) * KW;
   double y[KW];
 #pragma unroll
@@ -463,7 +501,7 @@ __device__ __forceinline__ void large_w_row(const LWParams<Ls>& p, const double*
       double v = 0.0;
       static_for<0, cnt>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
-        v = fma(lcoef<Ls, 2>(cw, p.cg, co + j), y[lo + band_step(kw, a, b) * j], v);
+        v = fma(lcoef<Ls, 2>(cw, cg, co + j), y[lo + band_step(kw, a, b) * j], v);
       });
       Zk[(a * NW + b) * K2P] = v;
     });
@@ -488,16 +526,18 @@ constexpr int kLargeWWarps = 8;
 
 template <class Ls>
 __global__ void __launch_bounds__(32 * kLargeWWarps) large_w_kernel(const __grid_constant__ LWParams<Ls> p) {
+  extern __shared__ __align__(16) double csh[];
+  const double* cg = stage_coef<Ls, 2>(p.cg, csh);
   const int lane = threadIdx.x & 31;
   const int g = static_cast<int>(blockIdx.x % Ls::NGRP);
   const int64_t item = static_cast<int64_t>(blockIdx.x / Ls::NGRP) * kLargeWWarps + threadIdx.x / 32;
-  const int row = static_cast<int>(item % Ls::KUTOT());
-  const int64_t unit = item / Ls::KUTOT();
+  const int row = static_cast<int>(item % Ls::KGTOT());   // (term, group of WR k1 rows)
+  const int64_t unit = item / Ls::KGTOT();
   if (unit >= p.n_units) return;
   static_for<0, Ls::S>([&](auto sc) {
     constexpr int s = decltype(sc)::value;
-    if (row >= Ls::kuoff(s) && row < Ls::kuoff(s) + Ls::K(s, 0))
-      large_w_row<Ls, s>(p, p.cw, unit, row - Ls::kuoff(s), g, lane);
+    if (row >= Ls::kgoff(s) && row < Ls::kgoff(s) + Ls::kgrp(s))
+      large_w_row<Ls, s>(p, p.cw, cg, unit, row - Ls::kgoff(s), g, lane);
   });
 }
 
@@ -513,8 +553,11 @@ template <class Ls>
 __global__ void __launch_bounds__(LVRows<Ls>::VR * Ls::NW * Ls::NW) large_v_kernel(const __grid_constant__ LVParams<Ls> p) {
   constexpr int NV = Ls::NV, NW = Ls::NW, NQV = Ls::NQV, K2P = Ls::K2P;
   constexpr int F = LVRows<Ls>::F;
+  extern __shared__ __align__(16) double csh[];
+  const double* cg = stage_coef<Ls, 1>(p.cg, csh);
   const int rl = LVRows<Ls>::VR == 1 ? 0 : static_cast<int>(threadIdx.x) / F;
-  const int64_t b = static_cast<int64_t>(blockIdx.x) * LVRows<Ls>::VR + rl;
+  const int slice = static_cast<int>(blockIdx.x % p.ns);
+  const int64_t b = static_cast<int64_t>(blockIdx.x / p.ns) * LVRows<Ls>::VR + rl;
   const int row = static_cast<int>(b % Ls::KUTOT());
   const int64_t unit = b / Ls::KUTOT();
   if (unit >= p.n_units) return;
@@ -532,6 +575,7 @@ __global__ void __launch_bounds__(LVRows<Ls>::VR * Ls::NW * Ls::NW) large_v_kern
     double* Xk = p.X + unit * Ls::XPU + Ls::xoff(s) + static_cast<int64_t>(k1) * NQV * NW * NW + t;
     static_for<0, NV>([&](auto n1c) {
       constexpr int a = decltype(n1c)::value;
+      if (a % p.ns != slice) return;  // CTA-uniform: this n1 row belongs to another slice
       static_for<(Ls::VSYM ? a : 0), NV>([&](auto n2c) {
         constexpr int c = decltype(n2c)::value;
         constexpr int lo = band_lo(kv, a, c), cnt = band_count(kv, a, c);
@@ -539,7 +583,7 @@ __global__ void __launch_bounds__(LVRows<Ls>::VR * Ls::NW * Ls::NW) large_v_kern
         double v = 0.0;
         static_for<0, cnt>([&](auto jc) {
           constexpr int j = decltype(jc)::value;
-          v = fma(lcoef<Ls, 1>(p.cv, p.cg, co + j), z[lo + band_step(kv, a, c) * j], v);
+          v = fma(lcoef<Ls, 1>(p.cv, cg, co + j), z[lo + band_step(kv, a, c) * j], v);
         });
         Xk[Ls::vidx(a, c) * NW * NW] = v;
       });
@@ -713,7 +757,8 @@ struct LUXs {
   static constexpr int TPC = T >= 128 ? 1 : (128 + T - 1) / T;
   static constexpr int THREADS = TPC * T;
   static constexpr int MINB = THREADS <= 96 ? 4 : THREADS <= 170 ? 3 : THREADS <= 256 ? 2 : 1;
-  static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(KXM) * T * TPC + 16;
+  static constexpr int XDBL = ((KXM * T * TPC + 1) & ~1) + 2;   // x slots (+ pad); the staged u table follows
+  static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(XDBL) + Ls::cs_bytes(0);
 };
 
 // Per-thread asynchronous copy (cp.async, 8 bytes) of the thread's own x values
@@ -758,6 +803,7 @@ __global__ void __launch_bounds__(LUXs<Ls>::THREADS, LUXs<Ls>::MINB)
   const int g = TPC == 1 ? 0 : static_cast<int>(threadIdx.x) / T;
   const int tid = static_cast<int>(threadIdx.x) - g * T;
   double* xbuf = xsm + g * (LUXs<Ls>::KXM * T);
+  const double* cu_g = stage_coef<Ls, 0>(p.cu_g, xsm + LUXs<Ls>::XDBL);
   const int64_t nit = (ntiles + TPC - 1) / TPC;
   int64_t it = blockIdx.x;
   if (it >= nit) return;
@@ -812,7 +858,7 @@ __global__ void __launch_bounds__(LUXs<Ls>::THREADS, LUXs<Ls>::MINB)
               static_for<0, cnt>([&](auto jc) {
                 constexpr int j = decltype(jc)::value;
                 constexpr int xi = Ls::kpo(s, PAR) + (lo - Ls::uk0(s, PAR)) / 2 + j;
-                v = fma(lcoef<Ls, 0>(p.cu, p.cu_g, co + j), x[xi], v);
+                v = fma(lcoef<Ls, 0>(p.cu, cu_g, co + j), x[xi], v);
               });
             });
             if (live) {
@@ -1151,11 +1197,14 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
   if constexpr (Ls::u_conforming() || Ls::NW % 2 != 0) {
     using PL = LUPlain<Ls, 1>;
     int bps = 0;
-    cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1>, 0, PL::THREADS, false, &bps);
+    // an over-size u table is staged in shared memory per (persistent) CTA
+    constexpr bool SC = Ls::GS(0);
+    constexpr size_t csm = Ls::cs_bytes(0);
+    cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1, SC>, csm, PL::THREADS, false, &bps);
     if (e != cudaSuccess) return e;
     const int64_t nit = (ntiles + PL::TPC - 1) / PL::TPC;
     const int64_t cap = max_ctas < 0 ? std::max<int64_t>(num_sms, static_cast<int64_t>(bps) * num_sms + max_ctas + 1) : max_ctas;
-    large_u_kernel<Ls, true, 1><<<static_cast<unsigned>(cap > 0 && cap < nit ? cap : nit), PL::THREADS, 0, st>>>(
+    large_u_kernel<Ls, true, 1, SC><<<static_cast<unsigned>(cap > 0 && cap < nit ? cap : nit), PL::THREADS, csm, st>>>(
         p, unit0, ntiles);
   }
 #else
@@ -1166,9 +1215,12 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
   }
   else if (ps && fib == 2)
     large_u_kernel<Ls, true, F2><<<grid, T / F2, 0, st>>>(p, unit0, ntiles);
-  else if (ps)
-    large_u_kernel<Ls, true, 1><<<grid, LUPlain<Ls, 1>::THREADS, 0, st>>>(p, unit0, ntiles);
-  else
+  else if (ps) {
+    constexpr bool SC = Ls::GS(0);
+    cudaError_t e = kernel_prepare(large_u_kernel<Ls, true, 1, SC>, Ls::cs_bytes(0), LUPlain<Ls, 1>::THREADS);
+    if (e != cudaSuccess) return e;
+    large_u_kernel<Ls, true, 1, SC><<<grid, LUPlain<Ls, 1>::THREADS, Ls::cs_bytes(0), st>>>(p, unit0, ntiles);
+  } else
     large_u_kernel<Ls, false, 1><<<grid, LUPlain<Ls, 1>::THREADS, 0, st>>>(p, unit0, ntiles);
 #endif
   return cudaGetLastError();

@@ -118,6 +118,7 @@ template <class Ls>
 cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t n_units,
                                   int64_t xchunk, int64_t ldM, int nc, int P, int Nt,
                                   const LargePack& pk, cudaStream_t st) {
+  cudaError_t e0 = cudaSuccess;
   LUParams<Ls> up;
   up.M = M;
   up.ldM = ldM;
@@ -143,6 +144,13 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
   vp.Z = pk.d_Z;
   vp.cg = pk.d_cvw;
   std::memcpy(vp.cv, pk.cvw.data(), sizeof(double) * Ls::cpar(1));
+  // over-size v / w tables are staged in shared memory per CTA (Ls::GS)
+  if (Ls::cs_bytes(2) > 0 &&
+      (e0 = kernel_prepare(large_w_kernel<Ls>, Ls::cs_bytes(2), 32 * kLargeWWarps)) != cudaSuccess)
+    return e0;
+  if (Ls::cs_bytes(1) > 0 &&
+      (e0 = kernel_prepare(large_v_kernel<Ls>, Ls::cs_bytes(1), LVRows<Ls>::VR * Ls::NW * Ls::NW)) != cudaSuccess)
+    return e0;
   // X holds two chunk buffers; chunk i uses buffer i % 2
   const bool ov = pk.overlap && pk.aux != nullptr;
   const bool two = ov && pk.two_u && pk.aux_u != nullptr && n_units > xchunk;
@@ -163,12 +171,19 @@ cudaError_t launch_large_contract(const double* I, double* X, double* M, int64_t
     cudaStream_t vs = ov ? pk.aux : st;
     if (ov && i >= 2 && (e = cudaStreamWaitEvent(pk.aux, pk.ev_u[b], 0)) != cudaSuccess) return e;
     // w step then v step (Z single-buffered: both on the same stream)
-    const int64_t wblocks = (cnt * Ls::KUTOT() + kLargeWWarps - 1) / kLargeWWarps * Ls::NGRP;
-    large_w_kernel<Ls><<<static_cast<unsigned>(wblocks), 32 * kLargeWWarps, 0, vs>>>(wp);
+    const int64_t wblocks = (cnt * Ls::KGTOT() + kLargeWWarps - 1) / kLargeWWarps * Ls::NGRP;
+    large_w_kernel<Ls><<<static_cast<unsigned>(wblocks), 32 * kLargeWWarps, Ls::cs_bytes(2), vs>>>(wp);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     {
       constexpr int VR = LVRows<Ls>::VR;
-      large_v_kernel<Ls><<<static_cast<unsigned>((cnt * Ls::KUTOT() + VR - 1) / VR), VR * Ls::NW * Ls::NW, 0, vs>>>(vp);
+      const int64_t items = (cnt * Ls::KUTOT() + VR - 1) / VR;
+      // few items per chunk (C5: 300 CTAs, one latency-bound wave): deal the n1 rows of
+      // an item to several CTAs
+      int64_t ns = 1;
+      if (pk.v_split > 0)
+        ns = std::max<int64_t>(1, std::min<int64_t>(Ls::NV, (int64_t(pk.v_split) * 2 * pk.num_sms + items - 1) / items));
+      vp.ns = static_cast<int>(ns);
+      large_v_kernel<Ls><<<static_cast<unsigned>(items * ns), VR * Ls::NW * Ls::NW, Ls::cs_bytes(1), vs>>>(vp);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     cudaStream_t us = (two && b == 1) ? pk.aux_u : st;

@@ -130,6 +130,9 @@ struct LargePack {
   int64_t u_ctas = -1;  // u-stage grid: persistent, resident CTAs (-1), k CTAs (> 0), one per tile (0)
   int num_sms = 148;
   int ufib = 1;  // u-stage fibers per thread (P2S_LARGE_FIB; 2 measured 18 % slower)
+  int v_split = 0;  // P2S_LARGE_VSPLIT: the n1 rows of a v-step item are dealt to up to N_v CTAs until
+                    // the step has this many waves of 2 CTAs per SM (0: one CTA per item; measured
+                    // slower: C5 0.65 -> 0.64 / 0.62 at 4 / 8 waves, c12 0.605 -> 0.573 / 0.53)
   cudaStream_t aux = nullptr, aux_u = nullptr;
   cudaEvent_t ev_start = nullptr, ev_join = nullptr, ev_vw[2]{}, ev_u[2]{};
 };
@@ -153,7 +156,7 @@ struct LargeEntry {
 
 // Registry entries of one generated per-shape module (p2s_jit.cu,
 // p2s_jit_module.cuh); kJitAbi changes whenever these structs change.
-constexpr int kJitAbi = 4;
+constexpr int kJitAbi = 5;
 struct JitEntries {
   int abi, family;   // family: 1 fused (+ two-stage entries of the shape), 2 large
   FusedEntry fused;

@@ -1,0 +1,19 @@
+# SYMB / IG parity (small shapes + C3 variants), C3 A/B of the two-CTA variants, launch lists of the slowest grid shapes
+for i in 37 19 29; do
+python tools/grid_one.py $i
+ncu --metrics gpu__time_duration.sum,launch__grid_size,launch__block_size,launch__registers_per_thread,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 240 --csv --log-file gpurun_out/r2y_launches_$i.csv python tools/grid_one.py $i 0 1 > /dev/null 2>&1
+python - <<EOF
+import csv,io,collections
+txt=open('gpurun_out/r2y_launches_$i.csv').read().splitlines()
+k=[j for j,l in enumerate(txt) if l.startswith('"ID"')][0]
+rows=list(csv.DictReader(io.StringIO('\n'.join(txt[k:]))))
+agg=collections.OrderedDict()
+for r in rows:
+    key=(r['ID'], r['Kernel Name'][:60]); agg.setdefault(key,{})[r['Metric Name']]=r['Metric Value']
+seen=collections.OrderedDict()
+for (id_,name),m in agg.items():
+    d=seen.setdefault(name,{'n':0,'t':0.0,'grid':m.get('launch__grid_size'),'blk':m.get('launch__block_size'),'regs':m.get('launch__registers_per_thread')})
+    d['n']+=1; d['t']+=float(m.get('gpu__time_duration.sum','0').replace(',',''))
+for name,d in seen.items(): print('   ',name, d)
+EOF
+done

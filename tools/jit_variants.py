@@ -17,6 +17,8 @@ PP, DD, DP, PD = 0, 1, 2, 3
 S7 = (1, (7, 7, 7), [PP, DD], (14, 14, 14), 0)
 S793 = (1, (7, 9, 3), [(DD, PD, DP), (PP, DP, DD), (PD, DP, DD), (PD, DP, DP)], (12, 12, 2), 0)
 S3 = (1, (3, 3, 3), [PP, DD], (6, 6, 6), 0)
+# P2S_JIT_SWEEP=<file.json>: cases from a JSON list of [grid index, {options}] over
+# shape_grid.ALL instead of the built-in list (planner sweeps over the drop-in grid)
 CASES = [
     # (shape, options)
     (S7, {"P2S_JIT_FLAGS": "0", "P2S_JIT_T": "1", "P2S_JIT_MINB": "1"}),
@@ -26,6 +28,11 @@ CASES = [
     (S3, {"P2S_FORCE_JIT": "1", "P2S_JIT_FLAGS": "1", "P2S_JIT_T": "1"}),
     (S793, {"P2S_JIT_T": "1", "P2S_JIT_MINB": "1", "P2S_JIT_FLAGS": "1"}),
 ]
+
+
+if os.environ.get("P2S_JIT_SWEEP"):
+    from paper_1703_09619_b200 import shape_grid as _sg
+    CASES = [(_sg.ALL[i][:5], o) for i, o in json.load(open(os.environ["P2S_JIT_SWEEP"]))]
 
 
 def one(idx):
