@@ -79,6 +79,7 @@ const char* const kOptionKeys[] = {
     "P2S_TWO_STAGE_OVERLAP", "P2S_MOM_PRIO",
     "P2S_HOST_CHUNK_MB",    // p2s_fill_host ring slot (MB of matrices)
     "P2S_GEO_CHUNK_MB",     // p2s_fill_geometry alpha buffer (MB)
+    "P2S_GRAPH",            // 0: large-path fills are never replayed from a CUDA graph
 };
 
 struct Options {
@@ -281,6 +282,23 @@ struct p2s_ctx {
   // ev_scratch whatever stream they come on; scratch_mu orders the host side
   std::mutex scratch_mu;
   cudaEvent_t ev_scratch = nullptr;
+  // large path: the launch sequence of a fill (hundreds of short w / v / u kernels
+  // with up to 30 KB of parameters each, ordered by events over three streams)
+  // costs the host about as long as the GPU needs to run it (c12: 9.4 ms of launch
+  // code for 10.6 ms of device time).  A fill that comes back with the same buffers
+  // is captured once into a CUDA graph and replayed (P2S_GRAPH=0: never).
+  struct FillGraph {
+    const double* alpha;
+    double* M;
+    int64_t ldM, n;
+    cudaGraphExec_t exec;  // null until the second call with this key
+    bool failed;           // capture / instantiation failed once: direct launches
+    uint64_t stamp;
+  };
+  std::vector<FillGraph> graphs;
+  cudaStream_t s_cap = nullptr;  // capture origin (the caller's stream may be the legacy stream)
+  uint64_t graph_clock = 0;
+  bool use_graphs = true;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -507,6 +525,82 @@ p2s_status run_fill(p2s_ctx* c, const double* alpha, double* M, int64_t ldM, int
     p2s_status s2 = run_contract(c, I, M + e0 * mstride, ldM, cnt, st);
     if (s2 != P2S_OK) return s2;
     P2S_CUDA(cudaEventRecord(c->ev_con_done[b], st));
+  }
+  return P2S_OK;
+}
+
+// Large path: run_fill through a cached CUDA graph.  First call with a key
+// (alpha, M, ld_M, n): direct launches (this also performs every per-kernel
+// attribute / occupancy call, which must not happen while capturing); second
+// call: the same launch code runs on the capture stream s_cap, the graph is
+// instantiated and launched into the caller's stream; later calls: one
+// cudaGraphLaunch.  At most 4 graphs per context (least recently used out).
+p2s_status run_fill_graphed(p2s_ctx* c, const double* alpha, double* M, int64_t ldM, int64_t n,
+                            cudaStream_t st) {
+  constexpr size_t kMaxGraphs = 4;
+  constexpr int64_t kMaxChunks = 1500;  // ~3 kernel nodes each; beyond that graphs cost too much memory
+  const int64_t chunks = c->xchunk > 0 ? (n * c->sz.n_pairs + c->xchunk - 1) / c->xchunk : 0;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (!c->use_graphs || n == 0 || chunks < 2 || chunks > kMaxChunks ||
+      cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return run_fill(c, alpha, M, ldM, n, st);
+  }
+  p2s_ctx::FillGraph* g = nullptr;
+  for (auto& e : c->graphs)
+    if (e.alpha == alpha && e.M == M && e.ldM == ldM && e.n == n) g = &e;
+  if (!g) {  // first sight: remember the key, launch directly
+    if (c->graphs.size() >= kMaxGraphs) {
+      size_t old = 0;
+      for (size_t i = 1; i < c->graphs.size(); ++i)
+        if (c->graphs[i].stamp < c->graphs[old].stamp) old = i;
+      if (c->graphs[old].exec) cudaGraphExecDestroy(c->graphs[old].exec);
+      c->graphs.erase(c->graphs.begin() + static_cast<std::ptrdiff_t>(old));
+    }
+    c->graphs.push_back({alpha, M, ldM, n, nullptr, false, ++c->graph_clock});
+    return run_fill(c, alpha, M, ldM, n, st);
+  }
+  g->stamp = ++c->graph_clock;
+  if (g->failed) return run_fill(c, alpha, M, ldM, n, st);
+  if (!g->exec) {
+    if (!c->s_cap && cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking) != cudaSuccess) {
+      g->failed = true;
+      cudaGetLastError();
+      return run_fill(c, alpha, M, ldM, n, st);
+    }
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      const std::string saved = g_last_error;
+      const bool prof = c->prof;
+      c->prof = false;  // no timing events inside the graph
+      ok = run_fill(c, alpha, M, ldM, n, c->s_cap) == P2S_OK;
+      c->prof = prof;
+      ok = (cudaStreamEndCapture(c->s_cap, &graph) == cudaSuccess) && ok && graph != nullptr;
+      if (!ok) g_last_error = saved;
+    }
+    if (ok) ok = cudaGraphInstantiate(&g->exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {
+      g->exec = nullptr;
+      g->failed = true;
+      cudaGetLastError();  // a failed capture is not an error of this call
+      return run_fill(c, alpha, M, ldM, n, st);
+    }
+  }
+  // profiling: one event pair around the whole replayed fill (moments included),
+  // reported as the contraction stage
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->prof) {
+    e0 = take_event(c);
+    e1 = take_event(c);
+    cudaEventRecord(e0, st);
+  }
+  P2S_CUDA(cudaGraphLaunch(g->exec, st));
+  if (c->prof) {
+    cudaEventRecord(e1, st);
+    c->ev_con.emplace_back(e0, e1);
+    ++c->n_con;
   }
   return P2S_OK;
 }
@@ -885,6 +979,7 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
     }
     if (const char* v = opt.get("P2S_LARGE_URESERVE"))  // CTA slots of the persistent u grid left free
       if (c->lpack.u_ctas < 0) c->lpack.u_ctas = -1 - std::max(0, std::atoi(v));
+    if (const char* v = opt.get("P2S_GRAPH")) c->use_graphs = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_VSPLIT")) c->lpack.v_split = std::max(0, std::atoi(v));
     if (const char* v = opt.get("P2S_LARGE_XS")) c->lpack.u_xs = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_UBULK")) c->lpack.u_bulk = v[0] != '0';
@@ -957,6 +1052,9 @@ void p2s_destroy(p2s_ctx* c) {
   if (c->lpack.d_cu) cudaFree(c->lpack.d_cu);
   if (c->lpack.d_cvw) cudaFree(c->lpack.d_cvw);
   if (c->lpack.d_T1) cudaFree(c->lpack.d_T1);
+  for (auto& g : c->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (c->s_cap) cudaStreamDestroy(c->s_cap);
   if (c->lpack.aux) cudaStreamDestroy(c->lpack.aux);
   if (c->lpack.aux_u) cudaStreamDestroy(c->lpack.aux_u);
   if (c->lpack.ev_start) cudaEventDestroy(c->lpack.ev_start);
@@ -1041,6 +1139,7 @@ p2s_status p2s_fill(p2s_ctx* c, const double* d_alpha, double* d_M, int64_t ldM,
   if (!c->fused) {  // two-stage / large paths: moment and intermediate scratch
     ScratchUse use(c, static_cast<cudaStream_t>(stream));
     if (!use.ok()) return fail(P2S_CUDA_ERROR, "p2s_fill: stream ordering");
+    if (c->large) return run_fill_graphed(c, d_alpha, d_M, ldM, n, static_cast<cudaStream_t>(stream));
     return run_fill(c, d_alpha, d_M, ldM, n, static_cast<cudaStream_t>(stream));
   }
   return run_fill(c, d_alpha, d_M, ldM, n, static_cast<cudaStream_t>(stream));

@@ -268,6 +268,17 @@ bool plan_large(const Desc& d, Plan* pl, std::string* why, const Overrides& ov) 
   auto mom_smem = [&](int k) {
     return 8 * (static_cast<int64_t>(k) * d.Q[2] * (d.Q[1] | 1) + static_cast<int64_t>(k) * d.KMAX(1) * (d.Q[2] | 1));
   };
+  if (ov.kc <= 0) {
+    // every k1 chunk re-reads and re-folds the alpha slab: take the largest (even)
+    // chunk whose scratch still lets two CTAs share an SM (80 KB; C5: 4), balanced
+    // over the chunks -- small rules (few quadrature points) get all k1 in one CTA
+    const int kmax0 = d.KMAX(0);
+    int kcmax = 4;
+    for (int k = 4; k <= ((kmax0 + 1) & ~1); k += 2)
+      if (mom_smem(k) <= 80 * 1024) kcmax = k;
+    const int nch = (kmax0 + kcmax - 1) / kcmax;
+    kc = std::max(2, ((kmax0 + nch - 1) / nch + 1) & ~1);
+  }
   while (kc > 2 && mom_smem(kc) > kSmemMax) kc -= 2;
   if (mom_smem(kc) > kSmemMax) {
     *why = "large path: moment scratch above 227 KB";

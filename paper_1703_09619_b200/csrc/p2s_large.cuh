@@ -797,7 +797,6 @@ template <class Ls, bool ROLL = true>
 __global__ void __launch_bounds__(LUXs<Ls>::THREADS, LUXs<Ls>::MINB)
     large_u_xs_kernel(const __grid_constant__ LUParams<Ls> p, int64_t unit0, int64_t ntiles) {
   constexpr int NU = Ls::NU, NV = Ls::NV, NW = Ls::NW, S = Ls::S, T = NV * NW, TPC = LUXs<Ls>::TPC;
-  static_assert(NW % 2 == 0, "bulk-copy rows must be 16-byte multiples");
   extern __shared__ __align__(128) double xsm[];
   // thread group g of the CTA works on tile it * TPC + g; tid = its fiber (n2, p2)
   const int g = TPC == 1 ? 0 : static_cast<int>(threadIdx.x) / T;
@@ -1143,8 +1142,9 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
   constexpr int T = Ls::NV * Ls::NW;
   constexpr int F2 = Ls::NV % 2 == 0 ? 2 : 1;
   constexpr size_t cs = sizeof(double) * Ls::ctot(0);
-  if constexpr (!Ls::u_conforming() && Ls::NW % 2 == 0) {
+  if constexpr (!Ls::u_conforming()) {
 #ifndef P2S_LEAN
+    if constexpr (Ls::NW % 2 == 0)
     if (p.pair) {
       int bps = 0;
       cudaError_t e = kernel_prepare(large_u_pair_kernel<Ls>, LUPair<Ls>::SMEM, LUPair<Ls>::THREADS, false, &bps);
@@ -1155,6 +1155,7 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
       large_u_pair_kernel<Ls><<<pg, LUPair<Ls>::THREADS, LUPair<Ls>::SMEM, st>>>(p, unit0, ntiles);
       return cudaGetLastError();
     }
+    if constexpr (Ls::NW % 2 == 0)
     if (p.bulk) {
       int bps = 0;
       cudaError_t e = kernel_prepare(large_u_bulk_kernel<Ls>, LUBulk<Ls>::SMEM, T, false, &bps);
@@ -1194,7 +1195,7 @@ cudaError_t large_u_dispatch(const LUParams<Ls>& p, int64_t unit0, int64_t cnt, 
   (void)cs;
   (void)F2;
   (void)ps;
-  if constexpr (Ls::u_conforming() || Ls::NW % 2 != 0) {
+  if constexpr (Ls::u_conforming()) {
     using PL = LUPlain<Ls, 1>;
     int bps = 0;
     // an over-size u table is staged in shared memory per (persistent) CTA

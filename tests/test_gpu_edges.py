@@ -201,6 +201,54 @@ def test_two_stage_chunk_pipeline_matches_oracle(env, monkeypatch):
         assert ok, (e, msg)
 
 
+@pytest.mark.parametrize("problem", [
+    (3, (5, 4, 3), [PP, DD], (8, 8, 6)),      # registered large-path test shape
+    (1, (9, 5, 4), [PP, DD], (11, 7, 6)),     # generated module of the large family
+])
+def test_large_path_graph_replay_matches_direct_launches(problem, monkeypatch):
+    """A large-path fill that comes back with the same buffers is captured into a
+    CUDA graph on its second call and replayed from the third: every call gives the
+    oracle's matrices, bitwise equal to a context with graphs off; other buffers
+    and other element counts launch directly (and get their own graphs)."""
+    monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_XCHUNK_MB", "1")  # several chunks
+    if problem[1] == (9, 5, 4):
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_JIT_FAMILY", "large")
+    n = 23
+    o = oracle_for(*problem)
+    alpha_np = o.alpha(O.ALPHA_SINE, 0.5, 3.0, 11, 0, n)
+    alpha = torch.from_numpy(alpha_np).cuda()
+    Mo = o.fill(alpha_np, threads=8)
+    st = torch.cuda.current_stream().cuda_stream
+    ref_ctx = capi.Context(*problem, options={"P2S_GRAPH": "0"})
+    Mref = _nan(n, ref_ctx.n_tot, ref_ctx.n_tot)
+    ref_ctx.fill(alpha, Mref, ref_ctx.n_tot, n, st)
+    torch.cuda.synchronize()
+    ctx = capi.Context(*problem)
+    assert ctx.kernel_path.startswith("large-order"), ctx.kernel_path
+    M = _nan(n, ctx.n_tot, ctx.n_tot)
+    side = torch.cuda.Stream()
+    for call in range(5):  # 0 direct, 1 capture + launch, 2.. replay; call 3 on another stream
+        M.fill_(float("nan"))
+        torch.cuda.synchronize()
+        s = side.cuda_stream if call == 3 else st
+        ctx.fill(alpha, M, ctx.n_tot, n, s)
+        torch.cuda.synchronize()
+        assert torch.equal(M, Mref), f"call {call}"
+    Nt = problem[1][0] * problem[1][1] * problem[1][2]
+    Mg = M.cpu().numpy()
+    for e in range(n):
+        ok, msg, _ = blocks_close(Mg[e], Mo[e], problem[0], Nt)
+        assert ok, (e, msg)
+    # a shorter batch and a second output buffer between replays
+    M2 = _nan(n, ctx.n_tot, ctx.n_tot)
+    for call in range(3):
+        ctx.fill(alpha, M2, ctx.n_tot, n - 5, st)
+        ctx.fill(alpha, M, ctx.n_tot, n, st)
+    torch.cuda.synchronize()
+    assert torch.equal(M2[:n - 5], Mref[:n - 5]) and torch.isnan(M2[n - 5:]).all()
+    assert torch.equal(M, Mref)
+
+
 @pytest.mark.parametrize("name,shift", [("c4", 2), ("c4", 4), ("c2", 2)])
 def test_alpha_alignment_is_checked(name, shift):
     """alpha rows are read with 32-B loads when nq_u % 4 == 0 (C4: nq 16): an
