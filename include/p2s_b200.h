@@ -146,7 +146,11 @@ p2s_status p2s_contract(p2s_ctx* ctx, const double* d_I, double* d_M, int64_t ld
                         int64_t n_elem, void* stream);
 
 /* Both stages over a batch, moments staged in context scratch (chunked so the
- * scratch stays L2-resident). */
+ * scratch stays L2-resident).  Large-order shapes (hundreds of short kernels per
+ * fill): a call that repeats the (d_alpha, d_M, ld_M, n_elem) of an earlier call
+ * is captured into a CUDA graph and replayed from then on -- same kernels, same
+ * results, one cudaGraphLaunch on `stream` (option P2S_GRAPH=0: never; a stream
+ * that is itself being captured launches directly). */
 p2s_status p2s_fill(p2s_ctx* ctx, const double* d_alpha, double* d_M, int64_t ld_M,
                     int64_t n_elem, void* stream);
 
