@@ -54,12 +54,15 @@ const std::vector<FusedEntry>& fused_registry() {
       // 1.105 M), 1 the same at 192 threads, then parity split with all six n1 per tile
       // and 2 fibers / thread (1 CTA of 288 threads per SM, 1.104 M), banded, paired
       // stores, DMMA
+      // (round 2: alpha loads without L1 allocation +2 %; with them the L2 prefetch of
+      // the next unit's alpha, 1.5 % slower in round 1, gains 1.6 %: 1.166 M vs 1.148 M,
+      // tools/gpu_ab_c4pf.sh; variant 7 = prefetch off)
       make_fused<Shape<10, 6, 4, 2, 4, 4, 256, 2, 70, 1, kPPP, kDDD>,
-                 MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>, false, false, false>(),
+                 MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>, false, false, true>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 70, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 256, 2, 1094, 1, kPPP, kDDD>,   // 2: default with L1-allocating alpha loads
-                 MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>>(),
+                 MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>, false, false, false>(),
       make_fused<Shape<10, 6, 4, 6, 4, 4, 288, 1, 70, 2, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 288, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 6, 1, kPPP, kDDD>,
@@ -68,6 +71,9 @@ const std::vector<FusedEntry>& fused_registry() {
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
       make_fused<Shape<10, 6, 4, 2, 4, 4, 192, 2, 22, 1, kPPP, kDDD>,
                  MShape<10, 6, 4, 16, 16, 16, 192, kPPP, kDDD>>(),
+      // C4 default without the L2 prefetch of the next unit's alpha (variant 7)
+      make_fused<Shape<10, 6, 4, 2, 4, 4, 256, 2, 70, 1, kPPP, kDDD>,
+                 MShape<10, 6, 4, 16, 16, 16, 256, kPPP, kDDD>, false, false, false>(),
       // C2 in the conforming basis
       make_fused<Shape<6, 6, 6, 2, 6, 6, 256, 2, 4, 2, kCPPP, kCDDD>,
                  MShape<6, 6, 6, 14, 14, 14, 256, kPPP, kDDD>>(),

@@ -142,7 +142,7 @@ def test_two_stage_contraction_variants_match_oracle(name, variant, monkeypatch)
                 cfg.alpha_hi, n_elem=3, seed=29, threads=16)
 
 
-@pytest.mark.parametrize("name,variant", [(c, v) for c in ("c2", "c3", "c4") for v in range(10)])
+@pytest.mark.parametrize("name,variant", [(c, v) for c in ("c2", "c3", "c4") for v in range(12)])
 def test_every_fused_variant_matches_oracle(name, variant, monkeypatch):
     # every registered fill_fused_kernel variant of the benchmark shapes
     # (P2S_FUSED_VARIANT; indices past the last fall back to the first)
