@@ -977,7 +977,18 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
       const int k = std::atoi(v);
       c->lpack.u_ctas = k < 0 ? -1 : static_cast<int64_t>(k) * c->num_sms;
     }
-    if (const char* v = opt.get("P2S_LARGE_URESERVE"))  // CTA slots of the persistent u grid left free
+    // CTA slots of the persistent u grid left free for the next chunk's w / v steps:
+    // the u stage fills every SM's registers, so those steps otherwise run only in
+    // its tail.  Worth it where they are a large share of the work -- (X + Z) bytes
+    // per unit against the unit's block of M: N = 9 (0.37) +21 % with one slot per
+    // SM, N = 10 (0.31) +5 % and N = 11 (0.27) +3 % with one per two SMs; c12 (0.23)
+    // and C5 (0.15) lose 0-4 % (tools/gpu_sweep_ures.sh, gpu_sweep_r2w.sh)
+    {
+      const double nt = static_cast<double>(spec->order[0]) * spec->order[1] * spec->order[2];
+      const double rho = static_cast<double>(lge->xpu + lge->zpu) / (nt * nt);
+      if (c->lpack.u_ctas < 0 && rho >= 0.25) c->lpack.u_ctas = -1 - (rho >= 0.34 ? c->num_sms : c->num_sms / 2);
+    }
+    if (const char* v = opt.get("P2S_LARGE_URESERVE"))
       if (c->lpack.u_ctas < 0) c->lpack.u_ctas = -1 - std::max(0, std::atoi(v));
     if (const char* v = opt.get("P2S_GRAPH")) c->use_graphs = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_VSPLIT")) c->lpack.v_split = std::max(0, std::atoi(v));

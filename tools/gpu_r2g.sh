@@ -1,8 +1,7 @@
-python -m pytest tests -m gpu -q > gpurun_out/r2g_pytest_gpu.log 2>&1; tail -12 gpurun_out/r2g_pytest_gpu.log
-python bench.py --steps 20 --warmup 5 > gpurun_out/r2g_bench.json 2> gpurun_out/r2g_bench.err; tail -3 gpurun_out/r2g_bench.err
+python -m pytest tests/test_gpu_shapes.py tests/test_gpu_edges.py -m gpu -q -x > gpurun_out/r2g_pytest.log 2>&1; tail -3 gpurun_out/r2g_pytest.log
+python tools/grid_perf.py > gpurun_out/r2g_grid_perf.jsonl 2> gpurun_out/r2g_grid_perf.err; tail -2 gpurun_out/r2g_grid_perf.err
 python -c "
-import json; d=json.loads(open('gpurun_out/r2g_bench.json').read())
-print('c2', round(d['value']), round(d['roofline']['frac'],3), d['parity'], d.get('sustained',{}).get('value'))
-for k,v in d.get('configs',{}).items(): print(k, round(v.get('value',0)), v.get('roofline',{}).get('frac'), v.get('parity',{}).get('ok'), v.get('error'))
-print(d['cpu_baseline'])
+import json
+for l in open('gpurun_out/r2g_grid_perf.jsonl'):
+    d=json.loads(l); print(d['shape'], round(d.get('elem_per_s',0)), round(d.get('frac',0),3), d.get('path','')[:30], d.get('error',''))
 "
