@@ -103,6 +103,25 @@ def test_every_grid_shape_is_supported():
     assert not missing, missing[:5]
 
 
+def test_planner_rules_of_the_generated_families():
+    """The planner's choices for grid shapes whose measured behaviour set the rules
+    (profiles/r2z_sweep_fused.jsonl): small units run as many
+    small CTAs per SM, a two-CTA tile must not starve stage C, the large family's
+    moment kernel takes every k1 of a small rule in one chunk."""
+    from paper_1703_09619_b200 import shape_grid
+    by_id = {shape_grid.shape_id(c): c for c in shape_grid.ALL}  # (modules cached by build())
+    small = capi.shape_prepare(*by_id["1c-1x1x12-DPDRLRDPRLDL-q3x6x16"])
+    assert "fused fill" in small and "64 threads, 8 CTA/SM" in small, small
+    mid = capi.shape_prepare(*by_id["1c-5x5x5-PD-q12x12x12"])
+    assert "192 threads, 3 CTA/SM" in mid, mid
+    wide = capi.shape_prepare(*by_id["1c-12x9x3-RLP-q15x10x4"])
+    assert "n1 tile 9" in wide and "1 CTA/SM" in wide, wide
+    c12 = capi.shape_prepare(*by_id["1c-12x12x12-PD-q18x18x18"])
+    assert c12.startswith("large-order") and "k1 chunks of 12" in c12, c12
+    n18 = capi.shape_prepare(*by_id["1c-18x18x18-PD-q25x25x25"])
+    assert "staged in shared memory" in n18, n18
+
+
 def test_cxx_host_logic_without_gpu():
     """Partition, first-exception rethrow, sizes and nq default of the C++ API
     (tests/cpp/test_wrapper_cpu.cpp), run here without a GPU."""
