@@ -74,7 +74,7 @@ const char* const kOptionKeys[] = {
     "P2S_GEO_MODE",         // geometry fill mode 0 / 1 / 2
     "P2S_XCHUNK_MB",        // large path: intermediate chunk (MB)
     "P2S_LARGE_PS", "P2S_LARGE_OVERLAP", "P2S_LARGE_PRIO", "P2S_LARGE_USTREAMS", "P2S_LARGE_UPERSIST", "P2S_LARGE_URESERVE", "P2S_LARGE_VSPLIT",
-    "P2S_LARGE_XS", "P2S_LARGE_UBULK", "P2S_LARGE_UROLL", "P2S_LARGE_UPAIR", "P2S_LARGE_MSPLIT", "P2S_LARGE_MOMCL", "P2S_LARGE_USMEM", "P2S_LARGE_FIB",
+    "P2S_LARGE_XS", "P2S_LARGE_UBULK", "P2S_LARGE_UROLL", "P2S_LARGE_UPAIR", "P2S_LARGE_MSPLIT", "P2S_LARGE_MOMCL", "P2S_LARGE_MOMG", "P2S_LARGE_MOMT", "P2S_LARGE_MOMW", "P2S_LARGE_USMEM", "P2S_LARGE_FIB",
     "P2S_CHUNK_MB",         // two-stage scheduler chunk (MB of moments)
     "P2S_TWO_STAGE_OVERLAP", "P2S_MOM_PRIO",
     "P2S_HOST_CHUNK_MB",    // p2s_fill_host ring slot (MB of matrices)
@@ -1001,6 +1001,9 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
       c->lpack.t1_units = std::max<int64_t>(1, (int64_t(24) << 20) / (lge->t1u * 8));
       P2S_CUDA(cudaMalloc(&c->lpack.d_T1, sizeof(double) * lge->t1u * c->lpack.t1_units));
     }
+    if (const char* v = opt.get("P2S_LARGE_MOMW")) c->lpack.mom_wfirst = v[0] != '0';
+    if (const char* v = opt.get("P2S_LARGE_MOMT")) c->lpack.mom_tiled = v[0] != '0';
+    if (const char* v = opt.get("P2S_LARGE_MOMG")) c->lpack.mom_grouped = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_MOMCL")) c->lpack.mom_cluster = v[0] == '1';
     if (const char* v = opt.get("P2S_LARGE_USMEM")) c->lpack.u_smemc = v[0] == '1';
     if (const char* v = opt.get("P2S_LARGE_FIB")) c->lpack.ufib = std::atoi(v) == 2 ? 2 : 1;

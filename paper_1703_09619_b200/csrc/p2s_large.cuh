@@ -306,6 +306,658 @@ __global__ void __launch_bounds__(P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM <= 110 * 1
   });
 }
 
+// Grouped moments: same CTA = (unit, term, k1 chunk) and the same folded u pass,
+// but the v and w passes hand out (row, k group) items -- a group is up to KG
+// kernel polynomials of one parity -- instead of one row with all K outputs per
+// thread.  (ncu, C5, r2h: a chunk has K_C Q_w = 144 rows in pass v and K_C K_v =
+// 124 in pass w for 256 threads, so half the warps idled through two of the
+// three passes, each live thread ran a 558-DFMA chain, and 28 % of the executed
+// instructions were UMOV / LDC shuffling 62 uniform registers: 21 % FP64 pipe.)
+// A thread folds its row to the group's parity with one DFMA per pair (sign as a
+// runtime factor: exact, no divergence between groups) and reads its group's
+// table rows from shared memory, so lanes of different groups share the code.
+#ifndef P2S_LARGE_MOMG_THREADS
+#define P2S_LARGE_MOMG_THREADS 288
+#endif
+#ifndef P2S_LARGE_MOMG_KG
+#define P2S_LARGE_MOMG_KG 8
+#endif
+
+template <class Ls>
+struct LMomG {
+  static constexpr int NT = P2S_LARGE_MOMG_THREADS, KG = P2S_LARGE_MOMG_KG;
+  static constexpr int hp(int d) { return (Ls::H(d) + 1) & ~1; }  // table row stride: 16-byte rows
+  static constexpr int groups(int K) { return ((K + 1) / 2 + KG - 1) / KG + (K / 2 + KG - 1) / KG; }
+  static constexpr int T1D = Ls::KC * Ls::Q(2) * Ls::S2, T2D = Ls::KC * Ls::KMAX(1) * Ls::S3;
+  static constexpr int TVO = (T1D + T2D + 1) & ~1;                // staged v table, then the w table
+  // each table is followed by 2 KG pad rows (zeros): a short last group runs all KG chains
+  static constexpr int TWO = TVO + (Ls::KMAX(1) + 2 * KG) * hp(1);
+  static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(TWO + (Ls::KMAX(2) + 2 * KG) * hp(2));
+  static constexpr bool FITS = SMEM <= 227 * 1024;
+  static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;
+};
+
+// outputs of k group g of a[Q] against the staged half table tbs[K][HP]
+template <int Q, int K, int KG, int HP, class Out>
+__device__ __forceinline__ void fold_contract_group(const double (&a)[Q], const double* tbs, int g, Out&& out) {
+  constexpr int Hf = Q / 2, H = (Q + 1) / 2;
+  constexpr int NE = (K + 1) / 2, NO = K / 2, GE = (NE + KG - 1) / KG;
+  const bool odd = g >= GE;
+  const double sg = odd ? -1.0 : 1.0;
+  double f[H];
+#pragma unroll
+  for (int h = 0; h < Hf; ++h) f[h] = fma(sg, a[Q - 1 - h], a[h]);  // a[h] +- a[Q-1-h], one rounding
+  if constexpr (Q & 1) f[Hf] = odd ? 0.0 : a[Hf];                    // centre node: even k only
+  const int gi = odd ? g - GE : g;
+  const int kb = (odd ? 1 : 0) + 2 * KG * gi;
+  const int n = (odd ? NO : NE) - KG * gi;
+  const double* t = tbs + kb * HP;
+  // KG independent accumulation chains (a short last group reads the table's pad rows)
+  double v[KG];
+#pragma unroll
+  for (int i = 0; i < KG; ++i) v[i] = 0.0;
+#pragma unroll
+  for (int h = 0; h < H; ++h)
+#pragma unroll
+    for (int i = 0; i < KG; ++i) v[i] = fma(t[i * 2 * HP + h], f[h], v[i]);
+#pragma unroll
+  for (int i = 0; i < KG; ++i)
+    if (i < n) out(kb + 2 * i, v[i]);
+}
+
+template <class Ls, int s>
+__device__ __forceinline__ void large_moments_g_term(const LMomParams<Ls>& p, const double* a, double* Iout,
+                                                     int chunk, double* sm) {
+  constexpr int QU = Ls::Q(0), QV = Ls::Q(1), QW = Ls::Q(2);
+  constexpr int KU = Ls::K(s, 0), KV = Ls::K(s, 1), KW = Ls::K(s, 2), KC = Ls::KC;
+  constexpr int S2 = Ls::S2, S3 = Ls::S3;
+  using G = LMomG<Ls>;
+  constexpr int NT = G::NT, KG = G::KG;
+  const int k0 = chunk * KC;
+  if (k0 >= KU) return;
+  const int kc = KU - k0 < KC ? KU - k0 : KC;  // live k1 of this chunk
+  double* T1 = sm;             // [KC][QW][S2]
+  double* T2 = sm + G::T1D;    // [KC*KV][S3]
+  const double* tu = p.tab + Ls::ttoff(0) + k0 * Ls::H(0);
+  for_items<QW * QV, NT>([&](int r) {
+    constexpr int Hf = QU / 2, H = (QU + 1) / 2;
+    const int q3 = r / QV, q2 = r - (r / QV) * QV;
+    double x[QU];
+    load_row<QU>(a + static_cast<int64_t>(r) * QU, x);
+    double ev[Hf > 0 ? Hf : 1], od[Hf > 0 ? Hf : 1];
+#pragma unroll
+    for (int h = 0; h < Hf; ++h) {
+      ev[h] = x[h] + x[QU - 1 - h];
+      od[h] = x[h] - x[QU - 1 - h];
+    }
+#pragma unroll
+    for (int j = 0; j < KC; ++j) {  // k1 = k0 + j, k0 even: parity of j = parity of k1
+      double v = 0.0;
+#pragma unroll
+      for (int h = 0; h < Hf; ++h) v = fma(tu[j * H + h], (j & 1) ? od[h] : ev[h], v);
+      if constexpr (QU & 1)
+        if ((j & 1) == 0) v = fma(tu[j * H + Hf], x[Hf], v);
+      T1[(j * QW + q3) * S2 + q2] = v;
+    }
+  });
+  __syncthreads();  // also orders the table staging of the kernel before its first use
+  {
+    const double* tvs = sm + G::TVO;
+    const int rows = kc * QW;
+    for (int it = threadIdx.x; it < rows * G::groups(KV); it += NT) {
+      const int g = it / rows, r = it - g * rows;
+      const int j = r / QW, q3 = r - j * QW;
+      double x[QV];
+#pragma unroll
+      for (int q = 0; q < QV; ++q) x[q] = T1[r * S2 + q];
+      fold_contract_group<QV, KV, KG, G::hp(1)>(x, tvs, g, [&](int k, double v) { T2[(j * KV + k) * S3 + q3] = v; });
+    }
+  }
+  __syncthreads();
+  // pass w: the chunk's outputs are one contiguous run of I; they go to shared
+  // memory first (T1 is free) and leave in one coalesced sweep when they fit
+  constexpr bool kStage = KC * KV * KW <= G::T1D;
+  double* Ic = Iout + static_cast<int64_t>(k0) * KV * KW;
+  {
+    const double* tws = sm + G::TWO;
+    const int rows = kc * KV;  // row r = (j, k2)
+    for (int it = threadIdx.x; it < rows * G::groups(KW); it += NT) {
+      const int g = it / rows, r = it - g * rows;
+      double x[QW];
+#pragma unroll
+      for (int q = 0; q < QW; ++q) x[q] = T2[r * S3 + q];
+      fold_contract_group<QW, KW, KG, G::hp(2)>(x, tws, g, [&](int k, double v) {
+        if constexpr (kStage)
+          T1[r * KW + k] = v;
+        else
+          Ic[r * KW + k] = v;
+      });
+    }
+    if constexpr (kStage) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < rows * KW; i += NT) Ic[i] = T1[i];
+    }
+  }
+}
+
+template <class Ls>
+__global__ void __launch_bounds__(LMomG<Ls>::NT, LMomG<Ls>::MINB)
+    large_moments_g_kernel(const __grid_constant__ LMomParams<Ls> p) {
+  extern __shared__ __align__(16) double sm[];
+  using G = LMomG<Ls>;
+  // half tables of the v and w passes -> shared memory, rows padded to an even length
+  for (int d = 1; d <= 2; ++d) {
+    const int H = d == 1 ? Ls::H(1) : Ls::H(2), HP = d == 1 ? G::hp(1) : G::hp(2);
+    const int K = d == 1 ? Ls::KMAX(1) : Ls::KMAX(2);
+    double* dst = sm + (d == 1 ? G::TVO : G::TWO);
+    const double* src = p.tab + (d == 1 ? Ls::ttoff(1) : Ls::ttoff(2));
+    for (int i = threadIdx.x; i < (K + 2 * G::KG) * HP; i += G::NT) {
+      const int k = i / HP, h = i - k * HP;
+      dst[i] = (h < H && k < K) ? src[k * H + h] : 0.0;
+    }
+  }
+  const int64_t b = blockIdx.x;
+  const int chunk = static_cast<int>(b % Ls::NCH);
+  const int64_t us = b / Ls::NCH;               // (unit, term)
+  const int s = static_cast<int>(us % Ls::S);
+  const int64_t unit = us / Ls::S;
+  constexpr int slab = Ls::Q(0) * Ls::Q(1) * Ls::Q(2);
+  const double* a = p.alpha + us * slab;
+  double* Ib = p.I + unit * Ls::MPP;
+  static_for<0, Ls::S>([&](auto sc) {
+    constexpr int ss = decltype(sc)::value;
+    if (s == ss) large_moments_g_term<Ls, ss>(p, a, Ib + Ls::moff(ss), chunk, sm);
+  });
+}
+
+// Tiled moments: the three passes as register-tiled contractions.  ncu (r2h) on the
+// two kernels above: every DFMA of a one-row-per-thread pass needs its own
+// coefficient operand (LDCU / LDS), and both stall on operand delivery at 21 % of
+// the FP64 pipe whatever the thread mapping.  Here a thread owns TWO rows -- the
+// pair the NEXT pass folds together (q2 / Q_v-1-q2 in pass u, q3 / Q_w-1-q3 in pass
+// v) -- so each coefficient feeds two DFMAs, the producer stores the folded sum and
+// difference (even / odd tables read only their half), and passes v / w block KG
+// kernel polynomials of one parity per thread: 2 x KG accumulators against 2 data +
+// KG coefficient loads per quadrature pair.  Same FMA order per output as the
+// kernels above (bitwise equal moments).
+#ifndef P2S_LARGE_MOMT_THREADS
+#define P2S_LARGE_MOMT_THREADS 224
+#endif
+#ifndef P2S_LARGE_MOMT_KG
+#define P2S_LARGE_MOMT_KG 8
+#endif
+
+template <class Ls>
+struct LMomT {
+  static constexpr int NT = P2S_LARGE_MOMT_THREADS, KG = P2S_LARGE_MOMT_KG;
+  static constexpr int hp(int d) { return (Ls::H(d) + 1) & ~1; }  // table row stride: 16-byte rows
+  // folded-row stride: even (16-byte rows) with stride / 2 odd, so the 16-byte loads
+  // of eight consecutive rows fall into eight different bank groups
+  static constexpr int rs(int d) {
+    const int r = (Ls::H(d) + 1) & ~1;
+    return (r / 2) % 2 ? r : r + 2;
+  }
+  static constexpr int groups(int K) { return ((K + 1) / 2 + KG - 1) / KG + (K / 2 + KG - 1) / KG; }
+  static constexpr int T1H = Ls::KC * Ls::Q(2) * rs(1);       // T1 even part, then the odd part
+  static constexpr int T2H = Ls::KC * Ls::KMAX(1) * rs(2);    // T2 even part, then the odd part
+  static constexpr int TVO = 2 * T1H + 2 * T2H;
+  static constexpr int TWO = TVO + (Ls::KMAX(1) + 2 * KG) * hp(1);  // 2 KG zero pad rows per table
+  static constexpr int TUO = TWO + (Ls::KMAX(2) + 2 * KG) * hp(2);  // the chunk's KC rows of the u table
+  static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(TUO + Ls::KC * hp(0));
+  static constexpr bool FITS = SMEM <= 227 * 1024;
+  static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;
+};
+
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
+// va[i], vb[i] = sum_h t[2 i][h] * fa[h], fb[h]  (two folded rows, KG table rows of one parity)
+template <int H, int KG, int HP>
+__device__ __forceinline__ void mom_tile2(const double* fa, const double* fb, const double* t,
+                                          double (&va)[KG], double (&vb)[KG]) {
+#pragma unroll
+  for (int i = 0; i < KG; ++i) va[i] = vb[i] = 0.0;
+#pragma unroll
+  for (int h2 = 0; h2 < H / 2; ++h2) {
+    const double2 a = lds2(fa + 2 * h2), b = lds2(fb + 2 * h2);
+#pragma unroll
+    for (int i = 0; i < KG; ++i) {
+      const double2 c = lds2(t + i * 2 * HP + 2 * h2);
+      va[i] = fma(c.x, a.x, va[i]);
+      vb[i] = fma(c.x, b.x, vb[i]);
+      va[i] = fma(c.y, a.y, va[i]);
+      vb[i] = fma(c.y, b.y, vb[i]);
+    }
+  }
+  if constexpr (H & 1) {
+    const double a = fa[H - 1], b = fb[H - 1];
+#pragma unroll
+    for (int i = 0; i < KG; ++i) {
+      const double c = t[i * 2 * HP + H - 1];
+      va[i] = fma(c, a, va[i]);
+      vb[i] = fma(c, b, vb[i]);
+    }
+  }
+}
+
+// W adjacent doubles of an alpha row (W = 4: 32-byte, 2: 16-byte, 1), schedulable loads
+template <int W>
+__device__ __forceinline__ void ld_chunk(const double* p, double (&x)[W]) {
+  if constexpr (W == 4) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
+                 : "l"(p));
+  } else if constexpr (W == 2) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    x[0] = v.x;
+    x[1] = v.y;
+  } else {
+    x[0] = __ldg(p);
+  }
+}
+
+template <class Ls, int s>
+__device__ __forceinline__ void large_moments_t_term(const LMomParams<Ls>& p, const double* a, double* Iout,
+                                                     int chunk, double* sm) {
+  constexpr int QU = Ls::Q(0), QV = Ls::Q(1), QW = Ls::Q(2);
+  constexpr int HU = Ls::H(0), HV = Ls::H(1), HW = Ls::H(2);
+  constexpr int KU = Ls::K(s, 0), KV = Ls::K(s, 1), KW = Ls::K(s, 2), KC = Ls::KC;
+  using G = LMomT<Ls>;
+  constexpr int NT = G::NT, KG = G::KG, RS1 = G::rs(1), RS2 = G::rs(2);
+  const int k0 = chunk * KC;
+  if (k0 >= KU) return;
+  const int kc = KU - k0 < KC ? KU - k0 : KC;  // live k1 of this chunk
+  double* T1e = sm;                 // [KC][QW][RS1]: sum of the rows q2, Q_v-1-q2 (h = q2 < H_v)
+  double* T1o = sm + G::T1H;        //                difference
+  double* T2e = sm + 2 * G::T1H;    // [KC * KV][RS2]: sum / difference of q3, Q_w-1-q3
+  double* T2o = T2e + G::T2H;
+  // ---- pass u: item = (q3, h2): alpha rows (q3, h2) and (q3, Q_v-1-h2), KC outputs each
+  {
+    constexpr int W = QU % 4 == 0 ? 4 : QU % 2 == 0 ? 2 : 1;
+    constexpr int Hf = QU / 2, NCK = (Hf + W - 1) / W;
+    constexpr int PD = NCK < 3 ? NCK : 3;  // chunks of loads in flight ahead of the arithmetic
+    constexpr int HPU = G::hp(0);
+    const double* tu = sm + G::TUO;        // [KC][HPU], staged by the kernel (uniform-address LDS)
+    for_items<QW * HV, NT>([&](int item) {
+      const int q3 = item / HV, h2 = item - (item / HV) * HV;
+      const int q2b = QV - 1 - h2;
+      const double* A = a + static_cast<int64_t>(q3 * QV + h2) * QU;
+      const double* B = a + static_cast<int64_t>(q3 * QV + q2b) * QU;
+      double vA[KC], vB[KC];
+#pragma unroll
+      for (int j = 0; j < KC; ++j) vA[j] = vB[j] = 0.0;
+      // chunk c = the W values from h = W c of both rows and their mirror images
+      double af[NCK][W], ab[NCK][W], bf[NCK][W], bb[NCK][W];
+      auto issue = [&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+#ifdef P2S_MOMT_FAKE_COALESCED  // timing experiment only (wrong data): lane-consecutive 32-byte pieces
+        const double* F = a + (item % NT) * W + (item / NT) * 36864;
+        ld_chunk<W>(F + (4 * c + 0) * 1024, af[c]);
+        ld_chunk<W>(F + (4 * c + 1) * 1024, ab[c]);
+        ld_chunk<W>(F + (4 * c + 2) * 1024, bf[c]);
+        ld_chunk<W>(F + (4 * c + 3) * 1024, bb[c]);
+#else
+        ld_chunk<W>(A + W * c, af[c]);
+        ld_chunk<W>(A + QU - W - W * c, ab[c]);
+        ld_chunk<W>(B + W * c, bf[c]);
+        ld_chunk<W>(B + QU - W - W * c, bb[c]);
+#endif
+      };
+      static_for<0, PD>([&](auto cc) { issue(cc); });
+      static_for<0, NCK>([&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+        if constexpr (c + PD < NCK) issue(std::integral_constant<int, c + PD>{});
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const int h = W * c + w;
+          if (h < Hf) {
+            const double ae = af[c][w] + ab[c][W - 1 - w], ao = af[c][w] - ab[c][W - 1 - w];
+            const double be = bf[c][w] + bb[c][W - 1 - w], bo = bf[c][w] - bb[c][W - 1 - w];
+#pragma unroll
+            for (int j = 0; j < KC; ++j) {  // k1 = k0 + j, k0 even: parity of j = parity of k1
+              const double cf = tu[j * HPU + h];
+              vA[j] = fma(cf, (j & 1) ? ao : ae, vA[j]);
+              vB[j] = fma(cf, (j & 1) ? bo : be, vB[j]);
+            }
+          }
+        }
+      });
+      if constexpr (QU & 1) {  // centre node: even k only
+        const double ac = __ldg(A + Hf), bc = __ldg(B + Hf);
+#pragma unroll
+        for (int j = 0; j < KC; j += 2) {
+          vA[j] = fma(tu[j * HPU + Hf], ac, vA[j]);
+          vB[j] = fma(tu[j * HPU + Hf], bc, vB[j]);
+        }
+      }
+      const double cb = h2 == q2b ? 0.0 : 1.0;  // centre row of an odd rule: the row itself, no partner
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        T1e[(j * QW + q3) * RS1 + h2] = fma(cb, vB[j], vA[j]);
+        T1o[(j * QW + q3) * RS1 + h2] = vA[j] - vB[j];
+      }
+    });
+  }
+  __syncthreads();  // also orders the kernel's table staging before its first use
+  // ---- pass v: item = (j, h3, k2 group): T1 rows q3 = h3 and Q_w-1-h3
+  {
+    constexpr int NE = (KV + 1) / 2, NO = KV / 2, GE = (NE + KG - 1) / KG, HP = G::hp(1);
+    const double* tvs = sm + G::TVO;
+    const int rows = kc * HW;
+    for (int it = threadIdx.x; it < rows * G::groups(KV); it += NT) {
+      const int g = it / rows, r = it - g * rows;
+      const int j = r / HW, h3 = r - j * HW;
+      const int q3b = QW - 1 - h3;
+      const bool odd = g >= GE;
+      const int gi = odd ? g - GE : g;
+      const int kb = (odd ? 1 : 0) + 2 * KG * gi;
+      const int n = (odd ? NO : NE) - KG * gi;
+      const double* src = (odd ? T1o : T1e) + j * QW * RS1;
+      double va[KG], vb[KG];
+      mom_tile2<HV, KG, HP>(src + h3 * RS1, src + q3b * RS1, tvs + kb * HP, va, vb);
+      const double cb = h3 == q3b ? 0.0 : 1.0;
+#pragma unroll
+      for (int i = 0; i < KG; ++i)
+        if (i < n) {
+          const int o = (j * KV + kb + 2 * i) * RS2 + h3;
+          T2e[o] = fma(cb, vb[i], va[i]);
+          T2o[o] = va[i] - vb[i];
+        }
+    }
+  }
+  __syncthreads();
+  // ---- pass w: item = (row pair, k3 group), rows (j, k2) = r and r + ceil(R / 2); the
+  // chunk's outputs are one contiguous run of I: through shared memory (T1 is free)
+  // and out in one coalesced sweep when they fit
+  constexpr bool kStage = KC * KV * KW <= 2 * G::T1H;
+  double* Ic = Iout + static_cast<int64_t>(k0) * KV * KW;
+  {
+    constexpr int NE = (KW + 1) / 2, NO = KW / 2, GE = (NE + KG - 1) / KG, HP = G::hp(2);
+    const double* tws = sm + G::TWO;
+    const int R = kc * KV, RH = (R + 1) / 2;
+    double* dst = kStage ? sm : Ic;
+    for (int it = threadIdx.x; it < RH * G::groups(KW); it += NT) {
+      const int g = it / RH, ra = it - g * RH;
+      const bool live_b = ra + RH < R;
+      const int rb = live_b ? ra + RH : ra;
+      const bool odd = g >= GE;
+      const int gi = odd ? g - GE : g;
+      const int kb = (odd ? 1 : 0) + 2 * KG * gi;
+      const int n = (odd ? NO : NE) - KG * gi;
+      const double* src = odd ? T2o : T2e;
+      double va[KG], vb[KG];
+      mom_tile2<HW, KG, HP>(src + ra * RS2, src + rb * RS2, tws + kb * HP, va, vb);
+#pragma unroll
+      for (int i = 0; i < KG; ++i)
+        if (i < n) {
+          dst[ra * KW + kb + 2 * i] = va[i];
+          if (live_b) dst[rb * KW + kb + 2 * i] = vb[i];
+        }
+    }
+    if constexpr (kStage) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < R * KW; i += NT) Ic[i] = sm[i];
+    }
+  }
+}
+
+template <class Ls>
+__global__ void __launch_bounds__(LMomT<Ls>::NT, LMomT<Ls>::MINB)
+    large_moments_t_kernel(const __grid_constant__ LMomParams<Ls> p) {
+  extern __shared__ __align__(16) double sm[];
+  using G = LMomT<Ls>;
+  const int64_t b = blockIdx.x;
+  const int chunk = static_cast<int>(b % Ls::NCH);
+  // half tables of the v and w passes and the chunk's rows of the u table -> shared
+  // memory, rows padded to an even length (independent loads: the trip counts are
+  // compile-time, so the constant-bank latencies overlap)
+  static_for<0, 3>([&](auto dc) {
+    constexpr int d = decltype(dc)::value;
+    constexpr int H = Ls::H(d), HP = G::hp(d);
+    constexpr int K = d == 0 ? Ls::KC : Ls::KMAX(d), ROWS = d == 0 ? Ls::KC : K + 2 * G::KG;
+    double* dst = sm + (d == 0 ? G::TUO : d == 1 ? G::TVO : G::TWO);
+    const double* src = p.tab + Ls::ttoff(d) + (d == 0 ? chunk * Ls::KC * H : 0);
+    const int kmax = d == 0 ? Ls::KMAX(0) - chunk * Ls::KC : K;  // rows past the table: zeros
+#pragma unroll
+    for (int i0 = 0; i0 < ROWS * HP; i0 += G::NT) {
+      const int i = i0 + static_cast<int>(threadIdx.x);
+      const int k = i / HP, h = i - k * HP;
+      if (i < ROWS * HP) dst[i] = (h < H && k < kmax) ? src[k * H + h] : 0.0;
+    }
+  });
+  __syncthreads();  // pass u reads the staged u rows
+  const int64_t us = b / Ls::NCH;               // (unit, term)
+  const int s = static_cast<int>(us % Ls::S);
+  const int64_t unit = us / Ls::S;
+  constexpr int slab = Ls::Q(0) * Ls::Q(1) * Ls::Q(2);
+  const double* a = p.alpha + us * slab;
+  double* Ib = p.I + unit * Ls::MPP;
+  static_for<0, Ls::S>([&](auto sc) {
+    constexpr int ss = decltype(sc)::value;
+    if (s == ss) large_moments_t_term<Ls, ss>(p, a, Ib + Ls::moff(ss), chunk, sm);
+  });
+}
+
+// w-first tiled moments: as the tiled kernel, but the first pass contracts the
+// SLOWEST direction (q3) and the CTA's chunk is KC kernel polynomials along w.
+// Pass u of the kernels above gives every lane its own 288-byte alpha row: each
+// 32-byte sector is its own L2 request (ncu r2h: 47.8 M sector requests, 0.8 % L1
+// hits, 11.8 wavefronts per load instruction), and four differently organised
+// kernels all ran C5 at 1.13-1.29 us per element; the tiled kernel with the same
+// sectors read lane-contiguously (wrong data, timing only: -DP2S_MOMT_FAKE_COALESCED)
+// ran at 0.85.  Here a thread owns the column pair (q2; q1 = h, Q_u-1-h) and walks
+// q3: consecutive lanes read consecutive doubles of an alpha row.  Then pass u
+// (over q1, rows folded by the first pass) and pass v (over q2) as tiles; the
+// chunk's outputs I[k1][k2][k0..k0+KC) leave through shared memory.  The sums run
+// w, u, v instead of u, v, w: same values to rounding (tests: 1e-12), not bitwise.
+#ifndef P2S_LARGE_MOMW_PD
+#define P2S_LARGE_MOMW_PD 4
+#endif
+
+template <class Ls>
+struct LMomW {
+  static constexpr int KG = P2S_LARGE_MOMT_KG, KC = Ls::KC;
+  static constexpr int hp(int d) { return LMomT<Ls>::hp(d); }
+  static constexpr int rs(int d) { return LMomT<Ls>::rs(d); }
+  static constexpr int groups(int K) { return LMomT<Ls>::groups(K); }
+  static constexpr int NCH = (Ls::KMAX(2) + KC - 1) / KC;        // k3 chunks
+  static constexpr int T1H = KC * Ls::Q(1) * rs(0);              // [KC][QV][rs(0)]: q1 folded (even, then odd)
+  static constexpr int T2H = KC * Ls::KMAX(0) * rs(1);           // [KC * KU][rs(1)]: q2 folded
+  static constexpr int TUO = 2 * T1H + 2 * T2H;                  // u table, 2 KG zero pad rows
+  static constexpr int TVO = TUO + (Ls::KMAX(0) + 2 * KG) * hp(0);
+  static constexpr int TWO = TVO + (Ls::KMAX(1) + 2 * KG) * hp(1);  // the chunk's w rows, [H_w][KC]
+  static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(TWO + Ls::H(2) * KC);
+  static constexpr bool FITS = SMEM <= 227 * 1024;
+  static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;
+  // two CTAs of 224 threads per SM (144-register cap), or one of 352 when the chunk's scratch needs the SM
+  static constexpr int NT = MINB == 2 ? P2S_LARGE_MOMT_THREADS : 352;
+};
+
+__device__ __forceinline__ double ld_nc_v(const double* p) {  // issue order = source order
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+template <class Ls, int s>
+__device__ __forceinline__ void large_moments_w_term(const LMomParams<Ls>& p, const double* a, double* Iout,
+                                                     int chunk, double* sm) {
+  constexpr int QU = Ls::Q(0), QV = Ls::Q(1), QW = Ls::Q(2);
+  constexpr int HU = Ls::H(0), HV = Ls::H(1);
+  constexpr int KU = Ls::K(s, 0), KV = Ls::K(s, 1), KW = Ls::K(s, 2), KC = Ls::KC;
+  using G = LMomW<Ls>;
+  constexpr int NT = G::NT, KG = G::KG, RS0 = G::rs(0), RS1 = G::rs(1);
+  const int k0 = chunk * KC;
+  if (k0 >= KW) return;
+  const int kc = KW - k0 < KC ? KW - k0 : KC;  // live k3 of this chunk
+  double* T1e = sm;
+  double* T1o = sm + G::T1H;
+  double* T2e = sm + 2 * G::T1H;
+  double* T2o = T2e + G::T2H;
+  // ---- pass w: item = (q2, h1): columns q1 = h1 and Q_u-1-h1 of alpha row q2, all q3
+  {
+    constexpr int Hf = QW / 2, PD = Hf < P2S_LARGE_MOMW_PD ? Hf : P2S_LARGE_MOMW_PD;  // q3 pairs in flight
+    constexpr int64_t PS = static_cast<int64_t>(QV) * QU;  // plane stride
+    const double* tw = sm + G::TWO;                         // [H_w][KC]
+    for_items<QV * HU, NT>([&](int item) {
+      const int q2 = item / HU, h1 = item - (item / HU) * HU;
+      const int q1b = QU - 1 - h1;
+      const double* Pa = a + q2 * QU + h1;
+      const double* Pb = a + q2 * QU + q1b;
+      double wA[KC], wB[KC];
+#pragma unroll
+      for (int j = 0; j < KC; ++j) wA[j] = wB[j] = 0.0;
+      double xa0[Hf > 0 ? Hf : 1], xa1[Hf > 0 ? Hf : 1], xb0[Hf > 0 ? Hf : 1], xb1[Hf > 0 ? Hf : 1];
+      auto issue = [&](auto hc) {
+        constexpr int h = decltype(hc)::value;
+        xa0[h] = ld_nc_v(Pa + h * PS);
+        xb0[h] = ld_nc_v(Pb + h * PS);
+        xa1[h] = ld_nc_v(Pa + (QW - 1 - h) * PS);
+        xb1[h] = ld_nc_v(Pb + (QW - 1 - h) * PS);
+      };
+      static_for<0, PD>([&](auto hc) { issue(hc); });
+      static_for<0, Hf>([&](auto hc) {
+        constexpr int h = decltype(hc)::value;
+        if constexpr (h + PD < Hf) issue(std::integral_constant<int, h + PD>{});
+        const double ea = xa0[h] + xa1[h], oa = xa0[h] - xa1[h];
+        const double eb = xb0[h] + xb1[h], ob = xb0[h] - xb1[h];
+#pragma unroll
+        for (int j = 0; j < KC; ++j) {  // k3 = k0 + j, k0 even: parity of j = parity of k3
+          const double cf = tw[h * KC + j];
+          wA[j] = fma(cf, (j & 1) ? oa : ea, wA[j]);
+          wB[j] = fma(cf, (j & 1) ? ob : eb, wB[j]);
+        }
+      });
+      if constexpr (QW & 1) {  // centre plane: even k only
+        const double ac = __ldg(Pa + Hf * PS), bc = __ldg(Pb + Hf * PS);
+#pragma unroll
+        for (int j = 0; j < KC; j += 2) {
+          wA[j] = fma(tw[Hf * KC + j], ac, wA[j]);
+          wB[j] = fma(tw[Hf * KC + j], bc, wB[j]);
+        }
+      }
+      const double cb = h1 == q1b ? 0.0 : 1.0;  // centre column of an odd rule: no partner
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        T1e[(j * QV + q2) * RS0 + h1] = fma(cb, wB[j], wA[j]);
+        T1o[(j * QV + q2) * RS0 + h1] = wA[j] - wB[j];
+      }
+    });
+  }
+  // u and v half tables (rows padded to an even length, 2 KG zero rows behind) -> shared memory
+  static_for<0, 2>([&](auto dc) {
+    constexpr int d = decltype(dc)::value;
+    constexpr int H = Ls::H(d), HP = G::hp(d), K = Ls::KMAX(d), ROWS = K + 2 * G::KG;
+    double* dst = sm + (d == 0 ? G::TUO : G::TVO);
+    const double* src = p.tab + Ls::ttoff(d);
+#pragma unroll
+    for (int i0 = 0; i0 < ROWS * HP; i0 += G::NT) {
+      const int i = i0 + static_cast<int>(threadIdx.x);
+      const int k = i / HP, h = i - k * HP;
+      if (i < ROWS * HP) dst[i] = (h < H && k < K) ? src[k * H + h] : 0.0;
+    }
+  });
+  __syncthreads();
+  // ---- pass u: item = (j, h2, k1 group): T1 rows q2 = h2 and Q_v-1-h2
+  {
+    constexpr int NE = (KU + 1) / 2, NO = KU / 2, GE = (NE + KG - 1) / KG, HP = G::hp(0);
+    const double* tus = sm + G::TUO;
+    const int rows = kc * HV;
+    for (int it = threadIdx.x; it < rows * G::groups(KU); it += NT) {
+      const int g = it / rows, r = it - g * rows;
+      const int j = r / HV, h2 = r - j * HV;
+      const int q2b = QV - 1 - h2;
+      const bool odd = g >= GE;
+      const int gi = odd ? g - GE : g;
+      const int kb = (odd ? 1 : 0) + 2 * KG * gi;
+      const int n = (odd ? NO : NE) - KG * gi;
+      const double* src = (odd ? T1o : T1e) + j * QV * RS0;
+      double va[KG], vb[KG];
+      mom_tile2<HU, KG, HP>(src + h2 * RS0, src + q2b * RS0, tus + kb * HP, va, vb);
+      const double cb = h2 == q2b ? 0.0 : 1.0;
+#pragma unroll
+      for (int i = 0; i < KG; ++i)
+        if (i < n) {
+          const int o = (j * KU + kb + 2 * i) * RS1 + h2;
+          T2e[o] = fma(cb, vb[i], va[i]);
+          T2o[o] = va[i] - vb[i];
+        }
+    }
+  }
+  __syncthreads();
+  // ---- pass v: item = (row pair, k2 group), rows (j, k1) = r and r + ceil(R / 2); the
+  // outputs I[k1][k2][k0 + j] go through shared memory (T1 is free) when they fit
+  constexpr bool kStage = KC * KU * KV <= 2 * G::T1H;
+  {
+    constexpr int NE = (KV + 1) / 2, NO = KV / 2, GE = (NE + KG - 1) / KG, HP = G::hp(1);
+    const double* tvs = sm + G::TVO;
+    const int R = kc * KU, RH = (R + 1) / 2;
+    for (int it = threadIdx.x; it < RH * G::groups(KV); it += NT) {
+      const int g = it / RH, ra = it - g * RH;
+      const bool live_b = ra + RH < R;
+      const int rb = live_b ? ra + RH : ra;
+      const bool odd = g >= GE;
+      const int gi = odd ? g - GE : g;
+      const int kb = (odd ? 1 : 0) + 2 * KG * gi;
+      const int n = (odd ? NO : NE) - KG * gi;
+      const double* src = odd ? T2o : T2e;
+      double va[KG], vb[KG];
+      mom_tile2<HV, KG, HP>(src + ra * RS1, src + rb * RS1, tvs + kb * HP, va, vb);
+      const int ja = ra / KU, k1a = ra - ja * KU, jb = rb / KU, k1b = rb - jb * KU;
+#pragma unroll
+      for (int i = 0; i < KG; ++i)
+        if (i < n) {
+          const int k2 = kb + 2 * i;
+          if constexpr (kStage) {
+            sm[(k1a * KV + k2) * KC + ja] = va[i];
+            if (live_b) sm[(k1b * KV + k2) * KC + jb] = vb[i];
+          } else {
+            Iout[(k1a * KV + k2) * KW + k0 + ja] = va[i];
+            if (live_b) Iout[(k1b * KV + k2) * KW + k0 + jb] = vb[i];
+          }
+        }
+    }
+    if constexpr (kStage) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < KU * KV * KC; i += NT) {
+        const int e = i / KC, j = i - e * KC;
+        if (j < kc) Iout[e * KW + k0 + j] = sm[i];
+      }
+    }
+  }
+}
+
+template <class Ls>
+__global__ void __launch_bounds__(LMomW<Ls>::NT, LMomW<Ls>::MINB)
+    large_moments_w_kernel(const __grid_constant__ LMomParams<Ls> p) {
+  extern __shared__ __align__(16) double sm[];
+  using G = LMomW<Ls>;
+  const int64_t b = blockIdx.x;
+  const int chunk = static_cast<int>(b % G::NCH);
+  // the chunk's rows of the w table, transposed to [h][j], -> shared memory (the u and
+  // v tables follow behind pass w, off the start of the CTA)
+  {
+    constexpr int H = Ls::H(2), KC = Ls::KC;
+    const double* src = p.tab + Ls::ttoff(2);
+#pragma unroll
+    for (int i0 = 0; i0 < H * KC; i0 += G::NT) {
+      const int i = i0 + static_cast<int>(threadIdx.x);
+      const int h = i / KC, j = i - h * KC;
+      if (i < H * KC) sm[G::TWO + i] = chunk * KC + j < Ls::KMAX(2) ? src[(chunk * KC + j) * H + h] : 0.0;
+    }
+  }
+  __syncthreads();  // pass w reads the staged w rows
+  const int64_t us = b / G::NCH;                // (unit, term)
+  const int s = static_cast<int>(us % Ls::S);
+  const int64_t unit = us / Ls::S;
+  constexpr int slab = Ls::Q(0) * Ls::Q(1) * Ls::Q(2);
+  const double* a = p.alpha + us * slab;
+  double* Ib = p.I + unit * Ls::MPP;
+  static_for<0, Ls::S>([&](auto sc) {
+    constexpr int ss = decltype(sc)::value;
+    if (s == ss) large_moments_w_term<Ls, ss>(p, a, Ib + Ls::moff(ss), chunk, sm);
+  });
+}
+
 // Split moments (default): the u pass of every (unit, term) computes ALL its
 // K_u outputs per alpha row at once -- each row is read and folded once, 18 FMAs
 // per k1 against 36 loaded values instead of 4 k1 per pass -- into a

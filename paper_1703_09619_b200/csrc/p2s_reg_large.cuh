@@ -109,6 +109,25 @@ cudaError_t launch_large_moments(const double* alpha, double* I, int64_t n_units
     return cudaLaunchKernelEx(&cfg, large_moments_kernel<Ls, true>, p);
   }
 #endif
+  if constexpr (LMomW<Ls>::FITS)
+    if (pk.mom_wfirst) {
+      if ((e = kernel_prepare(large_moments_w_kernel<Ls>, LMomW<Ls>::SMEM, LMomW<Ls>::NT)) != cudaSuccess) return e;
+      large_moments_w_kernel<Ls><<<static_cast<unsigned>(n_units * Ls::S * LMomW<Ls>::NCH), LMomW<Ls>::NT,
+                                   LMomW<Ls>::SMEM, st>>>(p);
+      return cudaGetLastError();
+    }
+  if constexpr (LMomT<Ls>::FITS)
+    if (pk.mom_tiled) {
+      if ((e = kernel_prepare(large_moments_t_kernel<Ls>, LMomT<Ls>::SMEM, LMomT<Ls>::NT)) != cudaSuccess) return e;
+      large_moments_t_kernel<Ls><<<grid, LMomT<Ls>::NT, LMomT<Ls>::SMEM, st>>>(p);
+      return cudaGetLastError();
+    }
+  if constexpr (LMomG<Ls>::FITS)
+    if (pk.mom_grouped) {
+      if ((e = kernel_prepare(large_moments_g_kernel<Ls>, LMomG<Ls>::SMEM, LMomG<Ls>::NT)) != cudaSuccess) return e;
+      large_moments_g_kernel<Ls><<<grid, LMomG<Ls>::NT, LMomG<Ls>::SMEM, st>>>(p);
+      return cudaGetLastError();
+    }
   large_moments_kernel<Ls><<<grid, P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM, st>>>(p);
   return cudaGetLastError();
 }

@@ -120,6 +120,10 @@ struct LargePack {
   bool u_pair = false;               // P2S_LARGE_UPAIR: two adjacent fibers per u-stage thread
                                      // (measured slower: c12 0.53 vs 0.58, C5 0.59 vs 0.65 of HBM)
   int u_roll = 1;                    // P2S_LARGE_UROLL: runtime row loop (1) or unrolled rows (0, slower)
+  bool mom_wfirst = true;            // P2S_LARGE_MOMW: w-first register-tiled moment kernel (coalesced alpha reads;
+                                     // C5 1.00 vs 1.24 us per element); 0: the u-first kernel, one row per thread
+  bool mom_tiled = false;            // P2S_LARGE_MOMT: register-tiled passes (two rows x KG polynomials per thread)
+  bool mom_grouped = false;          // P2S_LARGE_MOMG: (row, k group) items in the v / w passes, staged tables
   bool mom_cluster = false;          // P2S_LARGE_MOMCL: one cluster per (unit, term), alpha read once (0.77 vs 0.71 ms: slower)
   bool u_smemc = false;              // P2S_LARGE_USMEM (measured 28.1 k vs 28.4 k elem/s constant-bank)
   // runtime: parity-split u stage; v/w of chunk i+1 on `aux` overlapping u of

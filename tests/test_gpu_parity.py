@@ -105,12 +105,21 @@ def test_moments_match_oracle():
 
 
 @pytest.mark.parametrize("name,variant", [("c3", v) for v in range(5)] + [("c4", v) for v in range(3)]
-                         + [("c2", v) for v in range(3)] + [("c5", 0), ("c5", "cluster")])
+                         + [("c2", v) for v in range(3)] + [("c5", 0), ("c5", "cluster"), ("c5", "grouped"), ("c5", "tiled"), ("c5", "ufirst")])
 def test_moment_kernel_variants_match_oracle(name, variant, monkeypatch):
     # every registered moments_v2 thread-count variant (P2S_MV2_VARIANT) and the
     # large-order moment kernel (both modes) reproduce the oracle's moment integrals
     if variant == "cluster":
         monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_LARGE_MOMCL", "1")
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_LARGE_MOMW", "0")
+    elif variant == "grouped":
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_LARGE_MOMG", "1")
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_LARGE_MOMW", "0")
+    elif variant == "tiled":
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_LARGE_MOMT", "1")
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_LARGE_MOMW", "0")
+    elif variant == "ufirst":
+        monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_LARGE_MOMW", "0")
     else:
         monkeypatch.setitem(capi.DEFAULT_OPTIONS, "P2S_MV2_VARIANT", str(variant))
     cfg = CONFIGS[name]
@@ -277,7 +286,10 @@ def test_large_order_path_small_shape(n_comp):
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_UPERSIST": "1"},      # persistent u stage, 1 CTA / SM
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_UPERSIST": "0"},      # one u-stage CTA per tile
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_USMEM": "1"},         # u coefficients in shared memory
-    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_MOMCL": "1"},         # cluster moments (DSMEM)
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_MOMCL": "1", "P2S_LARGE_MOMW": "0"},  # cluster moments (DSMEM)
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_MOMG": "1", "P2S_LARGE_MOMW": "0"},   # grouped v / w moment passes
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_MOMT": "1", "P2S_LARGE_MOMW": "0"},   # register-tiled moment passes (u first)
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_MOMW": "0"},          # u-first moment kernel, one row per thread
 ])
 def test_large_order_path_chunk_schedules(env, monkeypatch):
     # the chunked v/w -> u pipeline over many X chunks (double buffer reuse,

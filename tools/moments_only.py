@@ -1,9 +1,11 @@
+"""Moment kernel only (a target for ncu): python tools/moments_only.py <config> <elements> [KEY=VALUE options ...]"""
 import sys, torch
 sys.path.insert(0, '.')
 from paper_1703_09619_b200 import capi
 from paper_1703_09619_b200.configs import CONFIGS
 cfg = CONFIGS[sys.argv[1]]
-ctx = capi.Context(**cfg.problem())
+opts = dict(kv.split("=", 1) for kv in sys.argv[3:])
+ctx = capi.Context(**cfg.problem(), options=opts)
 E = int(sys.argv[2])
 st = torch.cuda.current_stream().cuda_stream
 a = torch.empty((E, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")

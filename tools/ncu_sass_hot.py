@@ -11,7 +11,7 @@ txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(txt)))
 h = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
 hdr = rows[h]
-recs = [dict(zip(hdr, r)) for r in rows[h + 1:] if len(r) == len(hdr)]
+recs = [dict(zip(hdr, r)) for r in rows[h + 1:] if len(r) == len(hdr) and r[0] != "Address"]
 tot = sum(int(r["Warp Stall Sampling (All Samples)"]) for r in recs) or 1
 stall_cols = [c for c in hdr if c.startswith("stall_") and "Not Issued" not in c]
 agg = {c: sum(int(r[c]) for r in recs) for c in stall_cols}
