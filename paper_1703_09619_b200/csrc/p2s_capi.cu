@@ -1001,6 +1001,10 @@ p2s_status p2s_create_ex(const p2s_problem* spec_in, int device, const char* opt
       c->lpack.t1_units = std::max<int64_t>(1, (int64_t(24) << 20) / (lge->t1u * 8));
       P2S_CUDA(cudaMalloc(&c->lpack.d_T1, sizeof(double) * lge->t1u * c->lpack.t1_units));
     }
+    // moment kernel: the w-first tiled kernel where its first pass has at least two warps
+    // of (q2, q1 pair) columns per CTA; rules with few points along u / v keep the u-first
+    // kernel (grid shapes with Q_v (Q_u + 1) / 2 = 32-48 ran 5-18 % slower w-first)
+    c->lpack.mom_wfirst = spec->nq[1] * ((spec->nq[0] + 1) / 2) >= 64;
     if (const char* v = opt.get("P2S_LARGE_MOMW")) c->lpack.mom_wfirst = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_MOMT")) c->lpack.mom_tiled = v[0] != '0';
     if (const char* v = opt.get("P2S_LARGE_MOMG")) c->lpack.mom_grouped = v[0] != '0';

@@ -19,8 +19,9 @@ namespace reg {
 
 const std::vector<LargeEntry>& large_registry() {
   static const std::vector<LargeEntry> reg = {
-      // C5; k1 chunks of 4 (79 KB, 2 CTAs/SM): moments 0.71 ms vs 0.97 ms with chunks of 8
-      make_large<LShape<16, 16, 16, 36, 36, 36, 4, kPPP, kDDD>>(),
+      // C5; moment chunks of 8 (w-first tiled kernel: 169 KB, one CTA of 352 threads per SM,
+      // 0.94 us per element vs 1.05 with chunks of 4; the round-1 u-first kernel preferred 4)
+      make_large<LShape<16, 16, 16, 36, 36, 36, 8, kPPP, kDDD>>(),
       make_large<LShape<5, 4, 3, 8, 8, 6, 4, kPPP, kDDD>>(),         // test shape
       make_large<LShape<5, 4, 3, 8, 8, 6, 4, kCPPP, kCDDD>>(),       // test shape, conforming
   };

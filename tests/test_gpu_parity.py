@@ -290,6 +290,7 @@ def test_large_order_path_small_shape(n_comp):
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_MOMG": "1", "P2S_LARGE_MOMW": "0"},   # grouped v / w moment passes
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_MOMT": "1", "P2S_LARGE_MOMW": "0"},   # register-tiled moment passes (u first)
     {"P2S_XCHUNK_MB": "1", "P2S_LARGE_MOMW": "0"},          # u-first moment kernel, one row per thread
+    {"P2S_XCHUNK_MB": "1", "P2S_LARGE_MOMW": "1"},          # w-first register-tiled moment kernel
 ])
 def test_large_order_path_chunk_schedules(env, monkeypatch):
     # the chunked v/w -> u pipeline over many X chunks (double buffer reuse,

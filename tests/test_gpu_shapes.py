@@ -42,3 +42,29 @@ def test_shape_grid_matches_oracle(case):
         for e in range(n):
             ok, msg, _ = blocks_close(Mg[e], Mo[e], nc, Nt)
             assert ok, f"{name} element {e}: {msg} ({ctx.kernel_path})"
+
+
+@pytest.mark.parametrize("case", shape_grid.ALL, ids=shape_grid.shape_id)
+def test_large_family_moment_kernels_agree(case):
+    # both moment kernels of the large-order family (w-first register tiles, the default
+    # where its first pass is wide enough, and the u-first kernel) on every grid shape
+    # of the family: same moments to rounding (the sums run in a different order)
+    nc, order, kinds, nq, basis = case
+    res = []
+    for w in ("0", "1"):
+        ctx = capi.Context(nc, order, kinds, nq, basis=basis, options={"P2S_LARGE_MOMW": w})
+        if not ctx.kernel_path.startswith("large-order"):
+            ctx.close()
+            pytest.skip("not a large-order shape")
+        n = 2
+        st = torch.cuda.current_stream().cuda_stream
+        a = torch.empty((n, ctx.alpha_per_elem), dtype=torch.float64, device="cuda")
+        ctx.alpha_generate(O.ALPHA_SINE, 0.5, 3.0, 29 + sum(order), 0, n, a, st)
+        I = torch.zeros((n, ctx.moments_per_elem), dtype=torch.float64, device="cuda")
+        ctx.moments(a, I, n, st)
+        torch.cuda.synchronize()
+        res.append(I.cpu().numpy())
+        ctx.close()
+    scale = np.abs(res[0]).max()
+    assert scale > 0 and np.isfinite(res[1]).all()
+    assert np.abs(res[0] - res[1]).max() <= 1e-12 * scale
