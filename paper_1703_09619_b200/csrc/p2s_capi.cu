@@ -674,7 +674,9 @@ const char* p2s_kernel_path(const p2s_ctx* c) {
   if (!c) return "";
   static thread_local std::string path;
   if (c->large) {
-    path = "large-order: large_moments_kernel + large_w_kernel + large_v_kernel + large_u_kernel";
+    path = std::string("large-order: ") +
+           (c->lpack.mom_wfirst ? "large_moments_w_kernel" : "large_moments_kernel") +
+           " + large_w_kernel + large_v_kernel + large_u_kernel";
   } else if (c->fused) {
     path = std::string("fused: fill_fused_kernel (moments + contraction; ") + c->fused->desc + ")";
   } else if (c->v2 && !c->force_generic) {

@@ -918,6 +918,7 @@ __device__ __forceinline__ void large_moments_w_term(const LMomParams<Ls>& p, co
     }
     if constexpr (kStage) {
       __syncthreads();
+#pragma unroll 4
       for (int i = threadIdx.x; i < KU * KV * KC; i += NT) {
         const int e = i / KC, j = i - e * KC;
         if (j < kc) Iout[e * KW + k0 + j] = sm[i];
