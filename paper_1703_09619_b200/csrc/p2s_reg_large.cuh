@@ -116,6 +116,7 @@ cudaError_t launch_large_moments(const double* alpha, double* I, int64_t n_units
                                    LMomW<Ls>::SMEM, st>>>(p);
       return cudaGetLastError();
     }
+#ifndef P2S_LEAN  // measurement variants (u-first tiles, grouped v / w items): ahead-of-time builds only
   if constexpr (LMomT<Ls>::FITS)
     if (pk.mom_tiled) {
       if ((e = kernel_prepare(large_moments_t_kernel<Ls>, LMomT<Ls>::SMEM, LMomT<Ls>::NT)) != cudaSuccess) return e;
@@ -128,6 +129,7 @@ cudaError_t launch_large_moments(const double* alpha, double* I, int64_t n_units
       large_moments_g_kernel<Ls><<<grid, LMomG<Ls>::NT, LMomG<Ls>::SMEM, st>>>(p);
       return cudaGetLastError();
     }
+#endif
   large_moments_kernel<Ls><<<grid, P2S_LARGE_MOM_THREADS, Ls::MOM_SMEM, st>>>(p);
   return cudaGetLastError();
 }
