@@ -1,9 +1,13 @@
 // p2s_large.cuh -- large-order path (C5: N = 16, K = 31 / 29, 36^3 points),
 // where one element's moment block (433 KB) and intermediates do not fit a
 // CTA's shared memory.  Kernels per chunk of elements:
-//   large_moments_kernel  I_s[k1][k2][k3], one CTA per (unit, term, k1 chunk)
+//   large_moments_w_kernel  I_s[k1][k2][k3], one CTA per (unit, term, k3 chunk):
+//                         w-first register-tiled passes (default; section "w-first
+//                         tiled moments" below)
+//   large_moments_kernel  the round-1 kernel, one CTA per (unit, term, k1 chunk)
 //                         (three even/odd-folded 1-D passes as in
-//                         p2s_moments_v2.cuh, pass u restricted to the chunk)
+//                         p2s_moments_v2.cuh, pass u restricted to the chunk); used
+//                         where the w-first kernel's first pass is too narrow
 //   large_w_kernel,       X_s[k1][tri(n1,n2)][p1][p2] =
 //   large_v_kernel        sum_k2 Cv[n1 n2 k2] sum_k3 Cw[p1 p2 k3] I_s[k1][k2][k3]
 //                         (w step into Z, then v step; symmetric v kinds, so

@@ -1,5 +1,5 @@
-// p2s_reg_large.cu -- large-order registry (C5: large_moments_kernel, large_w_kernel, large_v_kernel,
-// large_u_kernel).
+// p2s_reg_large.cu -- large-order registry (C5: large_moments_w_kernel, large_w_kernel, large_v_kernel,
+// large_u_xs_kernel).
 #include <cuda_runtime.h>
 
 #include <algorithm>
